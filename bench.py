@@ -1,0 +1,306 @@
+#!/usr/bin/env python
+"""Benchmark: parameter vectors per second of trace(E X(v)) on B200 (BASELINE.json metric).
+
+python bench.py [--gpus N --steps K --warmup W] [--config c2] [--impl reference]
+
+A step = one lyap_trace_batch over the configuration's whole parameter grid (this rank's shard),
+followed by the all-gather of traces and the argmin.  Inputs are synthetic and
+seeded (workloads.make), resident in HBM before the timed region.  Multi-GPU: one process per GPU
+(torchrun), the grid is split into chunks of consecutive grid points dealt round-robin to ranks
+(strong scaling: the grid is fixed), NCCL all-gather of traces, max-over-ranks device time.
+
+Only the `cpu_baseline` leg and `--impl reference` execute oracle/ (the CPU oracle); the timed
+product path is liblyapgpu.so only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "parameter vectors/sec (trace(EX(v)))"
+UNIT = "v/s"
+FP64_PEAK_TFLOPS = 37.0   # measured: DMMA m8n8k4 burst, profiles/r01_fp64_peaks.md (MEASURED_PEAKS.json has no FP64)
+CHUNK = 64                # consecutive grid points per shard chunk
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=os.environ.get("BENCH_CONFIG", "c2"))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--max-dim", type=int, default=0)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------ clocks
+class Clocks:
+    """nvidia-smi sampling during the timed region (the B200_PROFILING.md clocks line)."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.rows, self.proc = [], None
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], [], set()
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, r[3:7]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------ CPU oracle timing
+_WK = {}
+
+
+def _oracle_worker_init(name):
+    from threadpoolctl import threadpool_limits
+    threadpool_limits(1)
+    import workloads
+    _WK["W"] = workloads.make(name)
+
+
+def _oracle_one(idx):
+    import oracle
+    W = _WK["W"]
+    return oracle.trace_EX(W.A0, W.Bl, W.Br, W.Q, W.E, W.V[idx])
+
+
+def oracle_rate(name: str, seconds: float, seed: int = 0):
+    """Time the CPU oracle (as it stands) on a bounded sample: C single-threaded worker processes."""
+    import multiprocessing as mp
+
+    import workloads
+    W = workloads.make(name)
+    cores = os.cpu_count() or 1
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(cores, initializer=_oracle_worker_init, initargs=(name,)) as pool:
+        pool.map(_oracle_one, [W.corner_indices()[0]] * cores)  # warm workers, size the sample
+        t = time.perf_counter()
+        pool.map(_oracle_one, [W.corner_indices()[-1]] * cores)
+        t1 = time.perf_counter() - t
+        count = int(max(cores, min(W.nv, cores * max(1, int(seconds / max(t1, 1e-3))))))
+        idx = W.sample_indices(count, seed=seed)
+        t = time.perf_counter()
+        pool.map(_oracle_one, [int(i) for i in idx], chunksize=1)
+        el = time.perf_counter() - t
+    return len(idx) / el, cores, len(idx), el
+
+
+# ------------------------------------------------------------------------------ helpers
+def shard_indices(nv: int, rank: int, world: int) -> np.ndarray:
+    chunks = [np.arange(s, min(nv, s + CHUNK)) for s in range(0, nv, CHUNK)]
+    mine = chunks[rank::world]
+    return np.concatenate(mine) if mine else np.zeros(0, dtype=np.int64)
+
+
+def emit(obj):
+    print(json.dumps(obj), flush=True)
+
+
+def config_dict(W, args, world, extra=None):
+    d = {"workload": W.name, "n": W.n, "k": W.k, "nv": W.nv, "grid": list(W.grid_shape),
+         "seed": W.meta.get("seed"), "parallelism": f"v-grid sharded over {world} GPU(s)",
+         "l2": "working set (Krylov bases, > 1 GB) exceeds the 126 MB L2; no flush needed"}
+    if extra:
+        d.update(extra)
+    return d
+
+
+# ------------------------------------------------------------------------------ reference arm
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import workloads
+    W = workloads.make(args.config)
+    per_step = max(2.0, min(args.cpu_seconds, 20.0))
+    for _ in range(args.warmup):
+        oracle_rate(args.config, per_step / 4, seed=1)
+    rates = []
+    t_all = time.perf_counter()
+    for s in range(args.steps):
+        r, cores, cnt, el = oracle_rate(args.config, per_step, seed=2 + s)
+        rates.append((r, cores, cnt, el))
+    wall = time.perf_counter() - t_all
+    value = statistics.median([r[0] for r in rates])
+    cores, cnt = rates[0][1], rates[0][2]
+    emit({"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+          "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / max(args.steps, 1),
+          "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+          "data": "synthetic (seeded workloads.make)",
+          "config": config_dict(W, args, world, {"sample_per_step": cnt}),
+          "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                           "sample": f"{cnt} grid points per step (2^k corners + centre + seeded uniform), "
+                                     "blocked Bartels-Stewart per v, one process per core, 1 BLAS thread"},
+          "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+
+
+# ------------------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import workloads
+    from paper_2312_08201_b200 import Problem
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    W = workloads.make(args.config)
+    idx = shard_indices(W.nv, rank, world)
+    P = Problem(W.A0, W.Bl, W.Br, W.Q, W.E, profile=True, device=local, batch=args.batch, max_dim=args.max_dim)
+    setup_ms = P.info["setup_ms"]
+    Vd = torch.tensor(W.V[idx], device=dev)
+    nmax = max(len(shard_indices(W.nv, r, world)) for r in range(world))
+    gathered = torch.empty(world * nmax, dtype=torch.float64, device=dev)
+    all_idx = torch.tensor(np.concatenate([np.pad(shard_indices(W.nv, r, world),
+                                                  (0, nmax - len(shard_indices(W.nv, r, world))),
+                                                  constant_values=-1) for r in range(world)]), device=dev)
+    valid = all_idx >= 0
+
+    def step():
+        tau = P.trace_batch(Vd)
+        if world > 1:
+            buf = torch.full((nmax,), float("inf"), dtype=torch.float64, device=dev)
+            buf[: tau.numel()] = tau
+            dist.all_gather_into_tensor(gathered, buf)
+            full = torch.empty(W.nv, dtype=torch.float64, device=dev)
+            full[all_idx[valid]] = gathered[valid]
+        else:
+            full = tau
+        return full, torch.argmin(full)  # first index on ties
+
+    for _ in range(args.warmup):
+        full, am = step()
+    torch.cuda.synchronize()
+    P.reset_stats()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = Clocks(local)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        full, am = step()
+    ev1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    ms = ev0.elapsed_time(ev1)
+    tmax = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    ms_max = float(tmax.item())
+    st = P.stats
+    value = W.nv * args.steps / (ms_max * 1e-3)
+    argmin = int(am.item())
+
+    # e2e: host buffers through the public API (H2D of V and D2H of traces inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        Vh = np.ascontiguousarray(W.V[idx])
+        P.trace_batch(Vh)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t = time.perf_counter()
+        for _ in range(args.steps):
+            tau_h = P.trace_batch(Vh)
+        el = torch.tensor([time.perf_counter() - t], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        e2e = {"value": W.nv * args.steps / float(el.item()), "unit": UNIT,
+               "h2d_bytes_per_step": int(Vh.nbytes), "d2h_bytes_per_step": int(len(idx) * (8 + 4 + 4 + 8))}
+
+    avg_k1_ms = st["k1_ms"] / max(st["k1_launches"], 1)
+    flops_per_launch = st["k1_flops"] / max(st["k1_launches"], 1)
+    achieved = flops_per_launch / (avg_k1_ms * 1e-3) / 1e12 if avg_k1_ms > 0 else 0.0
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", f"k1_traffic_{args.config}.json")
+    if os.path.exists(tfile):
+        traffic = json.load(open(tfile)).get("bytes_per_launch")
+    roof = {"bound": "fp64", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+            "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+            "kernel": "k1_dgemm (Cauchy-fused T-apply GEMM, DMMA)",
+            "peak_source": "measured DMMA mma.sync.m8n8k4.f64 microbench (profiles/r01_fp64_peaks.md); "
+                           "MEASURED_PEAKS.json carries no FP64 figure",
+            "avg_launch_ms": avg_k1_ms, "launches": st["k1_launches"],
+            "k1_share_of_step": st["k1_ms"] / ms if ms > 0 else None}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r, cores, cnt, el = oracle_rate(args.config, args.cpu_seconds)
+        cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{cnt} of {W.nv} grid points (corners + centre + seeded uniform) in {el:.1f} s, "
+                         "blocked Bartels-Stewart per v, one process per core, 1 BLAS thread"}
+    if rank == 0:
+        emit({"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+              "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+              "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded workloads.make)",
+              "config": config_dict(W, args, world, {"batch": P.info["batch"], "max_dim": P.info["max_dim"],
+                                                     "setup_ms": setup_ms, "argmin_flat_index": argmin,
+                                                     "applies_per_v": st["k1_vectors"] / (W.nv * args.steps / world)}),
+              "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+              "gpu_launches": st["kernel_launches"]})
+    P.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

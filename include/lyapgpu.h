@@ -1,0 +1,144 @@
+/* lyapgpu.h — C-ABI of the B200 trace(E X(v)) sweep engine (arXiv 2312.08201).
+ *
+ * The operation (eqs. (Ljap jdba 1), (eq:formA)): for every parameter vector
+ * v in R^k of a batch V,
+ *
+ *     A(v) = A0 - Bl diag(v) Br^T,     A(v) X + X A(v)^T = -Q,     tau(v) = trace(E X(v)).
+ *
+ * How: lyap_setup factors the seed once, A0 = S Lambda S^{-1} (the complex
+ * eigendecomposition of PAPER.md:183, computed on the device from the real LAPACK-style
+ * packing), and moves Q, E, Bl, Br into that basis (the offline column of Table 1,
+ * PAPER.md:493-506).  lyap_trace_batch then solves, per v, the symmetric nk-dimensional form
+ * of the SMW capacitance system eq. (SMW_linearsystem) (reduction in
+ * DESIGN.md §2.2) with a batched, right-preconditioned Krylov method on the GPU
+ * (preconditioner = the v-dependent exact diagonal blocks of eq. (prec))
+ * and returns tau(v) = trace(E X0) + 2 sum G_tj H_jt.
+ *
+ * Conventions (all calls):
+ *   - every matrix is float64, ROW-MAJOR (C order, the same as NumPy / torch);
+ *   - host pointers unless a flag says "on device";
+ *   - every call returns an lyap_status; on failure lyap_last_error(ctx) (or
+ *     lyap_last_error(NULL) when no ctx exists yet) gives a message;
+ *   - a ctx is not re-entrant: serialise calls per ctx.  Several ctx per device are fine.
+ *   - there is no CPU fallback: with no CUDA device every call returns LYAP_ENODEV.
+ */
+#ifndef LYAPGPU_H
+#define LYAPGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct lyap_ctx lyap_ctx; /* opaque; owns all device memory of one seed */
+
+typedef enum {
+  LYAP_OK = 0,
+  LYAP_EINVAL = 1,     /* bad dims / null pointer / k > LYAP_KMAX / Q not symmetric (rel 1e-13) */
+  LYAP_ENOMEM = 2,     /* device allocation failed */
+  LYAP_ECUDA = 3,      /* CUDA / cuBLAS / cuSOLVER error */
+  LYAP_EEIG = 4,       /* eig(A0) failed, pairing not conjugate, or cond(S) > opts.max_cond_S */
+  LYAP_ESINGULAR = 5,  /* min|lambda_i + lambda_j| <= 1e-12 max|lambda|: seed Lyapunov operator
+                          singular (the Cauchy matrix needs lambda_i + lambda_j != 0) */
+  LYAP_EPARTIAL = 6,   /* trace_batch: some v not converged / non-finite; see status[] */
+  LYAP_ENODEV = 7      /* no CUDA device (the library has no CPU path) */
+} lyap_status;
+
+/* per-v status codes written to status[i] */
+enum { LYAP_V_OK = 0, LYAP_V_NOCONV = 1, LYAP_V_NONFINITE = 2 };
+
+#define LYAP_KMAX 8
+
+typedef struct {
+  double tol;          /* stop when ||g0 - C(v) g|| <= tol ||g0|| (true residual of the nk
+                          capacitance system, reading R14). default 1e-12 */
+  int32_t max_dim;     /* Krylov restart length m_max; 0 = auto (default) */
+  int32_t max_restarts;/* restart cycles before status LYAP_V_NOCONV (default 30) */
+  int32_t batch;       /* parameter vectors in flight (slots); 0 = auto (default) */
+  int32_t warm_start;  /* 1 (default): a slot starts v from the solution of its previous v */
+  double max_cond_S;   /* setup fails with LYAP_EEIG above this 1-norm condition of S (1e8) */
+  int32_t device;      /* CUDA device ordinal (default: current device) */
+  int32_t profile;     /* 1: time every K1 GEMM launch with CUDA events (lyap_get_stats) */
+} lyap_opts;
+
+typedef struct {
+  int64_t n, k;
+  int64_t npad;        /* n rounded up to the K1 tile; vectors are k x npad float64 */
+  int64_t n_pairs;     /* complex-conjugate eigenpairs of A0 (real eigenvalues: n - 2 n_pairs) */
+  double t0;           /* trace(E X0), X0 the seed solution (eq. seedLE) */
+  double cond_S;       /* ||S_r||_1 ||S_r^{-1}||_1 of the real eigenvector basis */
+  double min_lam_sum;  /* min_{i,j} |lambda_i + lambda_j| */
+  double max_abs_lam;
+  double setup_ms;     /* device time of lyap_setup */
+  int32_t batch, max_dim;
+} lyap_info;
+
+typedef struct {
+  int64_t k1_launches;     /* K1 (Cauchy-fused T-apply GEMM) launches since the last reset */
+  int64_t k1_vectors;      /* parameter-vector columns applied (active slots only) */
+  double k1_ms;            /* summed CUDA-event time of the K1 GEMM launches (profile=1) */
+  double k1_flops;         /* algorithmic flops of those launches: 2 n^2 k^2 per vector */
+  int64_t iterations;      /* engine iterations (one batched T-apply each) */
+  int64_t kernel_launches; /* all kernels this library launched */
+  double batch_ms;         /* device time of the last lyap_trace_batch */
+} lyap_stats;
+
+/* Fills *opts with the defaults above. */
+void lyap_default_opts(lyap_opts* opts);
+
+/* Offline stage (Table 1 left column).  Copies every input; the caller may free
+ * them on return.  A0: n x n, Bl, Br: n x k, Q: n x n symmetric, E: n x n (symmetrised on input,
+ * trace(E X) = trace(((E + E^T)/2) X) since X is symmetric).  opts may be NULL.
+ * Errors: LYAP_EINVAL, LYAP_ENOMEM, LYAP_ECUDA, LYAP_EEIG, LYAP_ESINGULAR, LYAP_ENODEV.
+ * On success *out owns O(n^2 + n k^2 + batch * m_max * n k) device memory. */
+int lyap_setup(int64_t n, int64_t k, const double* A0, const double* Bl, const double* Br,
+               const double* Q, const double* E, const lyap_opts* opts, lyap_ctx** out);
+
+/* Online stage: traces[i] = trace(E X(V[i,:])) for the nv rows of V (nv x k, row-major).
+ * v_on_device = 0: V, traces, status are host pointers; the call is synchronous.
+ * v_on_device = 1: all three are device pointers (e.g. torch data_ptr()) and the work is
+ *   ordered on cuda_stream (cudaStream_t, NULL = legacy default stream); the call still returns
+ *   after the batch completes (the engine polls a device counter).
+ * status (nullable): per-v LYAP_V_* codes.  A component v_t == 0 is allowed and means column t
+ * is absent ("without loss of generality"); negative v are allowed.
+ * Returns LYAP_OK, or LYAP_EPARTIAL if any status[i] != 0 (traces[i] is still the last iterate,
+ * NaN if non-finite). */
+int lyap_trace_batch(lyap_ctx* ctx, int64_t nv, const double* V, double* traces, int32_t* status,
+                     int v_on_device, void* cuda_stream);
+
+/* As lyap_trace_batch, with per-v diagnostics (each nullable, same host/device placement as V):
+ * applies[i] = T-applications spent on v (Krylov iterations + verifications),
+ * resid[i] = final true relative residual ||g0 - C(v) g|| / ||g0||. */
+int lyap_trace_batch_ex(lyap_ctx* ctx, int64_t nv, const double* V, double* traces,
+                        int32_t* status, int32_t* applies, double* resid, int v_on_device,
+                        void* cuda_stream);
+
+int lyap_get_info(const lyap_ctx* ctx, lyap_info* info);
+int lyap_get_stats(const lyap_ctx* ctx, lyap_stats* stats);
+int lyap_reset_stats(lyap_ctx* ctx);
+
+/* K1 alone, for kernel tests and the roofline bench: Y = C(sigma) X = sigma o X - T X for nvec
+ * folded real vectors (each k x npad, row-major; the layout of DESIGN.md §3).  X, Y, sigma are
+ * DEVICE pointers; sigma is nvec x k (NULL: sigma = 0, i.e. Y = -T X).  Ordered on cuda_stream. */
+int lyap_apply_C(lyap_ctx* ctx, int64_t nvec, const double* X, const double* sigma, double* Y,
+                 void* cuda_stream);
+
+/* Host copies of the folded seed state, for tests (each pointer nullable; sizes from lyap_info):
+ *   lam: n x 2 (re, im) eigenvalue per folded coordinate (pair p: coords 2p, 2p+1 both hold the
+ *        eigenvalue with positive imaginary part);  bhr, btl: n x k folded  B^r = S^T Br and
+ *        B~l = S^{-1} Bl;  F: (n_pairs + n_real) x k x k x 2 complex T_d blocks;
+ *   g0, hf: k x npad folded right-hand side and trace weights. */
+int lyap_export_state(const lyap_ctx* ctx, double* lam, double* bhr, double* btl, double* F,
+                      double* g0, double* hf);
+
+void lyap_destroy(lyap_ctx* ctx);
+
+/* Message of the last failure on this ctx; lyap_last_error(NULL) gives the last failure of the
+ * calling thread when no ctx was produced (e.g. a failed lyap_setup).  Never NULL. */
+const char* lyap_last_error(const lyap_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LYAPGPU_H */

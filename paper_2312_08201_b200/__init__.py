@@ -1,0 +1,168 @@
+"""B200-native engine for trace(E X(v)) over batches of parameter vectors (arXiv 2312.08201).
+
+    prob = Problem(A0, Bl, Br, Q, E)          # lyap_setup   (offline stage)
+    tau = prob.trace_batch(V)                 # lyap_trace_batch (online stage)
+
+A thin ctypes binding over the C-ABI in include/lyapgpu.h (same names; argument marshalling
+only — every step runs in the CUDA library liblyapgpu.so).  V may be a NumPy array (host path,
+copies inside the call) or a CUDA torch tensor (device path, no copies).  There is no CPU
+fallback: without a CUDA device lyap_setup returns LYAP_ENODEV and Problem raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from ._lib import (EXPORTED, LYAP_EPARTIAL, LYAP_KMAX, LYAP_OK, Info, LyapError, Opts, Stats, lib)
+
+__all__ = ["Problem", "LyapError", "lib", "EXPORTED", "LYAP_KMAX", "default_opts"]
+
+
+def default_opts() -> Opts:
+    o = Opts()
+    lib.lyap_default_opts(C.byref(o))
+    return o
+
+
+def _f64(a, shape=None) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    if shape is not None and a.shape != shape:
+        raise ValueError(f"expected shape {shape}, got {a.shape}")
+    return a
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+class Problem:
+    """One seed A0 with its factors (lyap_setup); trace_batch evaluates trace(E X(v))."""
+
+    def __init__(self, A0, Bl, Br, Q, E, *, tol: float = 1e-12, max_dim: int = 0, max_restarts: int = 30,
+                 batch: int = 0, warm_start: bool = True, max_cond_S: float = 1e8, device: int = -1,
+                 profile: bool = False):
+        A0 = _f64(A0)
+        n = A0.shape[0]
+        Bl = _f64(Bl)
+        if Bl.ndim == 1:
+            Bl = Bl[:, None]
+        k = Bl.shape[1]
+        Br = _f64(Br).reshape(n, k)
+        Bl = Bl.reshape(n, k)
+        Q, E = _f64(Q, (n, n)), _f64(E, (n, n))
+        o = default_opts()
+        o.tol, o.max_dim, o.max_restarts, o.batch = tol, max_dim, max_restarts, batch
+        o.warm_start, o.max_cond_S, o.device, o.profile = int(warm_start), max_cond_S, device, int(profile)
+        self._ctx = C.c_void_p()
+        rc = lib.lyap_setup(n, k, _dp(A0), _dp(Bl), _dp(Br), _dp(Q), _dp(E), C.byref(o), C.byref(self._ctx))
+        if rc != LYAP_OK:
+            raise LyapError(rc, lib.lyap_last_error(None).decode())
+        self.n, self.k = n, k
+
+    # ------------------------------------------------------------------ queries
+    @property
+    def info(self) -> dict:
+        i = Info()
+        self._check(lib.lyap_get_info(self._ctx, C.byref(i)))
+        return {f: getattr(i, f) for f, _ in Info._fields_}
+
+    @property
+    def stats(self) -> dict:
+        s = Stats()
+        self._check(lib.lyap_get_stats(self._ctx, C.byref(s)))
+        return {f: getattr(s, f) for f, _ in Stats._fields_}
+
+    def reset_stats(self):
+        self._check(lib.lyap_reset_stats(self._ctx))
+
+    def _check(self, rc):
+        if rc != LYAP_OK:
+            raise LyapError(rc, lib.lyap_last_error(self._ctx).decode())
+
+    # ------------------------------------------------------------------ online stage
+    def trace_batch(self, V, *, return_diagnostics: bool = False, allow_partial: bool = False, stream=None):
+        """tau[i] = trace(E X(V[i])).  V: (nv, k) NumPy array (host path) or CUDA torch tensor.
+
+        With return_diagnostics: (tau, status, applies, resid).  A non-zero status raises
+        LyapError(LYAP_EPARTIAL) unless allow_partial."""
+        try:
+            import torch
+            is_dev = isinstance(V, torch.Tensor) and V.is_cuda
+        except ImportError:  # pragma: no cover
+            is_dev = False
+        if is_dev:
+            return self._trace_batch_device(V, return_diagnostics, allow_partial, stream)
+        V = _f64(V)
+        if V.ndim == 1:
+            V = V.reshape(-1, self.k)
+        nv = V.shape[0]
+        if V.shape[1] != self.k:
+            raise ValueError(f"V must be (nv, {self.k})")
+        tau = np.empty(nv)
+        st = np.empty(nv, dtype=np.int32)
+        ap = np.empty(nv, dtype=np.int32)
+        rs = np.empty(nv)
+        rc = lib.lyap_trace_batch_ex(self._ctx, nv, V.ctypes.data, tau.ctypes.data, st.ctypes.data,
+                                     ap.ctypes.data, rs.ctypes.data, 0, None)
+        if rc != LYAP_OK and not (rc == LYAP_EPARTIAL and allow_partial):
+            self._check(rc)
+        return (tau, st, ap, rs) if return_diagnostics else tau
+
+    def _trace_batch_device(self, V, return_diagnostics, allow_partial, stream):
+        import torch
+        V = V.to(torch.float64).contiguous()
+        nv = V.shape[0]
+        dev = V.device
+        tau = torch.empty(nv, dtype=torch.float64, device=dev)
+        st = torch.empty(nv, dtype=torch.int32, device=dev)
+        ap = torch.empty(nv, dtype=torch.int32, device=dev)
+        rs = torch.empty(nv, dtype=torch.float64, device=dev)
+        s = stream if stream is not None else torch.cuda.current_stream(dev)
+        rc = lib.lyap_trace_batch_ex(self._ctx, nv, V.data_ptr(), tau.data_ptr(), st.data_ptr(), ap.data_ptr(),
+                                     rs.data_ptr(), 1, C.c_void_p(s.cuda_stream))
+        if rc != LYAP_OK and not (rc == LYAP_EPARTIAL and allow_partial):
+            self._check(rc)
+        return (tau, st, ap, rs) if return_diagnostics else tau
+
+    def apply_C(self, X, sigma=None, stream=None):
+        """K1 alone: Y = sigma o X - T X for folded vectors X (CUDA tensor, (nvec, k, npad))."""
+        import torch
+        X = X.to(torch.float64).contiguous()
+        Y = torch.empty_like(X)
+        sp = None
+        if sigma is not None:
+            sigma = sigma.to(torch.float64).contiguous()
+            sp = sigma.data_ptr()
+        s = stream if stream is not None else torch.cuda.current_stream(X.device)
+        self._check(lib.lyap_apply_C(self._ctx, X.shape[0], X.data_ptr(), sp, Y.data_ptr(),
+                                     C.c_void_p(s.cuda_stream)))
+        return Y
+
+    def export_state(self) -> dict:
+        i = self.info
+        n, k, npad, npairs = i["n"], i["k"], i["npad"], i["n_pairs"]
+        nrep = n - npairs
+        out = {"lam": np.empty((n, 2)), "bhr": np.empty((n, k)), "btl": np.empty((n, k)),
+               "F": np.empty((nrep, k, k, 2)), "g0": np.empty((k, npad)), "hf": np.empty((k, npad))}
+        self._check(lib.lyap_export_state(self._ctx, *(out[x].ctypes.data for x in
+                                                       ("lam", "bhr", "btl", "F", "g0", "hf"))))
+        out.update(t0=i["t0"], n_pairs=npairs, npad=npad)
+        return out
+
+    def close(self):
+        if getattr(self, "_ctx", None) and self._ctx.value:
+            lib.lyap_destroy(self._ctx)
+            self._ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()

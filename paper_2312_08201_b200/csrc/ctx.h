@@ -1,0 +1,65 @@
+// Internal state of one lyap_ctx (one seed A0).  Not part of the C-ABI.
+#pragma once
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <string>
+
+#include "../../include/lyapgpu.h"
+
+namespace lyap {
+
+// Folded seed state that the per-v engine reads.  Folded real coordinates:
+// eigen index == coordinate; a conjugate pair occupies coords (2r, 2r+1) = (Re, Im) of the
+// representative with Im(lambda) > 0; real eigenvalues follow the pairs, one coord each;
+// coords n..npad-1 are zero padding.  Reps: r < npairs are pairs (coord 2r), r >= npairs are real
+// (coord r + npairs).
+struct Seed {
+  int64_t n = 0, k = 0, npad = 0, npairs = 0, nrep = 0;
+  double* lam = nullptr;  // npad x 2: eigenvalue (re, im) of the rep owning the coordinate
+  double* bhr = nullptr;  // npad x k: folded B^r = S^T Br        [coord][s]
+  double* btl = nullptr;  // npad x k: folded B~l = S^{-1} Bl     [coord][t]
+  double* F = nullptr;    // nrep x k x k complex (re, im):  T_d block of rep j, F_j[s][t]
+  double* g0 = nullptr;   // k x npad folded right-hand side G0 = B^r^T X~0
+  double* hf = nullptr;   // k x npad folded trace weights (tau = t0 + 2 <g, hf>)
+  double* Lf = nullptr;   // npad x npad folded Cauchy matrix (K1's A operand), row-major
+  double t0 = 0.0;
+};
+
+// Batched Krylov engine buffers (slot-major).
+struct Engine {
+  int b = 0;        // slots
+  int mmax = 0;     // restart length
+  int64_t L = 0;    // vector length k * npad
+  int64_t ncol = 0; // K1 GEMM columns, b*k*k rounded up to the N tile
+  int nchunk = 0;   // chunks of the vector length for the reductions
+  double *Bop = nullptr, *U = nullptr;            // npad x ncol
+  double *Xin = nullptr, *X = nullptr;            // b x L
+  double* Qb = nullptr;                           // b x (mmax+1) x L  (unnormalised basis)
+  double* Minv = nullptr;                         // b x nrep x k x k x 2
+  double *sigma = nullptr, *mask = nullptr;       // b x k
+  double *eta = nullptr, *H = nullptr, *cs = nullptr, *sn = nullptr, *e = nullptr, *y = nullptr;
+  double *bnorm = nullptr;                        // b
+  double *part = nullptr;                         // b x (mmax+2) x nchunk
+  double *part3 = nullptr;                        // b x nchunk x 3
+  int *phase = nullptr, *m = nullptr, *vidx = nullptr, *applies = nullptr, *restarts = nullptr;
+  int* ctrl = nullptr;                            // [0]=next v, [1]=done count, [2]=active slots
+  int* h_ctrl = nullptr;                          // pinned mirror
+};
+
+}  // namespace lyap
+
+struct lyap_ctx {
+  int device = 0;
+  lyap_opts opts{};
+  lyap_info info{};
+  lyap_stats stats{};
+  std::string err;
+  cudaStream_t stream = nullptr;  // library-owned stream (used when the caller passes NULL)
+  cublasHandle_t cublas = nullptr;
+  cusolverDnHandle_t cusolver = nullptr;
+  lyap::Seed seed;
+  lyap::Engine eng;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};

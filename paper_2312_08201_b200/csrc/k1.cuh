@@ -1,0 +1,259 @@
+// K1 — the Cauchy-fused T-apply: for a batch of folded vectors X (one per slot)
+//
+//   U_{(s,t),j} = sum_i L_ij (B^r_is X_ti)                     (dense Cauchy coupling, eqs. (N2M1),
+//                                                                (N1M2))
+//   (T X)_sj    = sum_t B~l_jt U_{(s,t),j} + sum_t F_j[s,t] X_tj  (T_d: eq. (N1M1) and the (2,2)
+//                                                                block)
+//   out         = sigma_s X_sj - (T X)_sj                        (C(v) = Delta(v) - T)
+//
+// in real pair-folded coordinates: U = Lf * Bop is one real FP64 GEMM (M = K = npad, N = slots*k^2)
+// on the DMMA tensor pipe (mma.sync.m8n8k4.f64), with a prologue kernel that builds the B operand
+// (B^r o X outer products) and an epilogue kernel that contracts over t and adds T_d.
+#pragma once
+#include "common.cuh"
+
+namespace lyap {
+
+constexpr int K1_TILE_C = 32;  // coordinates per prologue / epilogue tile
+
+template <int K>
+struct K1Tile {
+  static constexpr int TS = (64 / (K * K)) > 0 ? (64 / (K * K)) : 1;  // slots per tile
+  static constexpr int NC = TS * K * K;                                // GEMM columns per tile
+};
+
+// Per-launch arguments of the prologue / epilogue (engine mode or standalone apply mode).
+struct K1Args {
+  const double* Xin;   // nslot x L  (input vectors, slot-major)
+  int64_t L;           // k * npad
+  int nslot;
+  int mode;            // 0 = apply (Yout = sigma o X - T X), 1 = engine
+  const double* sigma; // nslot x k (apply mode: may be null -> 0)
+  const double* mask;  // nslot x k (engine mode) 1 = v_t != 0
+  const int* phase;    // engine: slot phases
+  const int* m;        // engine: current Krylov index per slot
+  double* Qb;          // engine: basis (nslot x (mmax+1) x L)
+  int64_t qstride;     // (mmax+1) * L
+  double* Yout;        // apply mode output (nslot x L)
+  const int* nactive;  // engine: skip everything if *nactive == 0 (may be null)
+};
+
+enum : int { PH_FREE = 0, PH_IDLE = 1, PH_VERIFY = 2, PH_ITER = 3, PH_XUPD = 4, PH_NEW = 5 };
+
+// ------------------------------------------------------------------------------------------
+// K1a prologue: Bop[i][(slot*k + s)*k + t] = folded (B^r_is * X_ti)   (the Hadamard B operand)
+template <int K>
+__global__ void __launch_bounds__(256) k1_gen(K1Args a, const double* __restrict__ bhr, int npad,
+                                               int two_np, double* __restrict__ Bop, int64_t ncol) {
+  if (a.nactive && *a.nactive == 0) return;
+  constexpr int TS = K1Tile<K>::TS, NC = K1Tile<K>::NC, TC = K1_TILE_C;
+  __shared__ double xs[TS][K][TC];
+  __shared__ double bs[TC][K];
+  const int i0 = blockIdx.x * TC, s0 = blockIdx.y * TS;
+  for (int idx = threadIdx.x; idx < TS * K * TC; idx += blockDim.x) {
+    int sl = idx / (K * TC), t = (idx / TC) % K, c = idx % TC;
+    xs[sl][t][c] = (s0 + sl < a.nslot) ? a.Xin[(int64_t)(s0 + sl) * a.L + (int64_t)t * npad + i0 + c] : 0.0;
+  }
+  for (int idx = threadIdx.x; idx < TC * K; idx += blockDim.x) bs[idx / K][idx % K] = bhr[(int64_t)i0 * K + idx];
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < TC * NC; idx += blockDim.x) {
+    int r = idx / NC, col = idx % NC;
+    int sl = col / (K * K), s = (col / K) % K, t = col % K;
+    if (s0 + sl >= a.nslot) continue;
+    int c = i0 + r;
+    double val;
+    if (c < two_np) {  // conjugate pair: (br + i bi)(x + i y)
+      int ce = r & ~1;
+      double x = xs[sl][t][ce], y = xs[sl][t][ce + 1];
+      double br = bs[ce][s], bi = bs[ce + 1][s];
+      val = (r & 1) ? (br * y + bi * x) : (br * x - bi * y);
+    } else {
+      val = bs[r][s] * xs[sl][t][r];
+    }
+    Bop[(int64_t)c * ncol + (int64_t)(s0 + sl) * K * K + col % (K * K)] = val;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// K1b: C = A * B, FP64, A: M x Kd row-major (the folded Cauchy matrix Lf), B: Kd x N row-major,
+// C: M x N row-major.  M % BM == N % BN == Kd % 16 == 0.  STAGES-deep cp.async pipeline, warp
+// tile WM x WN of m8n8k4 DMMA fragments.  Shared-memory strides 20 / BN+4 doubles make every
+// fragment load conflict-free (lane -> (row l/4, k l%4) maps onto 16 distinct 8-byte banks per
+// half-warp).
+template <int BM, int BN, int WM, int WN, int STAGES>
+struct DgemmCfg {
+  static constexpr int BK = 16, AST = BK + 4, BST = BN + 4;
+  static constexpr int WARPS_N = BN / WN, WARPS = (BM / WM) * (BN / WN), THREADS = WARPS * 32;
+  static constexpr int A_STAGE = BM * AST, B_STAGE = BK * BST;
+  static constexpr size_t SMEM = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double);
+};
+
+template <int BM, int BN, int WM, int WN, int STAGES>
+__global__ void __launch_bounds__(DgemmCfg<BM, BN, WM, WN, STAGES>::THREADS, 1)
+    k1_dgemm(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C, int M,
+             int N, int Kd, const int* __restrict__ nactive) {
+  using Cfg = DgemmCfg<BM, BN, WM, WN, STAGES>;
+  constexpr int BK = Cfg::BK, AST = Cfg::AST, BST = Cfg::BST, NT = Cfg::THREADS;
+  constexpr int MT = WM / 8, NTL = WN / 8;
+  if (nactive && *nactive == 0) return;
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;
+  double* Bs = smem + STAGES * Cfg::A_STAGE;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wm = warp / Cfg::WARPS_N, wn = warp % Cfg::WARPS_N;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+
+  double acc[MT][NTL][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NTL; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  auto load_stage = [&](int stage, int kt) {
+    const double* Ag = A + (int64_t)m0 * Kd + (int64_t)kt * BK;
+    double* as = As + stage * Cfg::A_STAGE;
+#pragma unroll
+    for (int c = tid; c < BM * BK / 2; c += NT) {
+      int r = c / (BK / 2), cc = (c % (BK / 2)) * 2;
+      cp_async16(as + r * AST + cc, Ag + (int64_t)r * Kd + cc);
+    }
+    const double* Bg = B + (int64_t)kt * BK * N + n0;
+    double* bs = Bs + stage * Cfg::B_STAGE;
+#pragma unroll
+    for (int c = tid; c < BK * BN / 2; c += NT) {
+      int r = c / (BN / 2), cc = (c % (BN / 2)) * 2;
+      cp_async16(bs + r * BST + cc, Bg + (int64_t)r * N + cc);
+    }
+  };
+
+  const int KT = Kd / BK;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) load_stage(s, s);
+    cp_async_commit();
+  }
+  const int ar = wm * WM + (lane >> 2), ac = lane & 3;
+  const int bc = wn * WN + (lane >> 2), br = lane & 3;
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      int nk = kt + STAGES - 1;
+      if (nk < KT) load_stage(nk % STAGES, nk);
+      cp_async_commit();
+    }
+    const double* as = As + (kt % STAGES) * Cfg::A_STAGE;
+    const double* bs = Bs + (kt % STAGES) * Cfg::B_STAGE;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[MT], bf[NTL];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) af[i] = as[(ar + i * 8) * AST + kk + ac];
+#pragma unroll
+      for (int j = 0; j < NTL; ++j) bf[j] = bs[(kk + br) * BST + bc + j * 8];
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NTL; ++j) dmma_884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+  // store: lane holds C[row][2c], C[row][2c+1]
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    int row = m0 + wm * WM + i * 8 + (lane >> 2);
+#pragma unroll
+    for (int j = 0; j < NTL; ++j) {
+      int col = n0 + wn * WN + j * 8 + (lane & 3) * 2;
+      *reinterpret_cast<double2*>(C + (int64_t)row * N + col) = make_double2(acc[i][j][0], acc[i][j][1]);
+    }
+  }
+  (void)M;
+}
+
+// ------------------------------------------------------------------------------------------
+// K1c epilogue: contract U over t with B~l, add T_d, form C(v) X (or the VERIFY residual).
+template <int K>
+__global__ void __launch_bounds__(256) k1_epi(K1Args a, const double* __restrict__ U, int64_t ncol,
+                                               const double* __restrict__ btl, const double* __restrict__ F,
+                                               const double* __restrict__ g0, int npad, int two_np, int npairs,
+                                               int n) {
+  if (a.nactive && *a.nactive == 0) return;
+  constexpr int TS = K1Tile<K>::TS, NC = K1Tile<K>::NC, TC = K1_TILE_C;
+  __shared__ double us[TC][NC + 1];
+  __shared__ double xs[TS][K][TC];
+  const int i0 = blockIdx.x * TC, s0 = blockIdx.y * TS;
+  for (int idx = threadIdx.x; idx < TC * NC; idx += blockDim.x) {
+    int r = idx / NC, col = idx % NC;
+    us[r][col] = (s0 + col / (K * K) < a.nslot) ? U[(int64_t)(i0 + r) * ncol + (int64_t)s0 * K * K + col] : 0.0;
+  }
+  for (int idx = threadIdx.x; idx < TS * K * TC; idx += blockDim.x) {
+    int sl = idx / (K * TC), t = (idx / TC) % K, c = idx % TC;
+    xs[sl][t][c] = (s0 + sl < a.nslot) ? a.Xin[(int64_t)(s0 + sl) * a.L + (int64_t)t * npad + i0 + c] : 0.0;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < TS * K * TC; idx += blockDim.x) {
+    int sl = idx / (K * TC), s = (idx / TC) % K, r = idx % TC;
+    int slot = s0 + sl;
+    if (slot >= a.nslot) continue;
+    int c = i0 + r;
+    double* dst;
+    bool verify = false;
+    double msk = 1.0, sig;
+    if (a.mode == 0) {
+      dst = a.Yout + (int64_t)slot * a.L + (int64_t)s * npad;
+      sig = a.sigma ? a.sigma[slot * K + s] : 0.0;
+    } else {
+      int ph = a.phase[slot];
+      if (ph == PH_ITER) {
+        dst = a.Qb + (int64_t)slot * a.qstride + (int64_t)(a.m[slot] + 1) * a.L + (int64_t)s * npad;
+      } else if (ph == PH_VERIFY) {
+        dst = a.Qb + (int64_t)slot * a.qstride + (int64_t)s * npad;
+        verify = true;
+      } else {
+        continue;
+      }
+      sig = a.sigma[slot * K + s];
+      msk = a.mask[slot * K + s];
+    }
+    if (c >= n) {  // zero padding stays zero
+      dst[c] = 0.0;
+      continue;
+    }
+    const int colb = sl * K * K + s * K;
+    if (c < two_np) {
+      if (r & 1) continue;  // the Re-coordinate thread writes both coordinates of the pair
+      const int rep = c >> 1;
+      cplx y = mk(0.0, 0.0);
+#pragma unroll
+      for (int t = 0; t < K; ++t) {
+        cplx u = mk(us[r][colb + t], us[r + 1][colb + t]);
+        cplx bl = mk(btl[(int64_t)c * K + t], btl[(int64_t)(c + 1) * K + t]);
+        const double* f = F + (((int64_t)rep * K + s) * K + t) * 2;
+        cplx x = mk(xs[sl][t][r], xs[sl][t][r + 1]);
+        y = y + bl * u + mk(f[0], f[1]) * x;
+      }
+      cplx xv = mk(xs[sl][s][r], xs[sl][s][r + 1]);
+      cplx o = (msk != 0.0) ? (sig * xv - y) : xv;
+      if (verify) {
+        o = mk(msk * g0[(int64_t)s * npad + c], msk * g0[(int64_t)s * npad + c + 1]) - o;
+      }
+      dst[c] = o.re;
+      dst[c + 1] = o.im;
+    } else {
+      const int rep = c - two_np + npairs;
+      double y = 0.0;
+#pragma unroll
+      for (int t = 0; t < K; ++t) {
+        y += btl[(int64_t)c * K + t] * us[r][colb + t];
+        y += F[(((int64_t)rep * K + s) * K + t) * 2] * xs[sl][t][r];
+      }
+      double xv = xs[sl][s][r];
+      double o = (msk != 0.0) ? (sig * xv - y) : xv;
+      if (verify) o = msk * g0[(int64_t)s * npad + c] - o;
+      dst[c] = o;
+    }
+  }
+}
+
+}  // namespace lyap

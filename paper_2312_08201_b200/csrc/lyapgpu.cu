@@ -1,0 +1,827 @@
+// lyapgpu — C-ABI implementation (include/lyapgpu.h).  One translation unit: the kernels live in
+// the .cuh files next to this one; this file holds the host control (setup flow, engine loop).
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/lyapgpu.h"
+#include "common.cuh"
+#include "ctx.h"
+#include "engine.cuh"
+#include "k1.cuh"
+#include "setup.cuh"
+
+using namespace lyap;
+
+namespace {
+
+thread_local std::string g_last_error = "no error";
+
+struct Fail {
+  int code;
+};
+
+void set_err(lyap_ctx* c, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  if (c) c->err = buf;
+}
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess) {                                                              \
+      set_err(ctx, "%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_));    \
+      throw Fail{e_ == cudaErrorMemoryAllocation ? LYAP_ENOMEM : LYAP_ECUDA};             \
+    }                                                                                     \
+  } while (0)
+#define CKB(call)                                                                         \
+  do {                                                                                    \
+    cublasStatus_t e_ = (call);                                                           \
+    if (e_ != CUBLAS_STATUS_SUCCESS) {                                                    \
+      set_err(ctx, "%s:%d %s: cublas status %d", __FILE__, __LINE__, #call, (int)e_);     \
+      throw Fail{LYAP_ECUDA};                                                             \
+    }                                                                                     \
+  } while (0)
+#define CKS(call)                                                                         \
+  do {                                                                                    \
+    cusolverStatus_t e_ = (call);                                                         \
+    if (e_ != CUSOLVER_STATUS_SUCCESS) {                                                  \
+      set_err(ctx, "%s:%d %s: cusolver status %d", __FILE__, __LINE__, #call, (int)e_);   \
+      throw Fail{LYAP_ECUDA};                                                             \
+    }                                                                                     \
+  } while (0)
+#define LAUNCHED()                      \
+  do {                                  \
+    CK(cudaGetLastError());             \
+    ctx->stats.kernel_launches++;       \
+  } while (0)
+
+template <typename T>
+T* dalloc(lyap_ctx* ctx, size_t count, bool zero = true) {
+  void* p = nullptr;
+  CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+  if (zero) CK(cudaMemset(p, 0, std::max<size_t>(count, 1) * sizeof(T)));
+  return static_cast<T*>(p);
+}
+void dfree(void* p) {
+  if (p) cudaFree(p);
+}
+
+int64_t roundup(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+// K1 GEMM configuration
+constexpr int G_BM = 128, G_BN = 128, G_WM = 64, G_WN = 32, G_ST = 4;
+using GCfg = DgemmCfg<G_BM, G_BN, G_WM, G_WN, G_ST>;
+
+#define K_DISPATCH(KV, ...)     \
+  switch (KV) {                  \
+    case 1: { constexpr int KK = 1; __VA_ARGS__; } break; \
+    case 2: { constexpr int KK = 2; __VA_ARGS__; } break; \
+    case 3: { constexpr int KK = 3; __VA_ARGS__; } break; \
+    case 4: { constexpr int KK = 4; __VA_ARGS__; } break; \
+    case 5: { constexpr int KK = 5; __VA_ARGS__; } break; \
+    case 6: { constexpr int KK = 6; __VA_ARGS__; } break; \
+    case 7: { constexpr int KK = 7; __VA_ARGS__; } break; \
+    case 8: { constexpr int KK = 8; __VA_ARGS__; } break; \
+    default: break;              \
+  }
+
+// ------------------------------------------------------------------ engine allocation
+void free_engine(Engine& g) {
+  void* ps[] = {g.Bop, g.U, g.Xin, g.X, g.Qb, g.Minv, g.sigma, g.mask, g.eta, g.H, g.e, g.y,
+                g.bnorm, g.part, g.part3, g.phase, g.m, g.vidx, g.applies, g.restarts, g.ctrl};
+  for (void* p : ps) dfree(p);
+  if (g.h_ctrl) cudaFreeHost(g.h_ctrl);
+  g = Engine{};
+}
+
+int auto_batch(const lyap_ctx* ctx, int64_t nv) {
+  const Seed& s = ctx->seed;
+  int b = ctx->opts.batch;
+  if (b <= 0) {
+    // aim for ~8 waves of 128x128 K1 tiles on 148 SMs
+    const int64_t mt = s.npad / G_BM;
+    const int64_t target_cols = (8 * 148 + mt - 1) / mt * G_BN;
+    b = (int)std::max<int64_t>(32, std::min<int64_t>(1024, target_cols / (s.k * s.k)));
+  }
+  b = (int)std::min<int64_t>(b, std::max<int64_t>(nv, 1));
+  b = std::max(1, std::min(b, 1024));
+  return b;
+}
+
+int auto_mmax(const lyap_ctx* ctx) {
+  if (ctx->opts.max_dim > 0) return ctx->opts.max_dim;
+  return 160;
+}
+
+void ensure_engine(lyap_ctx* ctx, int b, int mmax) {
+  Engine& g = ctx->eng;
+  if (g.b == b && g.mmax == mmax && g.Qb) return;
+  free_engine(g);
+  const Seed& s = ctx->seed;
+  g.b = b;
+  g.mmax = mmax;
+  g.L = s.k * s.npad;
+  g.ncol = roundup((int64_t)b * s.k * s.k, G_BN);
+  g.nchunk = (int)((g.L + RED_CE - 1) / RED_CE);
+  g.Bop = dalloc<double>(ctx, (size_t)s.npad * g.ncol);
+  g.U = dalloc<double>(ctx, (size_t)s.npad * g.ncol);
+  g.Xin = dalloc<double>(ctx, (size_t)b * g.L);
+  g.X = dalloc<double>(ctx, (size_t)b * g.L);
+  g.Qb = dalloc<double>(ctx, (size_t)b * (mmax + 1) * g.L);
+  g.Minv = dalloc<double>(ctx, (size_t)b * s.nrep * s.k * s.k * 2);
+  g.sigma = dalloc<double>(ctx, (size_t)b * s.k);
+  g.mask = dalloc<double>(ctx, (size_t)b * s.k);
+  g.eta = dalloc<double>(ctx, (size_t)b * (mmax + 1));
+  g.H = dalloc<double>(ctx, (size_t)b * (mmax + 1) * mmax);
+  g.e = dalloc<double>(ctx, (size_t)b * (mmax + 1) + 2 * (size_t)b * mmax);  // e | cs | sn
+  g.y = dalloc<double>(ctx, (size_t)b * mmax);
+  g.bnorm = dalloc<double>(ctx, b);
+  g.part = dalloc<double>(ctx, (size_t)b * (mmax + 2) * g.nchunk);
+  g.part3 = dalloc<double>(ctx, (size_t)b * g.nchunk * 3);
+  g.phase = dalloc<int>(ctx, b);
+  g.m = dalloc<int>(ctx, b);
+  g.vidx = dalloc<int>(ctx, b);
+  g.applies = dalloc<int>(ctx, b);
+  g.restarts = dalloc<int>(ctx, 2 * (size_t)b);  // restarts | newv
+  g.ctrl = dalloc<int>(ctx, 8);
+  CK(cudaMallocHost(&g.h_ctrl, 8 * sizeof(int)));
+  ctx->info.batch = b;
+  ctx->info.max_dim = mmax;
+}
+
+// ------------------------------------------------------------------ K1 launch (prologue, GEMM, epilogue)
+struct EvPool {
+  std::vector<cudaEvent_t> ev;
+  int used = 0;
+};
+
+void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, EvPool* pool) {
+  const Seed& s = ctx->seed;
+  const Engine& g = ctx->eng;
+  const int two_np = (int)(2 * s.npairs);
+  K_DISPATCH(s.k, {
+    dim3 grid((unsigned)(s.npad / K1_TILE_C), (unsigned)((a.nslot + K1Tile<KK>::TS - 1) / K1Tile<KK>::TS));
+    k1_gen<KK><<<grid, 256, 0, st>>>(a, s.bhr, (int)s.npad, two_np, g.Bop, g.ncol);
+  });
+  LAUNCHED();
+  {
+    dim3 grid((unsigned)(g.ncol / G_BN), (unsigned)(s.npad / G_BM));
+    if (pool) CK(cudaEventRecord(pool->ev[2 * pool->used], st));
+    k1_dgemm<G_BM, G_BN, G_WM, G_WN, G_ST><<<grid, GCfg::THREADS, GCfg::SMEM, st>>>(
+        s.Lf, g.Bop, g.U, (int)s.npad, (int)g.ncol, (int)s.npad, a.nactive);
+    LAUNCHED();
+    if (pool) {
+      CK(cudaEventRecord(pool->ev[2 * pool->used + 1], st));
+      pool->used++;
+    }
+    ctx->stats.k1_launches++;
+  }
+  K_DISPATCH(s.k, {
+    dim3 grid((unsigned)(s.npad / K1_TILE_C), (unsigned)((a.nslot + K1Tile<KK>::TS - 1) / K1Tile<KK>::TS));
+    k1_epi<KK><<<grid, 256, 0, st>>>(a, g.U, g.ncol, s.btl, s.F, s.g0, (int)s.npad, two_np, (int)s.npairs,
+                                     (int)s.n);
+  });
+  LAUNCHED();
+}
+
+void drain_pool(lyap_ctx* ctx, EvPool& pool) {
+  if (!pool.used) return;
+  CK(cudaEventSynchronize(pool.ev[2 * pool.used - 1]));
+  for (int i = 0; i < pool.used; ++i) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, pool.ev[2 * i], pool.ev[2 * i + 1]));
+    ctx->stats.k1_ms += ms;
+  }
+  pool.used = 0;
+}
+
+// ------------------------------------------------------------------ the batched engine
+int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, double* dtr, int32_t* dst, int32_t* dap,
+              double* dres, cudaStream_t st) {
+  const Seed& s = ctx->seed;
+  const int b = auto_batch(ctx, nv), mmax = auto_mmax(ctx);
+  ensure_engine(ctx, b, mmax);
+  Engine& g = ctx->eng;
+  CK(cudaMemsetAsync(g.phase, 0, sizeof(int) * b, st));  // PH_FREE
+  CK(cudaMemsetAsync(g.ctrl, 0, sizeof(int) * 8, st));
+  CK(cudaMemsetAsync(g.X, 0, sizeof(double) * (size_t)b * g.L, st));
+  CK(cudaMemsetAsync(g.restarts, 0, sizeof(int) * 2 * (size_t)b, st));
+
+  EngArgs a{};
+  a.b = b;
+  a.mmax = mmax;
+  a.K = (int)s.k;
+  a.nv = (int)nv;
+  a.L = g.L;
+  a.npad = s.npad;
+  a.nrep = s.nrep;
+  a.npairs = s.npairs;
+  a.two_np = 2 * s.npairs;
+  a.n = s.n;
+  a.nchunk = g.nchunk;
+  a.tol = ctx->opts.tol;
+  a.tol_inner = 0.5 * ctx->opts.tol;
+  a.t0 = s.t0;
+  a.max_restarts = ctx->opts.max_restarts;
+  a.warm = ctx->opts.warm_start;
+  a.V = dV;
+  a.g0 = s.g0;
+  a.hf = s.hf;
+  a.F = s.F;
+  a.X = g.X;
+  a.Xin = g.Xin;
+  a.Qb = g.Qb;
+  a.Minv = g.Minv;
+  a.sigma = g.sigma;
+  a.mask = g.mask;
+  a.eta = g.eta;
+  a.H = g.H;
+  a.e = g.e;
+  a.y = g.y;
+  a.bnorm = g.bnorm;
+  a.part = g.part;
+  a.part3 = g.part3;
+  a.phase = g.phase;
+  a.m = g.m;
+  a.vidx = g.vidx;
+  a.applies = g.applies;
+  a.restarts = g.restarts;
+  a.newv = g.restarts + b;
+  a.ctrl = g.ctrl;
+  a.traces = dtr;
+  a.status = dst;
+  a.out_applies = dap;
+  a.out_resid = dres;
+
+  K1Args k1{};
+  k1.Xin = g.Xin;
+  k1.L = g.L;
+  k1.nslot = b;
+  k1.mode = 1;
+  k1.mask = g.mask;
+  k1.sigma = g.sigma;
+  k1.phase = g.phase;
+  k1.m = g.m;
+  k1.Qb = g.Qb;
+  k1.qstride = (int64_t)(mmax + 1) * g.L;
+  k1.nactive = g.ctrl + 2;
+
+  EvPool pool;
+  EvPool* pp = nullptr;
+  if (ctx->opts.profile) {
+    pool.ev.resize(2 * 512);
+    for (auto& e : pool.ev) CK(cudaEventCreate(&e));
+    pp = &pool;
+  }
+  const dim3 grep((unsigned)((s.nrep + 127) / 128), (unsigned)b);
+  const dim3 gred((unsigned)g.nchunk, (unsigned)b);
+  const int assign_threads = (int)roundup(b, 32);
+  const size_t upd_smem = sizeof(double) * (mmax + 1);
+  const int64_t per_v = (int64_t)(ctx->opts.max_restarts + 1) * (mmax + 2);
+  const int64_t max_iter = ((nv + b - 1) / b) * per_v + 64;
+  const int poll = 4;
+  CK(cudaEventRecord(ctx->ev0, st));
+  int64_t it = 0;
+  int rc = LYAP_OK;
+  for (;;) {
+    k_assign<<<1, assign_threads, 0, st>>>(a);
+    LAUNCHED();
+    K_DISPATCH(s.k, (k_pfactor<KK><<<grep, 128, 0, st>>>(a)));
+    LAUNCHED();
+    K_DISPATCH(s.k, (k_prec<KK><<<grep, 128, 0, st>>>(a)));
+    LAUNCHED();
+    launch_k1(ctx, k1, st, pp);
+    k_dots<<<gred, 256, 0, st>>>(a, 1);
+    LAUNCHED();
+    k_upd<<<gred, 256, upd_smem, st>>>(a, 1);
+    LAUNCHED();
+    k_dots<<<gred, 256, 0, st>>>(a, 2);
+    LAUNCHED();
+    k_upd<<<gred, 256, upd_smem, st>>>(a, 2);
+    LAUNCHED();
+    k_ctrl<<<(b + 3) / 4, 128, 0, st>>>(a);
+    LAUNCHED();
+    K_DISPATCH(s.k, (k_xupd<KK><<<grep, 128, 0, st>>>(a)));
+    LAUNCHED();
+    ++it;
+    if (pp && pool.used == 512) drain_pool(ctx, pool);
+    if (it % poll == 0) {
+      CK(cudaMemcpyAsync(g.h_ctrl, g.ctrl, 8 * sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (g.h_ctrl[1] >= nv) break;
+      if (it > max_iter) {
+        set_err(ctx, "engine did not finish after %lld iterations (%d of %lld done)", (long long)it, g.h_ctrl[1],
+                (long long)nv);
+        rc = LYAP_ECUDA;
+        break;
+      }
+    }
+  }
+  CK(cudaEventRecord(ctx->ev1, st));
+  CK(cudaEventSynchronize(ctx->ev1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  ctx->stats.batch_ms = ms;
+  ctx->stats.iterations += it;
+  {
+    unsigned long long nvec = 0;
+    std::memcpy(&nvec, g.h_ctrl + 4, 8);
+    ctx->stats.k1_vectors += (int64_t)nvec;
+    ctx->stats.k1_flops += 2.0 * (double)s.n * s.n * s.k * s.k * (double)nvec;
+  }
+  if (pp) {
+    drain_pool(ctx, pool);
+    for (auto& e : pool.ev) cudaEventDestroy(e);
+  }
+  return rc;
+}
+
+}  // namespace
+
+// ====================================================================== C-ABI
+extern "C" {
+
+void lyap_default_opts(lyap_opts* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof *o);
+  o->tol = 1e-12;
+  o->max_dim = 0;
+  o->max_restarts = 30;
+  o->batch = 0;
+  o->warm_start = 1;
+  o->max_cond_S = 1e8;
+  o->device = -1;
+  o->profile = 0;
+}
+
+const char* lyap_last_error(const lyap_ctx* c) { return c ? c->err.c_str() : g_last_error.c_str(); }
+
+static void destroy_impl(lyap_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  free_engine(c->eng);
+  Seed& s = c->seed;
+  void* ps[] = {s.lam, s.bhr, s.btl, s.F, s.g0, s.hf, s.Lf};
+  for (void* p : ps) dfree(p);
+  if (c->cublas) cublasDestroy(c->cublas);
+  if (c->cusolver) cusolverDnDestroy(c->cusolver);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+void lyap_destroy(lyap_ctx* c) { destroy_impl(c); }
+
+int lyap_setup(int64_t n, int64_t k, const double* A0, const double* Bl, const double* Br, const double* Q,
+               const double* E, const lyap_opts* opts, lyap_ctx** out) {
+  lyap_ctx* ctx = nullptr;
+  if (!out) {
+    set_err(nullptr, "lyap_setup: out is NULL");
+    return LYAP_EINVAL;
+  }
+  *out = nullptr;
+  if (n < 1 || k < 1 || k > LYAP_KMAX || !A0 || !Bl || !Br || !Q || !E) {
+    set_err(nullptr, "lyap_setup: invalid arguments (n=%lld, k=%lld, k must be 1..%d, no NULL inputs)",
+            (long long)n, (long long)k, LYAP_KMAX);
+    return LYAP_EINVAL;
+  }
+  {  // Q symmetric (the nk reduction needs Q = Q^T)
+    double mx = 0.0, asym = 0.0;
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t j = 0; j < n; ++j) {
+        mx = std::max(mx, std::fabs(Q[i * n + j]));
+        asym = std::max(asym, std::fabs(Q[i * n + j] - Q[j * n + i]));
+      }
+    if (asym > 1e-13 * mx) {
+      set_err(nullptr, "lyap_setup: Q is not symmetric (max |Q - Q^T| = %.3e, max |Q| = %.3e)", asym, mx);
+      return LYAP_EINVAL;
+    }
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    set_err(nullptr, "lyap_setup: no CUDA device (this library has no CPU path)");
+    return LYAP_ENODEV;
+  }
+  ctx = new lyap_ctx();
+  lyap_default_opts(&ctx->opts);
+  if (opts) ctx->opts = *opts;
+  if (!(ctx->opts.tol > 0)) ctx->opts.tol = 1e-12;
+  if (ctx->opts.max_restarts <= 0) ctx->opts.max_restarts = 30;
+  if (!(ctx->opts.max_cond_S > 0)) ctx->opts.max_cond_S = 1e8;
+  // scratch
+  double *dA = nullptr, *dBl = nullptr, *dBr = nullptr, *dQ = nullptr, *dE = nullptr, *Acm = nullptr, *Qs = nullptr,
+         *Es = nullptr, *Blc = nullptr, *Brc = nullptr, *VR = nullptr, *Sr = nullptr, *Sinv = nullptr, *LU = nullptr,
+         *T1 = nullptr, *Qr = nullptr, *Er = nullptr, *Blr = nullptr, *Brr = nullptr, *W = nullptr, *work = nullptr,
+         *t0part = nullptr, *t0d = nullptr;
+  int *perm = nullptr, *ipiv = nullptr, *dinfo = nullptr;
+  unsigned long long* ext = nullptr;
+  void* hwork = nullptr;
+  int rc = LYAP_OK;
+  try {
+    int dev = ctx->opts.device;
+    if (dev < 0) CK(cudaGetDevice(&dev));
+    ctx->device = dev;
+    CK(cudaSetDevice(dev));
+    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&ctx->ev0));
+    CK(cudaEventCreate(&ctx->ev1));
+    CKB(cublasCreate(&ctx->cublas));
+    CKB(cublasSetStream(ctx->cublas, ctx->stream));
+    CKS(cusolverDnCreate(&ctx->cusolver));
+    CKS(cusolverDnSetStream(ctx->cusolver, ctx->stream));
+    CK(cudaFuncSetAttribute(k1_dgemm<G_BM, G_BN, G_WM, G_WN, G_ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)GCfg::SMEM));
+    cudaStream_t st = ctx->stream;
+    CK(cudaEventRecord(ctx->ev0, st));
+    Seed& s = ctx->seed;
+    s.n = n;
+    s.k = k;
+    s.npad = roundup(n, G_BM);
+    const size_t nn = (size_t)n * n;
+    dA = dalloc<double>(ctx, nn, false);
+    dQ = dalloc<double>(ctx, nn, false);
+    dE = dalloc<double>(ctx, nn, false);
+    dBl = dalloc<double>(ctx, (size_t)n * k, false);
+    dBr = dalloc<double>(ctx, (size_t)n * k, false);
+    CK(cudaMemcpyAsync(dA, A0, nn * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dQ, Q, nn * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dE, E, nn * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dBl, Bl, (size_t)n * k * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dBr, Br, (size_t)n * k * 8, cudaMemcpyHostToDevice, st));
+    Acm = dalloc<double>(ctx, nn, false);
+    Qs = dalloc<double>(ctx, nn, false);
+    Es = dalloc<double>(ctx, nn, false);
+    Blc = dalloc<double>(ctx, (size_t)n * k, false);
+    Brc = dalloc<double>(ctx, (size_t)n * k, false);
+    const dim3 tb(32, 8);
+    k_transpose<<<dim3((unsigned)((n + 31) / 32), (unsigned)((n + 31) / 32)), tb, 0, st>>>(dA, Acm, n, n);
+    LAUNCHED();
+    k_transpose<<<dim3((unsigned)((k + 31) / 32), (unsigned)((n + 31) / 32)), tb, 0, st>>>(dBl, Blc, n, k);
+    LAUNCHED();
+    k_transpose<<<dim3((unsigned)((k + 31) / 32), (unsigned)((n + 31) / 32)), tb, 0, st>>>(dBr, Brc, n, k);
+    LAUNCHED();
+    k_symmetrize<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(dQ, Qs, n);
+    LAUNCHED();
+    k_symmetrize<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(dE, Es, n);
+    LAUNCHED();
+
+    // ---- S1: eig(A0) on the device (real input, LAPACK-style real eigenvector packing)
+    VR = dalloc<double>(ctx, nn, false);
+    W = dalloc<double>(ctx, 2 * (size_t)n, false);
+    dinfo = dalloc<int>(ctx, 1);
+    cusolverDnParams_t params;
+    CKS(cusolverDnCreateParams(&params));
+    size_t dws = 0, hws = 0;
+    CKS(cusolverDnXgeev_bufferSize(ctx->cusolver, params, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR, n,
+                                   CUDA_R_64F, Acm, n, CUDA_C_64F, W, CUDA_R_64F, nullptr, n, CUDA_R_64F, VR, n,
+                                   CUDA_R_64F, &dws, &hws));
+    void* dwork = nullptr;
+    CK(cudaMalloc(&dwork, std::max<size_t>(dws, 8)));
+    hwork = std::malloc(std::max<size_t>(hws, 8));
+    cusolverStatus_t gs =
+        cusolverDnXgeev(ctx->cusolver, params, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR, n, CUDA_R_64F,
+                        Acm, n, CUDA_C_64F, W, CUDA_R_64F, nullptr, n, CUDA_R_64F, VR, n, CUDA_R_64F, dwork, dws,
+                        hwork, hws, dinfo);
+    cudaStreamSynchronize(st);
+    cudaFree(dwork);
+    cusolverDnDestroyParams(params);
+    if (gs != CUSOLVER_STATUS_SUCCESS) {
+      set_err(ctx, "cusolverDnXgeev failed with status %d", (int)gs);
+      throw Fail{LYAP_EEIG};
+    }
+    int hinfo = 0;
+    CK(cudaMemcpy(&hinfo, dinfo, sizeof(int), cudaMemcpyDeviceToHost));
+    if (hinfo != 0) {
+      set_err(ctx, "cusolverDnXgeev info = %d", hinfo);
+      throw Fail{LYAP_EEIG};
+    }
+    // ---- pairing map (host logic): conjugate pairs first (Re, Im coordinates), then reals
+    std::vector<double> hW(2 * (size_t)n);
+    CK(cudaMemcpy(hW.data(), W, 2 * (size_t)n * 8, cudaMemcpyDeviceToHost));
+    std::vector<int> pairs, reals;
+    for (int64_t i = 0; i < n;) {
+      const double re = hW[2 * i], im = hW[2 * i + 1];
+      if (im > 0.0 && i + 1 < n && hW[2 * (i + 1)] == re && hW[2 * (i + 1) + 1] == -im) {
+        pairs.push_back((int)i);
+        i += 2;
+      } else if (im == 0.0) {
+        reals.push_back((int)i);
+        i += 1;
+      } else {
+        set_err(ctx, "eig(A0): eigenvalue %lld (%.17g, %.17g) is not part of a conjugate pair in LAPACK order",
+                (long long)i, re, im);
+        throw Fail{LYAP_EEIG};
+      }
+    }
+    s.npairs = (int64_t)pairs.size();
+    s.nrep = s.npairs + (int64_t)reals.size();
+    const int64_t two_np = 2 * s.npairs;
+    std::vector<int> hperm(n);
+    std::vector<double> hlam(2 * (size_t)s.npad, 0.0);
+    for (int64_t r = 0; r < s.npairs; ++r) {
+      const int i = pairs[r];
+      hperm[2 * r] = i;
+      hperm[2 * r + 1] = i + 1;
+      for (int q = 0; q < 2; ++q) {
+        hlam[2 * (2 * r + q)] = hW[2 * i];
+        hlam[2 * (2 * r + q) + 1] = hW[2 * i + 1];
+      }
+    }
+    for (size_t r = 0; r < reals.size(); ++r) {
+      const int i = reals[r];
+      hperm[two_np + r] = i;
+      hlam[2 * (two_np + r)] = hW[2 * i];
+      hlam[2 * (two_np + r) + 1] = 0.0;
+    }
+    perm = dalloc<int>(ctx, n, false);
+    CK(cudaMemcpy(perm, hperm.data(), n * sizeof(int), cudaMemcpyHostToDevice));
+    s.lam = dalloc<double>(ctx, 2 * (size_t)s.npad);
+    CK(cudaMemcpy(s.lam, hlam.data(), 2 * (size_t)s.npad * 8, cudaMemcpyHostToDevice));
+    Sr = dalloc<double>(ctx, nn, false);
+    k_gather_cols<<<dim3((unsigned)((n + 255) / 256), (unsigned)n), 256, 0, st>>>(VR, perm, Sr, n);
+    LAUNCHED();
+
+    // ---- S2: S_r^{-1} (LU)
+    LU = dalloc<double>(ctx, nn, false);
+    Sinv = dalloc<double>(ctx, nn, false);
+    ipiv = dalloc<int>(ctx, n, false);
+    CK(cudaMemcpyAsync(LU, Sr, nn * 8, cudaMemcpyDeviceToDevice, st));
+    int lwork = 0;
+    CKS(cusolverDnDgetrf_bufferSize(ctx->cusolver, (int)n, (int)n, LU, (int)n, &lwork));
+    work = dalloc<double>(ctx, std::max(lwork, 1), false);
+    CKS(cusolverDnDgetrf(ctx->cusolver, (int)n, (int)n, LU, (int)n, work, ipiv, dinfo));
+    k_set_identity<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(Sinv, n);
+    LAUNCHED();
+    CKS(cusolverDnDgetrs(ctx->cusolver, CUBLAS_OP_N, (int)n, (int)n, LU, (int)n, ipiv, Sinv, (int)n, dinfo));
+    CK(cudaMemcpyAsync(&hinfo, dinfo, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (hinfo != 0) {
+      set_err(ctx, "eigenvector matrix S is singular (getrf/getrs info = %d)", hinfo);
+      throw Fail{LYAP_EEIG};
+    }
+    ext = dalloc<unsigned long long>(ctx, 4);
+    k_norm1<<<(unsigned)n, 256, 0, st>>>(Sr, n, ext);
+    LAUNCHED();
+    k_norm1<<<(unsigned)n, 256, 0, st>>>(Sinv, n, ext + 1);
+    LAUNCHED();
+    // ---- S3-S5: real n^3 products (cuBLAS DGEMM, column-major)
+    T1 = dalloc<double>(ctx, nn, false);
+    Qr = dalloc<double>(ctx, nn, false);
+    Er = dalloc<double>(ctx, nn, false);
+    Blr = dalloc<double>(ctx, (size_t)n * k, false);
+    Brr = dalloc<double>(ctx, (size_t)n * k, false);
+    const double one = 1.0, zero = 0.0;
+    const int ni = (int)n, ki = (int)k;
+    CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, ni, ni, ni, &one, Sinv, ni, Qs, ni, &zero, T1, ni));
+    CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_T, ni, ni, ni, &one, T1, ni, Sinv, ni, &zero, Qr, ni));
+    CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_T, CUBLAS_OP_N, ni, ni, ni, &one, Sr, ni, Es, ni, &zero, T1, ni));
+    CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, ni, ni, ni, &one, T1, ni, Sr, ni, &zero, Er, ni));
+    CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, ni, ki, ni, &one, Sinv, ni, Blc, ni, &zero, Blr, ni));
+    CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_T, CUBLAS_OP_N, ni, ki, ni, &one, Sr, ni, Brc, ni, &zero, Brr, ni));
+    // ---- eigenvalue extremes
+    {
+      unsigned long long big = 0x7fefffffffffffffULL;  // DBL_MAX bits
+      CK(cudaMemcpyAsync(ext + 2, &big, 8, cudaMemcpyHostToDevice, st));
+      k_lam_extremes<<<dim3((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)n), 256, 0, st>>>(
+          s.lam, n, two_np, ext + 2, ext + 3);
+      LAUNCHED();
+    }
+    // ---- S6-S7: seed quantities per representative, folded
+    s.g0 = dalloc<double>(ctx, (size_t)k * s.npad);
+    s.hf = dalloc<double>(ctx, (size_t)k * s.npad);
+    s.F = dalloc<double>(ctx, (size_t)s.nrep * k * k * 2);
+    s.bhr = dalloc<double>(ctx, (size_t)s.npad * k);
+    s.btl = dalloc<double>(ctx, (size_t)s.npad * k);
+    s.Lf = dalloc<double>(ctx, (size_t)s.npad * s.npad, false);
+    t0part = dalloc<double>(ctx, s.nrep);
+    t0d = dalloc<double>(ctx, 1);
+    K_DISPATCH(k, (k_seed_rep<KK><<<(unsigned)s.nrep, 128, 0, st>>>(s.lam, Qr, Er, Blr, Brr, n, s.npad, two_np,
+                                                                       s.npairs, s.g0, s.hf, s.F, t0part)));
+    LAUNCHED();
+    k_fold_b<<<(unsigned)((s.npad * k + 255) / 256), 256, 0, st>>>(Blr, Brr, n, s.npad, k, two_np, s.btl, s.bhr);
+    LAUNCHED();
+    k_build_Lf<<<dim3((unsigned)((s.npad + 255) / 256), (unsigned)s.npad), 256, 0, st>>>(s.lam, n, s.npad, two_np,
+                                                                                        s.Lf);
+    LAUNCHED();
+    k_sum<<<1, 1024, 0, st>>>(t0part, s.nrep, t0d);
+    LAUNCHED();
+    unsigned long long hext[4];
+    CK(cudaMemcpyAsync(hext, ext, sizeof hext, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&s.t0, t0d, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(ctx->ev1, st));
+    CK(cudaStreamSynchronize(st));
+    double n1S, n1Si, mins, maxl;
+    std::memcpy(&n1S, &hext[0], 8);
+    std::memcpy(&n1Si, &hext[1], 8);
+    std::memcpy(&mins, &hext[2], 8);
+    std::memcpy(&maxl, &hext[3], 8);
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    lyap_info& in = ctx->info;
+    in.n = n;
+    in.k = k;
+    in.npad = s.npad;
+    in.n_pairs = s.npairs;
+    in.t0 = s.t0;
+    in.cond_S = n1S * n1Si;
+    in.min_lam_sum = mins;
+    in.max_abs_lam = maxl;
+    in.setup_ms = ms;
+    if (!(in.cond_S <= ctx->opts.max_cond_S)) {
+      set_err(ctx, "eigenvector basis too ill-conditioned: cond_1(S_r) = %.3e > %.3e", in.cond_S,
+              ctx->opts.max_cond_S);
+      throw Fail{LYAP_EEIG};
+    }
+    if (!(mins > 1e-12 * maxl)) {
+      set_err(ctx, "seed Lyapunov operator singular: min |lambda_i + lambda_j| = %.3e (max |lambda| = %.3e)", mins,
+              maxl);
+      throw Fail{LYAP_ESINGULAR};
+    }
+    if (!std::isfinite(s.t0)) {
+      set_err(ctx, "seed trace t0 is not finite");
+      throw Fail{LYAP_EEIG};
+    }
+  } catch (Fail f) {
+    rc = f.code;
+  }
+  void* tmp[] = {dA, dBl, dBr, dQ, dE, Acm, Qs, Es, Blc, Brc, VR, Sr, Sinv, LU, T1, Qr, Er, Blr, Brr, W, work,
+                 t0part, t0d, perm, ipiv, dinfo, ext};
+  for (void* p : tmp) dfree(p);
+  std::free(hwork);
+  if (rc != LYAP_OK) {
+    g_last_error = ctx->err;
+    destroy_impl(ctx);
+    return rc;
+  }
+  *out = ctx;
+  return LYAP_OK;
+}
+
+int lyap_trace_batch_ex(lyap_ctx* ctx, int64_t nv, const double* V, double* traces, int32_t* status,
+                        int32_t* applies, double* resid, int v_on_device, void* cuda_stream) {
+  if (!ctx) {
+    set_err(nullptr, "lyap_trace_batch: ctx is NULL");
+    return LYAP_EINVAL;
+  }
+  if (nv < 0 || (nv > 0 && (!V || !traces)) || nv > (int64_t)INT32_MAX) {
+    set_err(ctx, "lyap_trace_batch: invalid arguments (nv=%lld)", (long long)nv);
+    return LYAP_EINVAL;
+  }
+  if (nv == 0) return LYAP_OK;
+  double *dV = nullptr, *dtr = nullptr, *dres = nullptr;
+  int32_t *dst = nullptr, *dap = nullptr;
+  bool own = !v_on_device;
+  int rc = LYAP_OK;
+  try {
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = v_on_device ? (cudaStream_t)cuda_stream : ctx->stream;
+    const int64_t k = ctx->seed.k;
+    if (own) {
+      dV = dalloc<double>(ctx, (size_t)nv * k, false);
+      dtr = dalloc<double>(ctx, nv, false);
+      dst = dalloc<int32_t>(ctx, nv, false);
+      if (applies) dap = dalloc<int32_t>(ctx, nv, false);
+      if (resid) dres = dalloc<double>(ctx, nv, false);
+      CK(cudaMemcpyAsync(dV, V, (size_t)nv * k * 8, cudaMemcpyHostToDevice, st));
+    } else {
+      dV = const_cast<double*>(V);
+      dtr = traces;
+      dst = status;
+      dap = applies;
+      dres = resid;
+    }
+    int* dbad = nullptr;
+    rc = run_batch(ctx, nv, dV, dtr, dst, dap, dres, st);
+    (void)dbad;
+    if (rc == LYAP_OK) {
+      // any per-v failure -> LYAP_EPARTIAL
+      std::vector<int32_t> hs;
+      const int32_t* sp = nullptr;
+      if (own) {
+        CK(cudaMemcpyAsync(traces, dtr, nv * 8, cudaMemcpyDeviceToHost, st));
+        if (applies) CK(cudaMemcpyAsync(applies, dap, nv * 4, cudaMemcpyDeviceToHost, st));
+        if (resid) CK(cudaMemcpyAsync(resid, dres, nv * 8, cudaMemcpyDeviceToHost, st));
+        hs.resize(nv);
+        CK(cudaMemcpyAsync(hs.data(), dst, nv * 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (status) std::memcpy(status, hs.data(), nv * 4);
+        sp = hs.data();
+      } else if (status) {
+        hs.resize(nv);
+        CK(cudaMemcpyAsync(hs.data(), status, nv * 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        sp = hs.data();
+      }
+      if (sp)
+        for (int64_t i = 0; i < nv; ++i)
+          if (sp[i] != 0) {
+            rc = LYAP_EPARTIAL;
+            set_err(ctx, "v %lld: status %d", (long long)i, (int)sp[i]);
+            break;
+          }
+    }
+  } catch (Fail f) {
+    rc = f.code;
+  }
+  if (own) {
+    dfree(dV);
+    dfree(dtr);
+    dfree(dst);
+    dfree(dap);
+    dfree(dres);
+  }
+  return rc;
+}
+
+int lyap_trace_batch(lyap_ctx* ctx, int64_t nv, const double* V, double* traces, int32_t* status,
+                     int v_on_device, void* cuda_stream) {
+  return lyap_trace_batch_ex(ctx, nv, V, traces, status, nullptr, nullptr, v_on_device, cuda_stream);
+}
+
+int lyap_apply_C(lyap_ctx* ctx, int64_t nvec, const double* X, const double* sigma, double* Y, void* cuda_stream) {
+  if (!ctx || nvec < 0 || (nvec > 0 && (!X || !Y))) {
+    set_err(ctx, "lyap_apply_C: invalid arguments");
+    return LYAP_EINVAL;
+  }
+  try {
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    const int b = auto_batch(ctx, std::max<int64_t>(nvec, 1));
+    ensure_engine(ctx, std::max(b, ctx->eng.b), ctx->eng.mmax > 0 ? ctx->eng.mmax : auto_mmax(ctx));
+    const Engine& g = ctx->eng;
+    for (int64_t v0 = 0; v0 < nvec; v0 += g.b) {
+      const int nb = (int)std::min<int64_t>(g.b, nvec - v0);
+      K1Args a{};
+      a.Xin = X + v0 * g.L;
+      a.L = g.L;
+      a.nslot = nb;
+      a.mode = 0;
+      a.sigma = sigma ? sigma + v0 * ctx->seed.k : nullptr;
+      a.Yout = Y + v0 * g.L;
+      a.nactive = nullptr;
+      if (nb < g.b) CK(cudaMemsetAsync(g.Bop, 0, sizeof(double) * ctx->seed.npad * g.ncol, st));
+      launch_k1(ctx, a, st, nullptr);
+      ctx->stats.k1_vectors += nb;
+      ctx->stats.k1_flops += 2.0 * (double)ctx->seed.n * ctx->seed.n * ctx->seed.k * ctx->seed.k * nb;
+    }
+  } catch (Fail f) {
+    return f.code;
+  }
+  return LYAP_OK;
+}
+
+int lyap_get_info(const lyap_ctx* ctx, lyap_info* info) {
+  if (!ctx || !info) return LYAP_EINVAL;
+  *info = ctx->info;
+  return LYAP_OK;
+}
+
+int lyap_get_stats(const lyap_ctx* ctx, lyap_stats* st) {
+  if (!ctx || !st) return LYAP_EINVAL;
+  *st = ctx->stats;
+  return LYAP_OK;
+}
+
+int lyap_reset_stats(lyap_ctx* ctx) {
+  if (!ctx) return LYAP_EINVAL;
+  ctx->stats = lyap_stats{};
+  return LYAP_OK;
+}
+
+int lyap_export_state(const lyap_ctx* cctx, double* lam, double* bhr, double* btl, double* F, double* g0,
+                      double* hf) {
+  lyap_ctx* ctx = const_cast<lyap_ctx*>(cctx);
+  if (!ctx) return LYAP_EINVAL;
+  try {
+    CK(cudaSetDevice(ctx->device));
+    const Seed& s = ctx->seed;
+    if (lam) CK(cudaMemcpy(lam, s.lam, 2 * s.n * 8, cudaMemcpyDeviceToHost));
+    if (bhr) CK(cudaMemcpy(bhr, s.bhr, s.n * s.k * 8, cudaMemcpyDeviceToHost));
+    if (btl) CK(cudaMemcpy(btl, s.btl, s.n * s.k * 8, cudaMemcpyDeviceToHost));
+    if (F) CK(cudaMemcpy(F, s.F, s.nrep * s.k * s.k * 2 * 8, cudaMemcpyDeviceToHost));
+    if (g0) CK(cudaMemcpy(g0, s.g0, s.k * s.npad * 8, cudaMemcpyDeviceToHost));
+    if (hf) CK(cudaMemcpy(hf, s.hf, s.k * s.npad * 8, cudaMemcpyDeviceToHost));
+  } catch (Fail f) {
+    return f.code;
+  }
+  return LYAP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,193 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle and independent references.
+
+Tolerance (north star, BASELINE.json): relative error <= 1e-9 in FP64 on every trace.
+"""
+import json
+import pathlib
+
+import numpy as np
+import pytest
+import scipy.linalg
+
+import oracle
+import workloads
+
+pytestmark = pytest.mark.gpu
+GOLDEN = pathlib.Path(__file__).parent / "golden"
+RTOL = 1e-9
+
+
+def _problem(*args, **kw):
+    from paper_2312_08201_b200 import Problem
+    return Problem(*args, **kw)
+
+
+def rel_err(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return np.abs(a - b) / np.maximum(np.abs(b), 1e-300)
+
+
+# ----------------------------------------------------------------------------- K1 unit test
+def _complex_factors(st, n):
+    """Full eigen-index complex lambda, B^r, B~l from the exported folded state."""
+    npairs = st["n_pairs"]
+    lam = st["lam"][:, 0] + 1j * st["lam"][:, 1]
+    br = st["bhr"].astype(complex)
+    bl = st["btl"].astype(complex)
+    for r in range(npairs):
+        c = 2 * r
+        lam[c + 1] = np.conj(lam[c])
+        zr = st["bhr"][c] + 1j * st["bhr"][c + 1]
+        zl = st["btl"][c] + 1j * st["btl"][c + 1]
+        br[c], br[c + 1] = zr, np.conj(zr)
+        bl[c], bl[c + 1] = zl, np.conj(zl)
+    return lam, br, bl
+
+
+def _fold(Gc, npairs, npad):
+    k, n = Gc.shape
+    X = np.zeros((k, npad))
+    for r in range(npairs):
+        X[:, 2 * r], X[:, 2 * r + 1] = Gc[:, 2 * r].real, Gc[:, 2 * r].imag
+    X[:, 2 * npairs:n] = Gc[:, 2 * npairs:n].real
+    return X
+
+
+def _unfold(X, npairs, n):
+    k = X.shape[0]
+    G = np.zeros((k, n), complex)
+    for r in range(npairs):
+        z = X[:, 2 * r] + 1j * X[:, 2 * r + 1]
+        G[:, 2 * r], G[:, 2 * r + 1] = z, np.conj(z)
+    G[:, 2 * npairs:n] = X[:, 2 * npairs:n]
+    return G
+
+
+@pytest.mark.parametrize("n,k,seed", [(7, 1, 0), (16, 2, 1), (33, 3, 2), (40, 4, 3), (130, 2, 4)])
+def test_k1_apply_against_paper_blocks(n, k, seed):
+    """K1 (folded DMMA GEMM + prologue + epilogue) against the complex operator built entrywise from
+    eqs. (N1M1), (N2M1), (N1M2) with the same seed factors."""
+    import torch
+    rng = np.random.default_rng(seed)
+    A0, Bl, Br, Q, E = workloads.random_stable(n, k, rng)
+    P = _problem(A0, Bl, Br, Q, E)
+    st = P.export_state()
+    npairs, npad = st["n_pairs"], st["npad"]
+    lam, br, bl = _complex_factors(st, n)
+    L = 1.0 / (lam[:, None] + lam[None, :])
+    F = np.einsum("ij,is,it->jst", L, br, bl)  # T_d blocks, eq. (N1M1) / (2,2) block
+    # exported F (reps only) agrees with the paper formula
+    reps = list(range(0, 2 * npairs, 2)) + list(range(2 * npairs, n))
+    Fx = st["F"][..., 0] + 1j * st["F"][..., 1]
+    np.testing.assert_allclose(Fx, F[reps], rtol=1e-11, atol=1e-11 * np.abs(F).max())
+    nvec = 5
+    Xs, sig = [], rng.uniform(-2, 3, (nvec, k))
+    Gs = []
+    for _ in range(nvec):
+        G = rng.standard_normal((k, n)) + 1j * rng.standard_normal((k, n))
+        G = _unfold(_fold(G, npairs, npad), npairs, n)  # conjugate-symmetric
+        Gs.append(G)
+        Xs.append(_fold(G, npairs, npad))
+    Y = P.apply_C(torch.tensor(np.stack(Xs), device="cuda"), torch.tensor(sig, device="cuda")).cpu().numpy()
+    for v in range(nvec):
+        G = Gs[v]
+        TG = np.einsum("jst,tj->sj", F, G) + np.einsum("jt,ij,is,ti->sj", bl, L, br, G)
+        expect = _fold(sig[v][:, None] * G - TG, npairs, npad)
+        scale = np.abs(expect).max()
+        np.testing.assert_allclose(Y[v], expect, rtol=0, atol=1e-12 * scale)
+        assert np.all(Y[v][:, n:] == 0.0)
+    P.close()
+
+
+def test_setup_spectrum_and_t0():
+    """Exported eigenvalues = eig(A0); t0 = trace(E X0) with X0 from an independent LAPACK solve."""
+    rng = np.random.default_rng(5)
+    n, k = 24, 3
+    A0, Bl, Br, Q, E = workloads.random_stable(n, k, rng)
+    P = _problem(A0, Bl, Br, Q, E)
+    st = P.export_state()
+    lam, _, _ = _complex_factors(st, n)
+    ref = np.linalg.eigvals(A0)
+    key = lambda z: (np.round(z.real, 9), np.round(z.imag, 9))
+    np.testing.assert_allclose(np.array(sorted(lam, key=key)), np.array(sorted(ref, key=key)), atol=1e-10)
+    X0 = scipy.linalg.solve_continuous_lyapunov(A0, -Q)
+    assert P.info["t0"] == pytest.approx(float(np.sum(0.5 * (E + E.T) * X0)), rel=1e-11)
+    P.close()
+
+
+# ----------------------------------------------------------------------------- parity vs oracle
+@pytest.mark.parametrize("n,k,seed,same_b", [(1, 1, 0, True), (6, 2, 1, False), (13, 3, 2, False),
+                                             (29, 4, 3, True), (40, 1, 4, False), (64, 2, 5, False)])
+def test_random_instances_all_v(n, k, seed, same_b):
+    rng = np.random.default_rng(50 + seed)
+    A0, Bl, Br, Q, E = workloads.random_stable(n, k, rng, same_b=same_b)
+    V = rng.uniform(0.05, 2.0, (37, k))  # ragged batch
+    P = _problem(A0, Bl, Br, Q, E, batch=8)
+    tau, st, ap, rs = P.trace_batch(V, return_diagnostics=True)
+    ref = oracle.trace_batch(A0, Bl, Br, Q, E, V)
+    assert np.all(st == 0), (st, rs)
+    assert rel_err(tau, ref).max() <= RTOL, rel_err(tau, ref).max()
+    assert np.all(rs <= 1e-12)
+    P.close()
+
+
+def test_scalar_closed_form():
+    """n = 1: A0 = -1, B = 1, Q = E = 1 -> tau(v) = 1/(2(1+v))."""
+    P = _problem(-np.eye(1), np.ones((1, 1)), np.ones((1, 1)), np.eye(1), np.eye(1))
+    v = np.array([[0.1], [1.0], [3.0], [250.0], [-0.5]])
+    np.testing.assert_allclose(P.trace_batch(v), 1.0 / (2.0 * (1.0 + v[:, 0])), rtol=1e-13)
+    P.close()
+
+
+def test_zero_and_negative_parameters():
+    """v_t = 0 means column t absent; negative v allowed."""
+    rng = np.random.default_rng(9)
+    A0, Bl, Br, Q, E = workloads.random_stable(20, 3, rng, shift=2.0)
+    V = np.array([[0.0, 0.5, 1.0], [0.3, 0.0, 0.0], [0.0, 0.0, 0.0], [-0.2, 0.4, -0.1], [1.0, 1.0, 1.0]])
+    P = _problem(A0, Bl, Br, Q, E)
+    tau = P.trace_batch(V)
+    ref = oracle.trace_batch(A0, Bl, Br, Q, E, V)
+    assert rel_err(tau, ref).max() <= RTOL
+    assert tau[2] == pytest.approx(P.info["t0"], rel=1e-13)
+    P.close()
+
+
+def test_device_path_equals_host_path_and_edge_batches():
+    import torch
+    W = workloads.make("c1")
+    P = _problem(W.A0, W.Bl, W.Br, W.Q, W.E)
+    h = P.trace_batch(W.V[:50])
+    d = P.trace_batch(torch.tensor(W.V[:50], device="cuda")).cpu().numpy()
+    assert rel_err(d, h).max() <= 1e-12
+    assert P.trace_batch(np.zeros((0, 2))).shape == (0,)
+    one = P.trace_batch(W.V[7:8])
+    assert one[0] == pytest.approx(h[7], rel=1e-11)
+    P.close()
+
+
+def test_cold_start_and_tiny_batch_agree():
+    W = workloads.make("c1")
+    idx = W.corner_indices()
+    a = _problem(W.A0, W.Bl, W.Br, W.Q, W.E, batch=3, warm_start=False).trace_batch(W.V[idx])
+    b = _problem(W.A0, W.Bl, W.Br, W.Q, W.E).trace_batch(W.V[idx])
+    assert rel_err(a, b).max() <= 1e-10
+
+
+def _golden(name):
+    return json.loads((GOLDEN / f"oracle_{name}.json").read_text())
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_config_full_batch_vs_oracle_samples(name):
+    """Full BASELINE config, whole grid in one trace_batch (the bench launch configuration); the
+    oracle traces of tests/golden (tools/make_golden.py: corners + centre + seeded sample)."""
+    g = _golden(name)
+    W = workloads.make(name)
+    P = _problem(W.A0, W.Bl, W.Br, W.Q, W.E)
+    tau, st, ap, rs = P.trace_batch(W.V, return_diagnostics=True)
+    idx = np.array(g["indices"])
+    err = rel_err(tau[idx], np.array(g["traces"]))
+    assert np.all(st == 0), np.nonzero(st)
+    assert err.max() <= RTOL, (err.max(), idx[np.argmax(err)])
+    assert np.all(np.isfinite(tau))
+    P.close()
