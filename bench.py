@@ -100,9 +100,16 @@ class Clocks:
 _WK = {}
 
 
+_THREAD_VARS = ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS", "BLIS_NUM_THREADS")
+
+
 def _oracle_worker_init(name):
+    # one BLAS thread per worker process: the env is inherited from the parent (set before the
+    # pool starts) and threadpoolctl re-limits every BLAS already loaded (numpy's and scipy's)
+    import scipy.linalg  # noqa: F401  (load scipy's OpenBLAS before limiting)
     from threadpoolctl import threadpool_limits
     threadpool_limits(1)
+    import oracle  # noqa: F401
     import workloads
     _WK["W"] = workloads.make(name)
 
@@ -120,6 +127,9 @@ def oracle_rate(name: str, seconds: float, seed: int = 0):
     import workloads
     W = workloads.make(name)
     cores = os.cpu_count() or 1
+    saved = {v: os.environ.get(v) for v in _THREAD_VARS}
+    for v in _THREAD_VARS:
+        os.environ[v] = "1"
     ctx = mp.get_context("spawn")
     with ctx.Pool(cores, initializer=_oracle_worker_init, initargs=(name,)) as pool:
         pool.map(_oracle_one, [W.corner_indices()[0]] * cores)  # warm workers, size the sample
@@ -131,6 +141,11 @@ def oracle_rate(name: str, seconds: float, seed: int = 0):
         t = time.perf_counter()
         pool.map(_oracle_one, [int(i) for i in idx], chunksize=1)
         el = time.perf_counter() - t
+    for v, val in saved.items():
+        if val is None:
+            os.environ.pop(v, None)
+        else:
+            os.environ[v] = val
     return len(idx) / el, cores, len(idx), el
 
 

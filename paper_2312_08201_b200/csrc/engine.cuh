@@ -27,7 +27,7 @@ struct EngArgs {
   int max_restarts, warm;
   const double *V, *g0, *hf, *F;
   double *X, *Xin, *Qb, *Minv, *sigma, *mask, *eta, *H, *e, *y, *bnorm, *part, *part3;
-  int *phase, *m, *vidx, *applies, *restarts, *ctrl, *newv;
+  int *phase, *m, *vidx, *applies, *restarts, *ctrl, *newv, *alist;
   double* traces;
   int32_t* status;
   int32_t* out_applies;
@@ -84,9 +84,21 @@ __global__ void k_assign(EngArgs a) {
     }
   }
   __syncthreads();
-  // active slots after assignment
-  int act = (tid < a.b) ? (a.phase[tid] != PH_IDLE) : 0;
-  act = __syncthreads_count(act);
+  // active slots after assignment (VERIFY or ITER), compacted in slot order for K1
+  int isact = (tid < a.b) ? (a.phase[tid] != PH_IDLE) : 0;
+  int xa = isact;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, xa, o);
+    if (lane >= o) xa += y;
+  }
+  __syncthreads();
+  if (lane == 31) wsum[w] = xa;
+  __syncthreads();
+  int offa = 0;
+  for (int i = 0; i < w; ++i) offa += wsum[i];
+  if (isact) a.alist[offa + xa - 1] = tid;
+  const int act = __syncthreads_count(isact);
   if (tid == 0) {
     a.ctrl[0] = base + total;
     a.ctrl[2] = act;
@@ -216,6 +228,18 @@ __global__ void __launch_bounds__(128) k_prec(EngArgs a) {
   }
 }
 
+// DGKS criterion ("twice is enough"): reorthogonalise only if ||w'||^2 < ||w||^2 / 2 after the first
+// classical Gram-Schmidt pass.  part3[slot][c] = (||w'||^2, ||w||^2, ||w''||^2) partial sums.
+__device__ __forceinline__ bool needs_reorth(const EngArgs& a, int slot) {
+  const double* p = a.part3 + (int64_t)slot * a.nchunk * 3;
+  double s0 = 0.0, s1 = 0.0;
+  for (int c = 0; c < a.nchunk; ++c) {
+    s0 += p[c * 3];
+    s1 += p[c * 3 + 1];
+  }
+  return s0 < 0.5 * s1;
+}
+
 // ---------------------------------------------------------------- CGS2 dot products (K3)
 // ITER: part[slot][i][chunk] = q^_i . w over the chunk (w = candidate q^_{m+1}), i <= m.
 // VERIFY (pass 1): part3[slot][chunk] = (||R||^2, ||rhs||^2, <hf, X>) with R in q^_0.
@@ -254,11 +278,19 @@ __global__ void __launch_bounds__(256) k_dots(EngArgs a, int pass) {
     return;
   }
   if (ph != PH_ITER) return;
+  if (pass == 2 && !needs_reorth(a, slot)) return;
   const int m = a.m[slot];
   const double* w = a.Qb + slot * qs + (int64_t)(m + 1) * a.L;
+  double nw = 0.0;
   for (int i = threadIdx.x; i < RED_CE; i += blockDim.x) {
     const int64_t e = e0 + i;
-    ws[i] = e < a.L ? w[e] : 0.0;
+    const double v = e < a.L ? w[e] : 0.0;
+    ws[i] = v;
+    nw += v * v;
+  }
+  if (pass == 1) {
+    nw = block_sum(nw, red);
+    if (threadIdx.x == 0) a.part3[((int64_t)slot * a.nchunk + chunk) * 3 + 1] = nw;
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -285,6 +317,7 @@ __global__ void __launch_bounds__(256) k_upd(EngArgs a, int pass) {
   __shared__ double red[8];
   const int slot = blockIdx.y, chunk = blockIdx.x;
   if (a.phase[slot] != PH_ITER) return;
+  if (pass == 2 && !needs_reorth(a, slot)) return;
   const int m = a.m[slot];
   const int64_t qs = (int64_t)(a.mmax + 1) * a.L;
   const double* eta = a.eta + (int64_t)slot * (a.mmax + 1);
@@ -320,7 +353,7 @@ __global__ void __launch_bounds__(256) k_upd(EngArgs a, int pass) {
     nrm += v * v;
   }
   nrm = block_sum(nrm, red);
-  if (threadIdx.x == 0) a.part3[((int64_t)slot * a.nchunk + chunk) * 3] = nrm;
+  if (threadIdx.x == 0) a.part3[((int64_t)slot * a.nchunk + chunk) * 3 + (pass == 1 ? 0 : 2)] = nrm;
 }
 
 // ---------------------------------------------------------------- per-slot control (K4)
@@ -371,8 +404,9 @@ __global__ void __launch_bounds__(128) k_ctrl(EngArgs a) {
   double* Hc = H + (int64_t)m * ld;
   int done = 0;
   if (lane == 0) {
+    const int col = needs_reorth(a, slot) ? 2 : 0;  // same decision the pass-2 kernels took
     double s = 0.0;
-    for (int c = 0; c < a.nchunk; ++c) s += p3[c * 3];
+    for (int c = 0; c < a.nchunk; ++c) s += p3[c * 3 + col];
     const double hn = sqrt(s);
     a.applies[slot] += 1;
     eta[m + 1] = hn > 0.0 ? hn : 1.0;

@@ -35,8 +35,13 @@ struct K1Args {
   double* Qb;          // engine: basis (nslot x (mmax+1) x L)
   int64_t qstride;     // (mmax+1) * L
   double* Yout;        // apply mode output (nslot x L)
-  const int* nactive;  // engine: skip everything if *nactive == 0 (may be null)
+  const int* nactive;  // engine: number of active slots (null: all nslot vectors are active)
+  const int* alist;    // engine: active slot ids, compacted (null: identity)
 };
+
+// GEMM column block p (of k^2 columns) belongs to active position p -> slot alist[p]
+__device__ __forceinline__ int k1_nact(const K1Args& a) { return a.nactive ? *a.nactive : a.nslot; }
+__device__ __forceinline__ int k1_slot(const K1Args& a, int pos) { return a.alist ? a.alist[pos] : pos; }
 
 enum : int { PH_FREE = 0, PH_IDLE = 1, PH_VERIFY = 2, PH_ITER = 3, PH_XUPD = 4, PH_NEW = 5 };
 
@@ -45,21 +50,22 @@ enum : int { PH_FREE = 0, PH_IDLE = 1, PH_VERIFY = 2, PH_ITER = 3, PH_XUPD = 4, 
 template <int K>
 __global__ void __launch_bounds__(256) k1_gen(K1Args a, const double* __restrict__ bhr, int npad,
                                                int two_np, double* __restrict__ Bop, int64_t ncol) {
-  if (a.nactive && *a.nactive == 0) return;
   constexpr int TS = K1Tile<K>::TS, NC = K1Tile<K>::NC, TC = K1_TILE_C;
+  const int nact = k1_nact(a);
+  const int i0 = blockIdx.x * TC, s0 = blockIdx.y * TS;
+  if (s0 >= nact) return;
   __shared__ double xs[TS][K][TC];
   __shared__ double bs[TC][K];
-  const int i0 = blockIdx.x * TC, s0 = blockIdx.y * TS;
   for (int idx = threadIdx.x; idx < TS * K * TC; idx += blockDim.x) {
     int sl = idx / (K * TC), t = (idx / TC) % K, c = idx % TC;
-    xs[sl][t][c] = (s0 + sl < a.nslot) ? a.Xin[(int64_t)(s0 + sl) * a.L + (int64_t)t * npad + i0 + c] : 0.0;
+    xs[sl][t][c] = (s0 + sl < nact) ? a.Xin[(int64_t)k1_slot(a, s0 + sl) * a.L + (int64_t)t * npad + i0 + c] : 0.0;
   }
   for (int idx = threadIdx.x; idx < TC * K; idx += blockDim.x) bs[idx / K][idx % K] = bhr[(int64_t)i0 * K + idx];
   __syncthreads();
   for (int idx = threadIdx.x; idx < TC * NC; idx += blockDim.x) {
     int r = idx / NC, col = idx % NC;
     int sl = col / (K * K), s = (col / K) % K, t = col % K;
-    if (s0 + sl >= a.nslot) continue;
+    if (s0 + sl >= nact) continue;
     int c = i0 + r;
     double val;
     if (c < two_np) {  // conjugate pair: (br + i bi)(x + i y)
@@ -91,11 +97,11 @@ struct DgemmCfg {
 template <int BM, int BN, int WM, int WN, int STAGES>
 __global__ void __launch_bounds__(DgemmCfg<BM, BN, WM, WN, STAGES>::THREADS, 1)
     k1_dgemm(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C, int M,
-             int N, int Kd, const int* __restrict__ nactive) {
+             int N, int Kd, const int* __restrict__ nactive, int cols_per_active) {
   using Cfg = DgemmCfg<BM, BN, WM, WN, STAGES>;
   constexpr int BK = Cfg::BK, AST = Cfg::AST, BST = Cfg::BST, NT = Cfg::THREADS;
   constexpr int MT = WM / 8, NTL = WN / 8;
-  if (nactive && *nactive == 0) return;
+  if (nactive && (int)blockIdx.x * BN >= (*nactive) * cols_per_active) return;  // no active column
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
   double* Bs = smem + STAGES * Cfg::A_STAGE;
@@ -178,24 +184,25 @@ __global__ void __launch_bounds__(256) k1_epi(K1Args a, const double* __restrict
                                                const double* __restrict__ btl, const double* __restrict__ F,
                                                const double* __restrict__ g0, int npad, int two_np, int npairs,
                                                int n) {
-  if (a.nactive && *a.nactive == 0) return;
   constexpr int TS = K1Tile<K>::TS, NC = K1Tile<K>::NC, TC = K1_TILE_C;
+  const int nact = k1_nact(a);
+  const int i0 = blockIdx.x * TC, s0 = blockIdx.y * TS;
+  if (s0 >= nact) return;
   __shared__ double us[TC][NC + 1];
   __shared__ double xs[TS][K][TC];
-  const int i0 = blockIdx.x * TC, s0 = blockIdx.y * TS;
   for (int idx = threadIdx.x; idx < TC * NC; idx += blockDim.x) {
     int r = idx / NC, col = idx % NC;
-    us[r][col] = (s0 + col / (K * K) < a.nslot) ? U[(int64_t)(i0 + r) * ncol + (int64_t)s0 * K * K + col] : 0.0;
+    us[r][col] = (s0 + col / (K * K) < nact) ? U[(int64_t)(i0 + r) * ncol + (int64_t)s0 * K * K + col] : 0.0;
   }
   for (int idx = threadIdx.x; idx < TS * K * TC; idx += blockDim.x) {
     int sl = idx / (K * TC), t = (idx / TC) % K, c = idx % TC;
-    xs[sl][t][c] = (s0 + sl < a.nslot) ? a.Xin[(int64_t)(s0 + sl) * a.L + (int64_t)t * npad + i0 + c] : 0.0;
+    xs[sl][t][c] = (s0 + sl < nact) ? a.Xin[(int64_t)k1_slot(a, s0 + sl) * a.L + (int64_t)t * npad + i0 + c] : 0.0;
   }
   __syncthreads();
   for (int idx = threadIdx.x; idx < TS * K * TC; idx += blockDim.x) {
     int sl = idx / (K * TC), s = (idx / TC) % K, r = idx % TC;
-    int slot = s0 + sl;
-    if (slot >= a.nslot) continue;
+    if (s0 + sl >= nact) continue;
+    const int slot = k1_slot(a, s0 + sl);
     int c = i0 + r;
     double* dst;
     bool verify = false;

@@ -157,7 +157,7 @@ void ensure_engine(lyap_ctx* ctx, int b, int mmax) {
   g.m = dalloc<int>(ctx, b);
   g.vidx = dalloc<int>(ctx, b);
   g.applies = dalloc<int>(ctx, b);
-  g.restarts = dalloc<int>(ctx, 2 * (size_t)b);  // restarts | newv
+  g.restarts = dalloc<int>(ctx, 3 * (size_t)b);  // restarts | newv | alist
   g.ctrl = dalloc<int>(ctx, 8);
   CK(cudaMallocHost(&g.h_ctrl, 8 * sizeof(int)));
   ctx->info.batch = b;
@@ -183,7 +183,7 @@ void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, EvPool* pool) {
     dim3 grid((unsigned)(g.ncol / G_BN), (unsigned)(s.npad / G_BM));
     if (pool) CK(cudaEventRecord(pool->ev[2 * pool->used], st));
     k1_dgemm<G_BM, G_BN, G_WM, G_WN, G_ST><<<grid, GCfg::THREADS, GCfg::SMEM, st>>>(
-        s.Lf, g.Bop, g.U, (int)s.npad, (int)g.ncol, (int)s.npad, a.nactive);
+        s.Lf, g.Bop, g.U, (int)s.npad, (int)g.ncol, (int)s.npad, a.nactive, (int)(s.k * s.k));
     LAUNCHED();
     if (pool) {
       CK(cudaEventRecord(pool->ev[2 * pool->used + 1], st));
@@ -220,7 +220,7 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, double* dtr, int32_t*
   CK(cudaMemsetAsync(g.phase, 0, sizeof(int) * b, st));  // PH_FREE
   CK(cudaMemsetAsync(g.ctrl, 0, sizeof(int) * 8, st));
   CK(cudaMemsetAsync(g.X, 0, sizeof(double) * (size_t)b * g.L, st));
-  CK(cudaMemsetAsync(g.restarts, 0, sizeof(int) * 2 * (size_t)b, st));
+  CK(cudaMemsetAsync(g.restarts, 0, sizeof(int) * 3 * (size_t)b, st));
 
   EngArgs a{};
   a.b = b;
@@ -262,6 +262,7 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, double* dtr, int32_t*
   a.applies = g.applies;
   a.restarts = g.restarts;
   a.newv = g.restarts + b;
+  a.alist = g.restarts + 2 * b;
   a.ctrl = g.ctrl;
   a.traces = dtr;
   a.status = dst;
@@ -280,6 +281,7 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, double* dtr, int32_t*
   k1.Qb = g.Qb;
   k1.qstride = (int64_t)(mmax + 1) * g.L;
   k1.nactive = g.ctrl + 2;
+  k1.alist = g.restarts + 2 * b;
 
   EvPool pool;
   EvPool* pp = nullptr;
@@ -776,6 +778,7 @@ int lyap_apply_C(lyap_ctx* ctx, int64_t nvec, const double* X, const double* sig
       a.sigma = sigma ? sigma + v0 * ctx->seed.k : nullptr;
       a.Yout = Y + v0 * g.L;
       a.nactive = nullptr;
+      a.alist = nullptr;
       if (nb < g.b) CK(cudaMemsetAsync(g.Bop, 0, sizeof(double) * ctx->seed.npad * g.ncol, st));
       launch_k1(ctx, a, st, nullptr);
       ctx->stats.k1_vectors += nb;
