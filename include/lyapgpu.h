@@ -60,6 +60,10 @@ typedef struct {
   double max_cond_S;   /* setup fails with LYAP_EEIG above this 1-norm condition of S (1e8) */
   int32_t device;      /* CUDA device ordinal (default: current device) */
   int32_t profile;     /* 1: time every K1 GEMM launch with CUDA events (lyap_get_stats) */
+  int32_t schedule;    /* 1 (default): solve v's in descending order of the cost proxy
+                          sum_t |v_t| ||B~l_t|| ||B^r_t|| (largest perturbation first, so the slow
+                          systems do not form a tail); 0: in row order of V.  Results are returned
+                          in row order either way. */
 } lyap_opts;
 
 typedef struct {

@@ -24,7 +24,7 @@ EXPORTED = ("lyap_default_opts", "lyap_setup", "lyap_trace_batch", "lyap_trace_b
 class Opts(C.Structure):
     _fields_ = [("tol", C.c_double), ("max_dim", C.c_int32), ("max_restarts", C.c_int32),
                 ("batch", C.c_int32), ("warm_start", C.c_int32), ("max_cond_S", C.c_double),
-                ("device", C.c_int32), ("profile", C.c_int32)]
+                ("device", C.c_int32), ("profile", C.c_int32), ("schedule", C.c_int32)]
 
 
 class Info(C.Structure):

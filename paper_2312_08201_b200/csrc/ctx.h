@@ -25,6 +25,7 @@ struct Seed {
   double* hf = nullptr;   // k x npad folded trace weights (tau = t0 + 2 <g, hf>)
   double* Lf = nullptr;   // npad x npad folded Cauchy matrix (K1's A operand), row-major
   double t0 = 0.0;
+  double wcost[LYAP_KMAX] = {};  // ||B~l_t|| ||B^r_t||: weights of the scheduling cost proxy
 };
 
 // Batched Krylov engine buffers (slot-major).
@@ -46,6 +47,8 @@ struct Engine {
   int *phase = nullptr, *m = nullptr, *vidx = nullptr, *applies = nullptr, *restarts = nullptr;
   int* ctrl = nullptr;                            // [0]=next v, [1]=done count, [2]=active slots
   int* h_ctrl = nullptr;                          // pinned mirror
+  int* order = nullptr;                           // queue order (nv_cap)
+  int64_t order_cap = 0;
 };
 
 }  // namespace lyap

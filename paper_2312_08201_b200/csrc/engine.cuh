@@ -26,6 +26,7 @@ struct EngArgs {
   double tol, tol_inner, t0;
   int max_restarts, warm;
   const double *V, *g0, *hf, *F;
+  const int* order;  // queue position -> row of V (null: identity)
   double *X, *Xin, *Qb, *Minv, *sigma, *mask, *eta, *H, *e, *y, *bnorm, *part, *part3;
   int *phase, *m, *vidx, *applies, *restarts, *ctrl, *newv, *alist;
   double* traces;
@@ -67,8 +68,9 @@ __global__ void k_assign(EngArgs a) {
   const int pos = off + x - flag;
   const int base = base_s;
   if (tid < a.b && flag) {
-    const int idx = base + pos;
-    if (idx < a.nv) {
+    const int qpos = base + pos;
+    if (qpos < a.nv) {
+      const int idx = a.order ? a.order[qpos] : qpos;
       a.vidx[tid] = idx;
       for (int t = 0; t < a.K; ++t) {
         const double v = a.V[(int64_t)idx * a.K + t];

@@ -101,12 +101,19 @@ using GCfg = DgemmCfg<G_BM, G_BN, G_WM, G_WN, G_ST>;
   }
 
 // ------------------------------------------------------------------ engine allocation
-void free_engine(Engine& g) {
+void free_engine(Engine& g, bool keep_order = true) {
   void* ps[] = {g.Bop, g.U, g.Xin, g.X, g.Qb, g.Minv, g.sigma, g.mask, g.eta, g.H, g.e, g.y,
                 g.bnorm, g.part, g.part3, g.phase, g.m, g.vidx, g.applies, g.restarts, g.ctrl};
   for (void* p : ps) dfree(p);
   if (g.h_ctrl) cudaFreeHost(g.h_ctrl);
+  int* order = g.order;
+  const int64_t cap = g.order_cap;
+  if (!keep_order) dfree(order);
   g = Engine{};
+  if (keep_order) {
+    g.order = order;
+    g.order_cap = cap;
+  }
 }
 
 int auto_batch(const lyap_ctx* ctx, int64_t nv) {
@@ -211,8 +218,8 @@ void drain_pool(lyap_ctx* ctx, EvPool& pool) {
 }
 
 // ------------------------------------------------------------------ the batched engine
-int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, double* dtr, int32_t* dst, int32_t* dap,
-              double* dres, cudaStream_t st) {
+int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, double* dtr, int32_t* dst,
+              int32_t* dap, double* dres, cudaStream_t st) {
   const Seed& s = ctx->seed;
   const int b = auto_batch(ctx, nv), mmax = auto_mmax(ctx);
   ensure_engine(ctx, b, mmax);
@@ -240,6 +247,7 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, double* dtr, int32_t*
   a.max_restarts = ctx->opts.max_restarts;
   a.warm = ctx->opts.warm_start;
   a.V = dV;
+  a.order = dorder;
   a.g0 = s.g0;
   a.hf = s.hf;
   a.F = s.F;
@@ -369,6 +377,7 @@ void lyap_default_opts(lyap_opts* o) {
   o->max_cond_S = 1e8;
   o->device = -1;
   o->profile = 0;
+  o->schedule = 1;
 }
 
 const char* lyap_last_error(const lyap_ctx* c) { return c ? c->err.c_str() : g_last_error.c_str(); }
@@ -376,7 +385,7 @@ const char* lyap_last_error(const lyap_ctx* c) { return c ? c->err.c_str() : g_l
 static void destroy_impl(lyap_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
-  free_engine(c->eng);
+  free_engine(c->eng, false);
   Seed& s = c->seed;
   void* ps[] = {s.lam, s.bhr, s.btl, s.F, s.g0, s.hf, s.Lf};
   for (void* p : ps) dfree(p);
@@ -656,6 +665,19 @@ int lyap_setup(int64_t n, int64_t k, const double* A0, const double* Bl, const d
               maxl);
       throw Fail{LYAP_ESINGULAR};
     }
+    {  // scheduling weights ||B~l_t|| ||B^r_t|| (folded coordinates)
+      std::vector<double> hb((size_t)s.npad * k), hr((size_t)s.npad * k);
+      CK(cudaMemcpy(hb.data(), s.btl, hb.size() * 8, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(hr.data(), s.bhr, hr.size() * 8, cudaMemcpyDeviceToHost));
+      for (int64_t t = 0; t < k; ++t) {
+        double nb = 0.0, nr = 0.0;
+        for (int64_t c = 0; c < s.npad; ++c) {
+          nb += hb[c * k + t] * hb[c * k + t];
+          nr += hr[c * k + t] * hr[c * k + t];
+        }
+        s.wcost[t] = std::sqrt(nb * nr);
+      }
+    }
     if (!std::isfinite(s.t0)) {
       set_err(ctx, "seed trace t0 is not finite");
       throw Fail{LYAP_EEIG};
@@ -709,9 +731,36 @@ int lyap_trace_batch_ex(lyap_ctx* ctx, int64_t nv, const double* V, double* trac
       dap = applies;
       dres = resid;
     }
-    int* dbad = nullptr;
-    rc = run_batch(ctx, nv, dV, dtr, dst, dap, dres, st);
-    (void)dbad;
+    // schedule: expensive (large-perturbation) v first, so slow systems do not form a tail
+    const int* dorder = nullptr;
+    if (ctx->opts.schedule) {
+      std::vector<double> hV((size_t)nv * k);
+      if (own) {
+        std::memcpy(hV.data(), V, hV.size() * 8);
+      } else {
+        CK(cudaMemcpyAsync(hV.data(), V, hV.size() * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+      }
+      std::vector<double> cost(nv);
+      for (int64_t i = 0; i < nv; ++i) {
+        double c = 0.0;
+        for (int64_t t = 0; t < k; ++t) c += std::fabs(hV[i * k + t]) * ctx->seed.wcost[t];
+        cost[i] = c;
+      }
+      std::vector<int> ord(nv);
+      for (int64_t i = 0; i < nv; ++i) ord[i] = (int)i;
+      std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return cost[x] > cost[y]; });
+      Engine& g = ctx->eng;
+      if (g.order_cap < nv) {
+        dfree(g.order);
+        g.order = dalloc<int>(ctx, nv, false);
+        g.order_cap = nv;
+      }
+      CK(cudaMemcpyAsync(g.order, ord.data(), nv * sizeof(int), cudaMemcpyHostToDevice, st));
+      CK(cudaStreamSynchronize(st));
+      dorder = g.order;
+    }
+    rc = run_batch(ctx, nv, dV, dorder, dtr, dst, dap, dres, st);
     if (rc == LYAP_OK) {
       // any per-v failure -> LYAP_EPARTIAL
       std::vector<int32_t> hs;

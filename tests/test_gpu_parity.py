@@ -191,3 +191,13 @@ def test_config_full_batch_vs_oracle_samples(name):
     assert err.max() <= RTOL, (err.max(), idx[np.argmax(err)])
     assert np.all(np.isfinite(tau))
     P.close()
+
+
+def test_schedule_does_not_change_results():
+    """Cost-ordered scheduling only permutes the work: traces come back in row order of V."""
+    W = workloads.make("c1")
+    a = _problem(W.A0, W.Bl, W.Br, W.Q, W.E, schedule=True, batch=16).trace_batch(W.V)
+    b = _problem(W.A0, W.Bl, W.Br, W.Q, W.E, schedule=False, batch=16).trace_batch(W.V)
+    assert rel_err(a, b).max() <= 1e-10
+    g = _golden("c1")
+    assert rel_err(a[np.array(g["indices"])], np.array(g["traces"])).max() <= RTOL
