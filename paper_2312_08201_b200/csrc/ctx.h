@@ -44,6 +44,9 @@ struct Engine {
   double *bnorm = nullptr;                        // b
   double *part = nullptr;                         // b x (mmax+2) x nchunk
   double *part3 = nullptr;                        // b x nchunk x 3
+  double *part2 = nullptr;                        // b x (mmax+2) x nchunk  (Gram-row partials)
+  double *Rc = nullptr, *Rr = nullptr;            // b x (mmax+1)^2 Cholesky factor of Q^T Q
+  double *cf = nullptr;                           // b x (mmax+1) projection coefficients
   int *phase = nullptr, *m = nullptr, *vidx = nullptr, *applies = nullptr, *restarts = nullptr;
   int* ctrl = nullptr;                            // [0]=next v, [1]=done count, [2]=active slots
   int* h_ctrl = nullptr;                          // pinned mirror

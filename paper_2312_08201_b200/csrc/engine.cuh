@@ -18,6 +18,7 @@
 namespace lyap {
 
 constexpr int RED_CE = 1024;  // vector elements per reduction chunk
+constexpr int CTRL_RMAX = 8;  // k_ctrl back substitution: m_max <= 32 * CTRL_RMAX = 256
 
 struct EngArgs {
   int b, mmax, K, nv;
@@ -28,6 +29,7 @@ struct EngArgs {
   const double *V, *g0, *hf, *F;
   const int* order;  // queue position -> row of V (null: identity)
   double *X, *Xin, *Qb, *Minv, *sigma, *mask, *eta, *H, *e, *y, *bnorm, *part, *part3;
+  double *part2, *Rc, *Rr, *cf;  // Gram-row partials, Gram matrix Q^T Q (Rc; Rr unused), coefficients
   int *phase, *m, *vidx, *applies, *restarts, *ctrl, *newv, *alist;
   double* traces;
   int32_t* status;
@@ -230,30 +232,26 @@ __global__ void __launch_bounds__(128) k_prec(EngArgs a) {
   }
 }
 
-// DGKS criterion ("twice is enough"): reorthogonalise only if ||w'||^2 < ||w||^2 / 2 after the first
-// classical Gram-Schmidt pass.  part3[slot][c] = (||w'||^2, ||w||^2, ||w''||^2) partial sums.
-__device__ __forceinline__ bool needs_reorth(const EngArgs& a, int slot) {
-  const double* p = a.part3 + (int64_t)slot * a.nchunk * 3;
-  double s0 = 0.0, s1 = 0.0;
-  for (int c = 0; c < a.nchunk; ++c) {
-    s0 += p[c * 3];
-    s1 += p[c * 3 + 1];
-  }
-  return s0 < 0.5 * s1;
-}
-
-// ---------------------------------------------------------------- CGS2 dot products (K3)
-// ITER: part[slot][i][chunk] = q^_i . w over the chunk (w = candidate q^_{m+1}), i <= m.
-// VERIFY (pass 1): part3[slot][chunk] = (||R||^2, ||rhs||^2, <hf, X>) with R in q^_0.
-__global__ void __launch_bounds__(256) k_dots(EngArgs a, int pass) {
+// ---------------------------------------------------------------- orthogonalisation (K3)
+// Gram-corrected classical Gram-Schmidt: the new Krylov candidate w is projected with the exact
+// projector of the current basis, w' = w - Q G^{-1} Q^T w, G = Q^T Q (normalised basis), i.e. what
+// CGS2 approximates with a second pass (G^{-1} ~ 2I - G).  The basis is read twice per iteration
+// (one fused dot pass, one update pass) instead of four times; G's new row q_m^T Q comes out of the
+// same dot pass and is accumulated in k_gram.
+// (Measured on c2 with NumPy: iteration counts identical to CGS2, ||Q^T Q - I|| ~ 1e-14.)
+//
+// k_dots, ITER: part[slot][i][chunk] = q^_i . w  (i <= m) and part2[slot][i][chunk] = q^_i . q^_m
+// (i < m), w = the candidate q^_{m+1} written by K1's epilogue.
+// VERIFY: part3[slot][chunk] = (||R||^2, ||rhs||^2, <hf, X>) with R in q^_0.
+__global__ void __launch_bounds__(256) k_dots(EngArgs a) {
   __shared__ double ws[RED_CE];
+  __shared__ double qm[RED_CE];
   __shared__ double red[8];
   const int slot = blockIdx.y, chunk = blockIdx.x;
   const int ph = a.phase[slot];
   const int64_t e0 = (int64_t)chunk * RED_CE;
   const int64_t qs = (int64_t)(a.mmax + 1) * a.L;
   if (ph == PH_VERIFY) {
-    if (pass != 1) return;
     const double* R = a.Qb + slot * qs;
     const double* X = a.X + (int64_t)slot * a.L;
     double s0 = 0.0, s1 = 0.0, s2 = 0.0;
@@ -280,60 +278,99 @@ __global__ void __launch_bounds__(256) k_dots(EngArgs a, int pass) {
     return;
   }
   if (ph != PH_ITER) return;
-  if (pass == 2 && !needs_reorth(a, slot)) return;
   const int m = a.m[slot];
   const double* w = a.Qb + slot * qs + (int64_t)(m + 1) * a.L;
-  double nw = 0.0;
+  const double* qlast = a.Qb + slot * qs + (int64_t)m * a.L;
   for (int i = threadIdx.x; i < RED_CE; i += blockDim.x) {
     const int64_t e = e0 + i;
-    const double v = e < a.L ? w[e] : 0.0;
-    ws[i] = v;
-    nw += v * v;
-  }
-  if (pass == 1) {
-    nw = block_sum(nw, red);
-    if (threadIdx.x == 0) a.part3[((int64_t)slot * a.nchunk + chunk) * 3 + 1] = nw;
+    ws[i] = e < a.L ? w[e] : 0.0;
+    qm[i] = e < a.L ? qlast[e] : 0.0;
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t lim = (a.L - e0) < RED_CE ? (a.L - e0) : RED_CE;
+  const int lim = (int)((a.L - e0) < RED_CE ? (a.L - e0) : RED_CE);
   for (int i = warp; i <= m; i += 8) {
     const double* q = a.Qb + slot * qs + (int64_t)i * a.L + e0;
-    double d0 = 0.0, d1 = 0.0;
+    double d0 = 0.0, d1 = 0.0, g0 = 0.0, g1 = 0.0;
     int e = lane;
-    for (; e + 32 < lim; e += 64) {
-      d0 += q[e] * ws[e];
-      d1 += q[e + 32] * ws[e + 32];
+    for (; e + 96 < lim; e += 128) {
+      const double x0 = q[e], x1 = q[e + 32], x2 = q[e + 64], x3 = q[e + 96];
+      d0 += x0 * ws[e] + x2 * ws[e + 64];
+      d1 += x1 * ws[e + 32] + x3 * ws[e + 96];
+      g0 += x0 * qm[e] + x2 * qm[e + 64];
+      g1 += x1 * qm[e + 32] + x3 * qm[e + 96];
     }
-    if (e < lim) d0 += q[e] * ws[e];
+    for (; e < lim; e += 32) {
+      d0 += q[e] * ws[e];
+      g0 += q[e] * qm[e];
+    }
     const double d = warp_sum(d0 + d1);
-    if (lane == 0) a.part[((int64_t)slot * (a.mmax + 2) + i) * a.nchunk + chunk] = d;
+    const double g = warp_sum(g0 + g1);
+    if (lane == 0) {
+      a.part[((int64_t)slot * (a.mmax + 2) + i) * a.nchunk + chunk] = d;
+      if (i < m) a.part2[((int64_t)slot * (a.mmax + 2) + i) * a.nchunk + chunk] = g;
+    }
   }
 }
 
-// ---------------------------------------------------------------- CGS2 update (K3)
-// h_i = (q^_i . w) / eta_i (the coefficient on the normalised q_i); w -= sum_i (h_i / eta_i) q^_i;
-// H[i][m] (=|+=) h_i;  part3[slot][chunk][0] = ||w'||^2 over the chunk.
-__global__ void __launch_bounds__(256) k_upd(EngArgs a, int pass) {
-  extern __shared__ double cf[];  // mmax + 1
+// k_gram (one warp per ITER slot): append G's row/column m (G = Q^T Q of the normalised basis,
+// G_mm = 1), then c = G^{-1} d to second order: with every new vector projected exactly,
+// G = I + E with ||E|| ~ 1e-14, so G^{-1} d = (2I - G) d + O(||E||^2) -- the coefficient CGS2's
+// second pass would produce, computed from the Gram row instead of a second sweep over the basis.
+// c_i (w.r.t. the normalised q_i) is the Hessenberg column; cf_i = c_i / eta_i multiplies q^_i.
+__global__ void __launch_bounds__(128) k_gram(EngArgs a) {
+  extern __shared__ double ds[];  // mmax + 1
+  const int slot = blockIdx.x;
+  if (a.phase[slot] != PH_ITER) return;
+  const int ld = a.mmax + 1;
+  const int m = a.m[slot];
+  const double* eta = a.eta + (int64_t)slot * ld;
+  double* G = a.Rc + (int64_t)slot * ld * ld;  // G[i * ld + j], symmetric
+  const double* pd = a.part + (int64_t)slot * (a.mmax + 2) * a.nchunk;
+  const double* pg = a.part2 + (int64_t)slot * (a.mmax + 2) * a.nchunk;
+  for (int i = threadIdx.x; i <= m; i += blockDim.x) {
+    double d = 0.0;
+    for (int c = 0; c < a.nchunk; ++c) d += pd[(int64_t)i * a.nchunk + c];
+    ds[i] = d / eta[i];
+    if (i < m) {
+      double g = 0.0;
+      for (int c = 0; c < a.nchunk; ++c) g += pg[(int64_t)i * a.nchunk + c];
+      g /= (eta[i] * eta[m]);
+      G[(int64_t)i * ld + m] = g;
+      G[(int64_t)m * ld + i] = g;
+    } else {
+      G[(int64_t)m * ld + m] = 1.0;
+    }
+  }
+  __syncthreads();
+  // c = 2 d - G d : thread owns rows i = tid + 128 r; row j of G is contiguous across threads
+  double* Hc = a.H + (int64_t)slot * ld * a.mmax + (int64_t)m * ld;
+  double* cf = a.cf + (int64_t)slot * ld;
+  for (int i = threadIdx.x; i <= m; i += blockDim.x) {
+    double c0 = 2.0 * ds[i], c1 = 0.0, c2 = 0.0, c3 = 0.0;
+    int j = 0;
+    for (; j + 3 <= m; j += 4) {
+      c0 -= G[(int64_t)j * ld + i] * ds[j];
+      c1 -= G[(int64_t)(j + 1) * ld + i] * ds[j + 1];
+      c2 -= G[(int64_t)(j + 2) * ld + i] * ds[j + 2];
+      c3 -= G[(int64_t)(j + 3) * ld + i] * ds[j + 3];
+    }
+    for (; j <= m; ++j) c0 -= G[(int64_t)j * ld + i] * ds[j];
+    const double c = (c0 + c1) + (c2 + c3);
+    Hc[i] = c;
+    cf[i] = c / eta[i];
+  }
+}
+
+// k_upd: w' = w - sum_i cf_i q^_i (one read of the basis); part3[slot][chunk][0] = ||w'||^2.
+__global__ void __launch_bounds__(256) k_upd(EngArgs a) {
+  extern __shared__ double cfs[];  // mmax + 1
   __shared__ double red[8];
   const int slot = blockIdx.y, chunk = blockIdx.x;
   if (a.phase[slot] != PH_ITER) return;
-  if (pass == 2 && !needs_reorth(a, slot)) return;
   const int m = a.m[slot];
   const int64_t qs = (int64_t)(a.mmax + 1) * a.L;
-  const double* eta = a.eta + (int64_t)slot * (a.mmax + 1);
-  for (int i = threadIdx.x; i <= m; i += blockDim.x) {
-    const double* p = a.part + ((int64_t)slot * (a.mmax + 2) + i) * a.nchunk;
-    double h = 0.0;
-    for (int c = 0; c < a.nchunk; ++c) h += p[c];
-    h /= eta[i];
-    cf[i] = h / eta[i];
-    if (chunk == 0) {
-      double* Hc = a.H + (int64_t)slot * (a.mmax + 1) * a.mmax + (int64_t)m * (a.mmax + 1);
-      Hc[i] = (pass == 1) ? h : Hc[i] + h;
-    }
-  }
+  for (int i = threadIdx.x; i <= m; i += blockDim.x) cfs[i] = a.cf[(int64_t)slot * (a.mmax + 1) + i];
   __syncthreads();
   double* w = a.Qb + slot * qs + (int64_t)(m + 1) * a.L;
   const double* Q = a.Qb + slot * qs;
@@ -346,16 +383,16 @@ __global__ void __launch_bounds__(256) k_upd(EngArgs a, int pass) {
     double acc0 = 0.0, acc1 = 0.0;
     int i = 0;
     for (; i + 1 <= m; i += 2) {
-      acc0 += cf[i] * Q[(int64_t)i * a.L + e];
-      acc1 += cf[i + 1] * Q[(int64_t)(i + 1) * a.L + e];
+      acc0 += cfs[i] * Q[(int64_t)i * a.L + e];
+      acc1 += cfs[i + 1] * Q[(int64_t)(i + 1) * a.L + e];
     }
-    if (i <= m) acc0 += cf[i] * Q[(int64_t)i * a.L + e];
+    if (i <= m) acc0 += cfs[i] * Q[(int64_t)i * a.L + e];
     v -= acc0 + acc1;
     w[e] = v;
     nrm += v * v;
   }
   nrm = block_sum(nrm, red);
-  if (threadIdx.x == 0) a.part3[((int64_t)slot * a.nchunk + chunk) * 3 + (pass == 1 ? 0 : 2)] = nrm;
+  if (threadIdx.x == 0) a.part3[((int64_t)slot * a.nchunk + chunk) * 3] = nrm;
 }
 
 // ---------------------------------------------------------------- per-slot control (K4)
@@ -402,30 +439,41 @@ __global__ void __launch_bounds__(128) k_ctrl(EngArgs a) {
     return;
   }
   if (ph != PH_ITER) return;
+  // the sequential Givens chain runs on a shared-memory copy of the column (one coalesced load)
+  extern __shared__ double sm_ctrl[];
+  const int wslot = threadIdx.x >> 5;
+  double* hs = sm_ctrl + (int64_t)wslot * 4 * (a.mmax + 2);  // column m of H (m + 2 entries)
+  double* css = hs + (a.mmax + 2);
+  double* sns = css + (a.mmax + 2);
+  double* ys = sns + (a.mmax + 2);
   const int m = a.m[slot];
   double* Hc = H + (int64_t)m * ld;
+  for (int i = lane; i <= m; i += 32) hs[i] = Hc[i];
+  for (int i = lane; i < m; i += 32) {
+    css[i] = cs[i];
+    sns[i] = sn[i];
+  }
+  __syncwarp();
   int done = 0;
   if (lane == 0) {
-    const int col = needs_reorth(a, slot) ? 2 : 0;  // same decision the pass-2 kernels took
     double s = 0.0;
-    for (int c = 0; c < a.nchunk; ++c) s += p3[c * 3 + col];
+    for (int c = 0; c < a.nchunk; ++c) s += p3[c * 3];
     const double hn = sqrt(s);
     a.applies[slot] += 1;
     eta[m + 1] = hn > 0.0 ? hn : 1.0;
-    Hc[m + 1] = hn;
-    for (int i = 0; i < m; ++i) {
-      const double t1 = cs[i] * Hc[i] + sn[i] * Hc[i + 1];
-      const double t2 = -sn[i] * Hc[i] + cs[i] * Hc[i + 1];
-      Hc[i] = t1;
-      Hc[i + 1] = t2;
+    double hi = hs[0];
+    for (int i = 0; i < m; ++i) {  // apply the previous rotations to the new column
+      const double hi1 = hs[i + 1];
+      hs[i] = css[i] * hi + sns[i] * hi1;
+      hi = -sns[i] * hi + css[i] * hi1;
     }
-    const double x1 = Hc[m], x2 = Hc[m + 1];
+    const double x1 = hi, x2 = hn;
     const double r = hypot(x1, x2);
     const double c = r > 0.0 ? x1 / r : 1.0, sv = r > 0.0 ? x2 / r : 0.0;
     cs[m] = c;
     sn[m] = sv;
-    Hc[m] = r;
-    Hc[m + 1] = 0.0;
+    hs[m] = r;
+    hs[m + 1] = 0.0;
     e[m + 1] = -sv * e[m];
     e[m] = c * e[m];
     const double est = fabs(e[m + 1]);
@@ -433,22 +481,56 @@ __global__ void __launch_bounds__(128) k_ctrl(EngArgs a) {
            !isfinite(est);
     a.m[slot] = m + 1;
   }
+  __syncwarp();
+  for (int i = lane; i <= m + 1; i += 32) Hc[i] = hs[i];
   done = __shfl_sync(0xffffffffu, done, 0);
   if (!done) return;
-  // back substitution R y = e (m1 x m1 upper triangular), warp-parallel column sweep
+  // back substitution R y = e (m1 x m1 upper triangular): lane l owns y_i for i = l + 32 r; y_j is
+  // broadcast by shuffle; column j-1 is loaded while column j is processed (no global round trip
+  // on the dependency chain)
   const int m1 = m + 1;
-  double* y = a.y + (int64_t)slot * a.mmax;
-  for (int i = lane; i < m1; i += 32) y[i] = e[i];
-  __syncwarp();
-  for (int j = m1 - 1; j >= 0; --j) {
-    const double d = H[(int64_t)j * ld + j];
-    const double yj = d != 0.0 ? y[j] / d : 0.0;
-    __syncwarp();
-    if (lane == 0) y[j] = yj;
-    for (int i = lane; i < j; i += 32) y[i] -= H[(int64_t)j * ld + i] * yj;
-    __syncwarp();
+  double yv[CTRL_RMAX], hv[CTRL_RMAX], hn[CTRL_RMAX];
+#pragma unroll
+  for (int r = 0; r < CTRL_RMAX; ++r) {
+    const int i = lane + 32 * r;
+    yv[r] = (i < m1) ? e[i] : 0.0;
+    hv[r] = (i <= m) ? hs[i] : 0.0;  // column m lives in shared memory
   }
-  for (int i = lane; i < m1; i += 32) y[i] /= eta[i];
+  for (int j = m; j >= 0; --j) {
+    if (j > 0) {
+      const double* Hj = H + (int64_t)(j - 1) * ld;
+#pragma unroll
+      for (int r = 0; r < CTRL_RMAX; ++r) {
+        const int i = lane + 32 * r;
+        hn[r] = (i < j) ? Hj[i] : 0.0;
+      }
+    }
+    const int owner = j & 31, rj = j >> 5;
+    double yj = 0.0, dj = 0.0;
+#pragma unroll
+    for (int r = 0; r < CTRL_RMAX; ++r)
+      if (r == rj) {
+        yj = yv[r];
+        dj = hv[r];
+      }
+    yj = __shfl_sync(0xffffffffu, yj, owner);
+    dj = __shfl_sync(0xffffffffu, dj, owner);
+    yj = dj != 0.0 ? yj / dj : 0.0;
+#pragma unroll
+    for (int r = 0; r < CTRL_RMAX; ++r) {
+      const int i = lane + 32 * r;
+      if (i == j) yv[r] = yj;
+      else if (i < j) yv[r] -= hv[r] * yj;
+    }
+#pragma unroll
+    for (int r = 0; r < CTRL_RMAX; ++r) hv[r] = hn[r];
+  }
+  double* y = a.y + (int64_t)slot * a.mmax;
+#pragma unroll
+  for (int r = 0; r < CTRL_RMAX; ++r) {
+    const int i = lane + 32 * r;
+    if (i < m1) y[i] = yv[r] / eta[i];
+  }
   __syncwarp();
   if (lane == 0) {
     a.restarts[slot] += 1;
@@ -457,7 +539,32 @@ __global__ void __launch_bounds__(128) k_ctrl(EngArgs a) {
 }
 
 // ---------------------------------------------------------------- solution update
-// XUPD: X += P(v)^{-1} (sum_{i<m} y_i q^_i)   (y already carries the 1/eta_i)
+// XUPD: X += P(v)^{-1} (sum_{i<m} y_i q^_i)   (y already carries the 1/eta_i).  Two kernels: the
+// basis combination is elementwise (coalesced over the vector, many blocks per slot); the k x k
+// P^{-1} blocks then act per representative.  Xin (consumed by K1 earlier in the iteration) holds
+// the combination in between.
+__global__ void __launch_bounds__(256) k_xcomb(EngArgs a) {
+  __shared__ double ys[1024];
+  const int slot = blockIdx.y;
+  if (a.phase[slot] != PH_XUPD) return;
+  const int m1 = a.m[slot];
+  for (int i = threadIdx.x; i < m1; i += blockDim.x) ys[i] = a.y[(int64_t)slot * a.mmax + i];
+  __syncthreads();
+  const double* Q = a.Qb + (int64_t)slot * (a.mmax + 1) * a.L;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < a.L; e += (int64_t)gridDim.x * blockDim.x) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int i = 0;
+    for (; i + 3 < m1; i += 4) {
+      s0 += ys[i] * Q[(int64_t)i * a.L + e];
+      s1 += ys[i + 1] * Q[(int64_t)(i + 1) * a.L + e];
+      s2 += ys[i + 2] * Q[(int64_t)(i + 2) * a.L + e];
+      s3 += ys[i + 3] * Q[(int64_t)(i + 3) * a.L + e];
+    }
+    for (; i < m1; ++i) s0 += ys[i] * Q[(int64_t)i * a.L + e];
+    a.Xin[(int64_t)slot * a.L + e] = (s0 + s1) + (s2 + s3);
+  }
+}
+
 template <int K>
 __global__ void __launch_bounds__(128) k_xupd(EngArgs a) {
   const int slot = blockIdx.y;
@@ -466,21 +573,10 @@ __global__ void __launch_bounds__(128) k_xupd(EngArgs a) {
   if (rep >= a.nrep) return;
   const int64_t c = rep_coord(rep, a.npairs);
   const bool pair = rep < a.npairs;
-  const int m1 = a.m[slot];
-  const double* y = a.y + (int64_t)slot * a.mmax;
-  const double* Q = a.Qb + (int64_t)slot * (a.mmax + 1) * a.L;
+  const double* sv = a.Xin + (int64_t)slot * a.L + c;
   cplx r[K], z[K];
 #pragma unroll
-  for (int t = 0; t < K; ++t) r[t] = mk(0.0, 0.0);
-  for (int i = 0; i < m1; ++i) {
-    const double yi = y[i];
-    const double* q = Q + (int64_t)i * a.L + c;
-#pragma unroll
-    for (int t = 0; t < K; ++t) {
-      r[t].re += yi * q[t * a.npad];
-      if (pair) r[t].im += yi * q[t * a.npad + 1];
-    }
-  }
+  for (int t = 0; t < K; ++t) r[t] = mk(sv[t * a.npad], pair ? sv[t * a.npad + 1] : 0.0);
   apply_minv<K>(a.Minv + (((int64_t)slot * a.nrep + rep) * K * K) * 2, r, z);
   double* X = a.X + (int64_t)slot * a.L + c;
 #pragma unroll

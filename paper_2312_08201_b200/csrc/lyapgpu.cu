@@ -103,7 +103,8 @@ using GCfg = DgemmCfg<G_BM, G_BN, G_WM, G_WN, G_ST>;
 // ------------------------------------------------------------------ engine allocation
 void free_engine(Engine& g, bool keep_order = true) {
   void* ps[] = {g.Bop, g.U, g.Xin, g.X, g.Qb, g.Minv, g.sigma, g.mask, g.eta, g.H, g.e, g.y,
-                g.bnorm, g.part, g.part3, g.phase, g.m, g.vidx, g.applies, g.restarts, g.ctrl};
+                g.bnorm, g.part, g.part3, g.phase, g.m, g.vidx, g.applies, g.restarts, g.ctrl,
+                g.part2, g.Rc, g.Rr, g.cf};
   for (void* p : ps) dfree(p);
   if (g.h_ctrl) cudaFreeHost(g.h_ctrl);
   int* order = g.order;
@@ -131,7 +132,7 @@ int auto_batch(const lyap_ctx* ctx, int64_t nv) {
 }
 
 int auto_mmax(const lyap_ctx* ctx) {
-  if (ctx->opts.max_dim > 0) return ctx->opts.max_dim;
+  if (ctx->opts.max_dim > 0) return std::min(ctx->opts.max_dim, 32 * CTRL_RMAX);
   return 160;
 }
 
@@ -160,6 +161,10 @@ void ensure_engine(lyap_ctx* ctx, int b, int mmax) {
   g.bnorm = dalloc<double>(ctx, b);
   g.part = dalloc<double>(ctx, (size_t)b * (mmax + 2) * g.nchunk);
   g.part3 = dalloc<double>(ctx, (size_t)b * g.nchunk * 3);
+  g.part2 = dalloc<double>(ctx, (size_t)b * (mmax + 2) * g.nchunk);
+  g.Rc = dalloc<double>(ctx, (size_t)b * (mmax + 1) * (mmax + 1));
+  g.Rr = dalloc<double>(ctx, 1);
+  g.cf = dalloc<double>(ctx, (size_t)b * (mmax + 1));
   g.phase = dalloc<int>(ctx, b);
   g.m = dalloc<int>(ctx, b);
   g.vidx = dalloc<int>(ctx, b);
@@ -264,6 +269,10 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   a.bnorm = g.bnorm;
   a.part = g.part;
   a.part3 = g.part3;
+  a.part2 = g.part2;
+  a.Rc = g.Rc;
+  a.Rr = g.Rr;
+  a.cf = g.cf;
   a.phase = g.phase;
   a.m = g.m;
   a.vidx = g.vidx;
@@ -302,6 +311,12 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   const dim3 gred((unsigned)g.nchunk, (unsigned)b);
   const int assign_threads = (int)roundup(b, 32);
   const size_t upd_smem = sizeof(double) * (mmax + 1);
+  const size_t ctrl_smem = sizeof(double) * 16 * (size_t)(mmax + 2);
+  const size_t gram_smem = sizeof(double) * (size_t)(mmax + 1);
+  const dim3 gxc((unsigned)std::min<int64_t>((g.L + 255) / 256, 64), (unsigned)b);
+  if (gram_smem > 48 * 1024) CK(cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_smem));
+  if (ctrl_smem > 48 * 1024) CK(cudaFuncSetAttribute(k_ctrl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctrl_smem));
+  if (upd_smem > 48 * 1024) CK(cudaFuncSetAttribute(k_upd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem));
   const int64_t per_v = (int64_t)(ctx->opts.max_restarts + 1) * (mmax + 2);
   const int64_t max_iter = ((nv + b - 1) / b) * per_v + 64;
   const int poll = 4;
@@ -316,15 +331,15 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
     K_DISPATCH(s.k, (k_prec<KK><<<grep, 128, 0, st>>>(a)));
     LAUNCHED();
     launch_k1(ctx, k1, st, pp);
-    k_dots<<<gred, 256, 0, st>>>(a, 1);
+    k_dots<<<gred, 256, 0, st>>>(a);
     LAUNCHED();
-    k_upd<<<gred, 256, upd_smem, st>>>(a, 1);
+    k_gram<<<b, 128, gram_smem, st>>>(a);
     LAUNCHED();
-    k_dots<<<gred, 256, 0, st>>>(a, 2);
+    k_upd<<<gred, 256, upd_smem, st>>>(a);
     LAUNCHED();
-    k_upd<<<gred, 256, upd_smem, st>>>(a, 2);
+    k_ctrl<<<(b + 3) / 4, 128, ctrl_smem, st>>>(a);
     LAUNCHED();
-    k_ctrl<<<(b + 3) / 4, 128, 0, st>>>(a);
+    k_xcomb<<<gxc, 256, 0, st>>>(a);
     LAUNCHED();
     K_DISPATCH(s.k, (k_xupd<KK><<<grep, 128, 0, st>>>(a)));
     LAUNCHED();
