@@ -81,8 +81,8 @@ __global__ void __launch_bounds__(256) k1_gen(K1Args a, const double* __restrict
 }
 
 // ------------------------------------------------------------------------------------------
-// K1b: C = A * B, FP64, A: M x Kd row-major (the folded Cauchy matrix Lf), B: Kd x N row-major,
-// C: M x N row-major.  M % BM == N % BN == Kd % 16 == 0.  STAGES-deep cp.async pipeline, warp
+// K1b: C = A * B, FP64, A: M x Kd (row stride lda; the folded Cauchy matrix Lf), B: Kd x N
+// row-major, C: M x N row-major.  M % BM == N % BN == Kd % 16 == 0.  STAGES-deep cp.async pipeline, warp
 // tile WM x WN of m8n8k4 DMMA fragments.  Shared-memory strides 20 / BN+4 doubles make every
 // fragment load conflict-free (lane -> (row l/4, k l%4) maps onto 16 distinct 8-byte banks per
 // half-warp).
@@ -95,9 +95,10 @@ struct DgemmCfg {
 };
 
 template <int BM, int BN, int WM, int WN, int STAGES>
-__global__ void __launch_bounds__(DgemmCfg<BM, BN, WM, WN, STAGES>::THREADS, 1)
+__global__ void __launch_bounds__(DgemmCfg<BM, BN, WM, WN, STAGES>::THREADS,
+                                  DgemmCfg<BM, BN, WM, WN, STAGES>::THREADS <= 128 ? 3 : 1)
     k1_dgemm(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C, int M,
-             int N, int Kd, const int* __restrict__ nactive, int cols_per_active) {
+             int N, int Kd, int lda, const int* __restrict__ nactive, int cols_per_active) {
   using Cfg = DgemmCfg<BM, BN, WM, WN, STAGES>;
   constexpr int BK = Cfg::BK, AST = Cfg::AST, BST = Cfg::BST, NT = Cfg::THREADS;
   constexpr int MT = WM / 8, NTL = WN / 8;
@@ -116,12 +117,12 @@ __global__ void __launch_bounds__(DgemmCfg<BM, BN, WM, WN, STAGES>::THREADS, 1)
     for (int j = 0; j < NTL; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   auto load_stage = [&](int stage, int kt) {
-    const double* Ag = A + (int64_t)m0 * Kd + (int64_t)kt * BK;
+    const double* Ag = A + (int64_t)m0 * lda + (int64_t)kt * BK;
     double* as = As + stage * Cfg::A_STAGE;
 #pragma unroll
     for (int c = tid; c < BM * BK / 2; c += NT) {
       int r = c / (BK / 2), cc = (c % (BK / 2)) * 2;
-      cp_async16(as + r * AST + cc, Ag + (int64_t)r * Kd + cc);
+      cp_async16(as + r * AST + cc, Ag + (int64_t)r * lda + cc);
     }
     const double* Bg = B + (int64_t)kt * BK * N + n0;
     double* bs = Bs + stage * Cfg::B_STAGE;

@@ -84,8 +84,16 @@ void dfree(void* p) {
 int64_t roundup(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 // K1 GEMM configuration
+// large n: 128 x 128 CTA tiles (8 warps of 64 x 32), one CTA per SM
 constexpr int G_BM = 128, G_BN = 128, G_WM = 64, G_WN = 32, G_ST = 4;
 using GCfg = DgemmCfg<G_BM, G_BN, G_WM, G_WN, G_ST>;
+// small n (<= SMALL_N): 64 x 64 tiles (4 warps of 32 x 32), several CTAs per SM -> less padding
+// and finer wave quantisation
+constexpr int S_BM = 64, S_BN = 64, S_WM = 32, S_WN = 32, S_ST = 3;
+using SCfg = DgemmCfg<S_BM, S_BN, S_WM, S_WN, S_ST>;
+constexpr int64_t SMALL_N = 1536;
+inline int tile_m(const Seed& s) { return s.n <= SMALL_N ? S_BM : G_BM; }
+inline int tile_n(const Seed& s) { return s.n <= SMALL_N ? S_BN : G_BN; }
 
 #define K_DISPATCH(KV, ...)     \
   switch (KV) {                  \
@@ -122,8 +130,9 @@ int auto_batch(const lyap_ctx* ctx, int64_t nv) {
   int b = ctx->opts.batch;
   if (b <= 0) {
     // aim for ~8 waves of 128x128 K1 tiles on 148 SMs
-    const int64_t mt = s.npad / G_BM;
-    const int64_t target_cols = (8 * 148 + mt - 1) / mt * G_BN;
+    const int64_t mt = s.npad / tile_m(s);
+    const int64_t waves = s.n <= SMALL_N ? 16 * 148 : 8 * 148;
+    const int64_t target_cols = (waves + mt - 1) / mt * tile_n(s);
     b = (int)std::max<int64_t>(32, std::min<int64_t>(1024, target_cols / (s.k * s.k)));
   }
   b = (int)std::min<int64_t>(b, std::max<int64_t>(nv, 1));
@@ -144,7 +153,7 @@ void ensure_engine(lyap_ctx* ctx, int b, int mmax) {
   g.b = b;
   g.mmax = mmax;
   g.L = s.k * s.npad;
-  g.ncol = roundup((int64_t)b * s.k * s.k, G_BN);
+  g.ncol = roundup((int64_t)b * s.k * s.k, tile_n(s));
   g.nchunk = (int)((g.L + RED_CE - 1) / RED_CE);
   g.Bop = dalloc<double>(ctx, (size_t)s.npad * g.ncol);
   g.U = dalloc<double>(ctx, (size_t)s.npad * g.ncol);
@@ -192,10 +201,17 @@ void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, EvPool* pool) {
   });
   LAUNCHED();
   {
-    dim3 grid((unsigned)(g.ncol / G_BN), (unsigned)(s.npad / G_BM));
+    const int kpad = (int)roundup(s.n, 16);  // Lf / Bop rows >= n are zero: skip them in K
     if (pool) CK(cudaEventRecord(pool->ev[2 * pool->used], st));
-    k1_dgemm<G_BM, G_BN, G_WM, G_WN, G_ST><<<grid, GCfg::THREADS, GCfg::SMEM, st>>>(
-        s.Lf, g.Bop, g.U, (int)s.npad, (int)g.ncol, (int)s.npad, a.nactive, (int)(s.k * s.k));
+    if (s.n <= SMALL_N) {
+      dim3 grid((unsigned)(g.ncol / S_BN), (unsigned)(s.npad / S_BM));
+      k1_dgemm<S_BM, S_BN, S_WM, S_WN, S_ST><<<grid, SCfg::THREADS, SCfg::SMEM, st>>>(
+          s.Lf, g.Bop, g.U, (int)s.npad, (int)g.ncol, kpad, (int)s.npad, a.nactive, (int)(s.k * s.k));
+    } else {
+      dim3 grid((unsigned)(g.ncol / G_BN), (unsigned)(s.npad / G_BM));
+      k1_dgemm<G_BM, G_BN, G_WM, G_WN, G_ST><<<grid, GCfg::THREADS, GCfg::SMEM, st>>>(
+          s.Lf, g.Bop, g.U, (int)s.npad, (int)g.ncol, kpad, (int)s.npad, a.nactive, (int)(s.k * s.k));
+    }
     LAUNCHED();
     if (pool) {
       CK(cudaEventRecord(pool->ev[2 * pool->used + 1], st));
@@ -474,12 +490,14 @@ int lyap_setup(int64_t n, int64_t k, const double* A0, const double* Bl, const d
     CKS(cusolverDnSetStream(ctx->cusolver, ctx->stream));
     CK(cudaFuncSetAttribute(k1_dgemm<G_BM, G_BN, G_WM, G_WN, G_ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)GCfg::SMEM));
+    CK(cudaFuncSetAttribute(k1_dgemm<S_BM, S_BN, S_WM, S_WN, S_ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)SCfg::SMEM));
     cudaStream_t st = ctx->stream;
     CK(cudaEventRecord(ctx->ev0, st));
     Seed& s = ctx->seed;
     s.n = n;
     s.k = k;
-    s.npad = roundup(n, G_BM);
+    s.npad = roundup(n, n <= SMALL_N ? S_BM : G_BM);
     const size_t nn = (size_t)n * n;
     dA = dalloc<double>(ctx, nn, false);
     dQ = dalloc<double>(ctx, nn, false);
