@@ -31,7 +31,6 @@ sys.path.insert(0, ROOT)
 METRIC = "parameter vectors/sec (trace(EX(v)))"
 UNIT = "v/s"
 FP64_PEAK_TFLOPS = 37.0   # measured: DMMA m8n8k4 burst, profiles/r01_fp64_peaks.md (MEASURED_PEAKS.json has no FP64)
-CHUNK = 64                # consecutive grid points per shard chunk
 
 
 def parse():
@@ -150,12 +149,6 @@ def oracle_rate(name: str, seconds: float, seed: int = 0):
 
 
 # ------------------------------------------------------------------------------ helpers
-def shard_indices(nv: int, rank: int, world: int) -> np.ndarray:
-    chunks = [np.arange(s, min(nv, s + CHUNK)) for s in range(0, nv, CHUNK)]
-    mine = chunks[rank::world]
-    return np.concatenate(mine) if mine else np.zeros(0, dtype=np.int64)
-
-
 def emit(obj):
     print(json.dumps(obj), flush=True)
 
@@ -211,34 +204,21 @@ def main():
 
     import workloads
     from paper_2312_08201_b200 import Problem
+    from paper_2312_08201_b200.sweep import Sweep
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     W = workloads.make(args.config)
-    idx = shard_indices(W.nv, rank, world)
+    sweep = Sweep(W.nv, rank, world, dev)
+    idx = sweep.mine
     P = Problem(W.A0, W.Bl, W.Br, W.Q, W.E, profile=True, device=local, batch=args.batch, max_dim=args.max_dim)
     setup_ms = P.info["setup_ms"]
     Vd = torch.tensor(W.V[idx], device=dev)
-    nmax = max(len(shard_indices(W.nv, r, world)) for r in range(world))
-    gathered = torch.empty(world * nmax, dtype=torch.float64, device=dev)
-    all_idx = torch.tensor(np.concatenate([np.pad(shard_indices(W.nv, r, world),
-                                                  (0, nmax - len(shard_indices(W.nv, r, world))),
-                                                  constant_values=-1) for r in range(world)]), device=dev)
-    valid = all_idx >= 0
 
     def step():
-        tau = P.trace_batch(Vd)
-        if world > 1:
-            buf = torch.full((nmax,), float("inf"), dtype=torch.float64, device=dev)
-            buf[: tau.numel()] = tau
-            dist.all_gather_into_tensor(gathered, buf)
-            full = torch.empty(W.nv, dtype=torch.float64, device=dev)
-            full[all_idx[valid]] = gathered[valid]
-        else:
-            full = tau
-        return full, torch.argmin(full)  # first index on ties
+        return sweep.run(lambda rows: P.trace_batch(Vd))
 
     for _ in range(args.warmup):
         full, am = step()

@@ -56,7 +56,9 @@ typedef struct {
   int32_t max_dim;     /* Krylov restart length m_max; 0 = auto (default) */
   int32_t max_restarts;/* restart cycles before status LYAP_V_NOCONV (default 30) */
   int32_t batch;       /* parameter vectors in flight (slots); 0 = auto (default) */
-  int32_t warm_start;  /* 1 (default): a slot starts v from the solution of its previous v */
+  int32_t warm_start;  /* 1: a slot starts v from the solution of its previous v; 0 (default):
+                          from g = 0 (warm starts were measured to save no iterations, and with
+                          them a result would depend on which slot solved which v) */
   double max_cond_S;   /* setup fails with LYAP_EEIG above this 1-norm condition of S (1e8) */
   int32_t device;      /* CUDA device ordinal (default: current device) */
   int32_t profile;     /* 1: time every K1 GEMM launch with CUDA events (lyap_get_stats) */

@@ -40,7 +40,7 @@ class Problem:
     """One seed A0 with its factors (lyap_setup); trace_batch evaluates trace(E X(v))."""
 
     def __init__(self, A0, Bl, Br, Q, E, *, tol: float = 1e-12, max_dim: int = 0, max_restarts: int = 30,
-                 batch: int = 0, warm_start: bool = True, max_cond_S: float = 1e8, device: int = -1,
+                 batch: int = 0, warm_start: bool = False, max_cond_S: float = 1e8, device: int = -1,
                  profile: bool = False, schedule: bool = True):
         A0 = _f64(A0)
         n = A0.shape[0]

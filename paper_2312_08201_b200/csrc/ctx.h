@@ -35,7 +35,8 @@ struct Engine {
   int64_t L = 0;    // vector length k * npad
   int64_t ncol = 0; // K1 GEMM columns, b*k*k rounded up to the N tile
   int nchunk = 0;   // chunks of the vector length for the reductions
-  double *Bop = nullptr, *U = nullptr;            // npad x ncol
+  int groups = 1;   // slot groups, each on its own stream (K1 of one overlaps the Krylov kernels of the other)
+  double *Bop = nullptr, *U = nullptr;            // groups x npad x ncol  (ncol per group)
   double *Xin = nullptr, *X = nullptr;            // b x L
   double* Qb = nullptr;                           // b x (mmax+1) x L  (unnormalised basis)
   double* Minv = nullptr;                         // b x nrep x k x k x 2
@@ -48,7 +49,8 @@ struct Engine {
   double *Rc = nullptr, *Rr = nullptr;            // b x (mmax+1)^2 Cholesky factor of Q^T Q
   double *cf = nullptr;                           // b x (mmax+1) projection coefficients
   int *phase = nullptr, *m = nullptr, *vidx = nullptr, *applies = nullptr, *restarts = nullptr;
-  int* ctrl = nullptr;                            // [0]=next v, [1]=done count, [2]=active slots
+  int* ctrl = nullptr;                            // per group 8 ints: [2]=active slots, [4..5]=applied vectors;
+                                                  // then 8 shared: [0]=next queue position, [1]=done count
   int* h_ctrl = nullptr;                          // pinned mirror
   int* order = nullptr;                           // queue order (nv_cap)
   int64_t order_cap = 0;
@@ -67,5 +69,6 @@ struct lyap_ctx {
   cusolverDnHandle_t cusolver = nullptr;
   lyap::Seed seed;
   lyap::Engine eng;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, evfork = nullptr, evjoin = nullptr;
+  cudaStream_t stream2 = nullptr;  // second slot group
 };

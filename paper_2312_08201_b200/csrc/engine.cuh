@@ -31,6 +31,8 @@ struct EngArgs {
   double *X, *Xin, *Qb, *Minv, *sigma, *mask, *eta, *H, *e, *y, *bnorm, *part, *part3;
   double *part2, *Rc, *Rr, *cf;  // Gram-row partials, Gram matrix Q^T Q (Rc; Rr unused), coefficients
   int *phase, *m, *vidx, *applies, *restarts, *ctrl, *newv, *alist;
+  int* qctr;      // shared by all slot groups: [0] next queue position, [1] finished v's
+  double *cs, *sn;  // Givens rotations (b x mmax each)
   double* traces;
   int32_t* status;
   int32_t* out_applies;
@@ -60,13 +62,15 @@ __global__ void k_assign(EngArgs a) {
     if (lane >= o) x += y;
   }
   if (lane == 31) wsum[w] = x;
-  if (tid == 0) base_s = a.ctrl[0];
   __syncthreads();
   int off = 0, total = 0;
   for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
     if (i < w) off += wsum[i];
     total += wsum[i];
   }
+  // claim `total` consecutive queue positions (the queue is shared by the slot groups)
+  if (tid == 0) base_s = total ? atomicAdd(&a.qctr[0], total) : 0;
+  __syncthreads();
   const int pos = off + x - flag;
   const int base = base_s;
   if (tid < a.b && flag) {
@@ -104,7 +108,6 @@ __global__ void k_assign(EngArgs a) {
   if (isact) a.alist[offa + xa - 1] = tid;
   const int act = __syncthreads_count(isact);
   if (tid == 0) {
-    a.ctrl[0] = base + total;
     a.ctrl[2] = act;
     *reinterpret_cast<unsigned long long*>(a.ctrl + 4) += (unsigned long long)act;  // applied vectors
   }
@@ -375,22 +378,32 @@ __global__ void __launch_bounds__(256) k_upd(EngArgs a) {
   double* w = a.Qb + slot * qs + (int64_t)(m + 1) * a.L;
   const double* Q = a.Qb + slot * qs;
   const int64_t e0 = (int64_t)chunk * RED_CE;
-  double nrm = 0.0;
-  for (int ii = threadIdx.x; ii < RED_CE; ii += blockDim.x) {
-    const int64_t e = e0 + ii;
-    if (e >= a.L) break;
-    double v = w[e];
-    double acc0 = 0.0, acc1 = 0.0;
-    int i = 0;
-    for (; i + 1 <= m; i += 2) {
-      acc0 += cfs[i] * Q[(int64_t)i * a.L + e];
-      acc1 += cfs[i + 1] * Q[(int64_t)(i + 1) * a.L + e];
-    }
-    if (i <= m) acc0 += cfs[i] * Q[(int64_t)i * a.L + e];
-    v -= acc0 + acc1;
-    w[e] = v;
-    nrm += v * v;
+  // each thread owns 4 elements of the chunk; the basis loop issues 4 independent loads per vector
+  constexpr int EPT = RED_CE / 256;
+  double acc[EPT];
+  bool ok[EPT];
+  int64_t eo[EPT];
+#pragma unroll
+  for (int r = 0; r < EPT; ++r) {
+    eo[r] = e0 + threadIdx.x + 256 * r;
+    ok[r] = eo[r] < a.L;
+    acc[r] = 0.0;
   }
+  for (int i = 0; i <= m; ++i) {
+    const double c = cfs[i];
+    const double* q = Q + (int64_t)i * a.L;
+#pragma unroll
+    for (int r = 0; r < EPT; ++r)
+      if (ok[r]) acc[r] += c * q[eo[r]];
+  }
+  double nrm = 0.0;
+#pragma unroll
+  for (int r = 0; r < EPT; ++r)
+    if (ok[r]) {
+      const double v = w[eo[r]] - acc[r];
+      w[eo[r]] = v;
+      nrm += v * v;
+    }
   nrm = block_sum(nrm, red);
   if (threadIdx.x == 0) a.part3[((int64_t)slot * a.nchunk + chunk) * 3] = nrm;
 }
@@ -406,8 +419,8 @@ __global__ void __launch_bounds__(128) k_ctrl(EngArgs a) {
   double* H = a.H + (int64_t)slot * ld * a.mmax;
   double* e = a.e + (int64_t)slot * ld;
   double* eta = a.eta + (int64_t)slot * ld;
-  double* cs = a.e + (int64_t)a.b * ld + (int64_t)slot * a.mmax;   // cs, sn live after e
-  double* sn = cs + (int64_t)a.b * a.mmax;
+  double* cs = a.cs + (int64_t)slot * a.mmax;
+  double* sn = a.sn + (int64_t)slot * a.mmax;
   const double* p3 = a.part3 + (int64_t)slot * a.nchunk * 3;
   if (ph == PH_VERIFY) {
     if (lane != 0) return;
@@ -428,7 +441,7 @@ __global__ void __launch_bounds__(128) k_ctrl(EngArgs a) {
       if (a.out_applies) a.out_applies[idx] = ap;
       if (a.out_resid) a.out_resid[idx] = bn > 0.0 ? rho / bn : rho;
       a.phase[slot] = PH_FREE;
-      atomicAdd(&a.ctrl[1], 1);
+      atomicAdd(&a.qctr[1], 1);
     } else {
       eta[0] = rho;
       e[0] = rho;
@@ -485,56 +498,60 @@ __global__ void __launch_bounds__(128) k_ctrl(EngArgs a) {
   for (int i = lane; i <= m + 1; i += 32) Hc[i] = hs[i];
   done = __shfl_sync(0xffffffffu, done, 0);
   if (!done) return;
-  // back substitution R y = e (m1 x m1 upper triangular): lane l owns y_i for i = l + 32 r; y_j is
-  // broadcast by shuffle; column j-1 is loaded while column j is processed (no global round trip
-  // on the dependency chain)
-  const int m1 = m + 1;
-  double yv[CTRL_RMAX], hv[CTRL_RMAX], hn[CTRL_RMAX];
+  if (lane == 0) {
+    a.restarts[slot] += 1;
+    a.phase[slot] = PH_XUPD;
+  }
+}
+
+// ---------------------------------------------------------------- cycle end: R y = e
+// One block per slot that just finished a cycle (phase XUPD): the rotated Hessenberg (upper
+// triangular R, m1 x m1, packed by columns) is staged in shared memory with one coalesced load,
+// then one warp runs the back substitution with y distributed over the lanes (shuffle broadcast).
+__global__ void __launch_bounds__(256) k_backsub(EngArgs a) {
+  extern __shared__ double Rs[];  // m1 (m1 + 1) / 2
+  const int slot = blockIdx.x;
+  if (a.phase[slot] != PH_XUPD) return;
+  const int ld = a.mmax + 1;
+  const int m1 = a.m[slot];
+  const double* H = a.H + (int64_t)slot * ld * a.mmax;
+  for (int j = threadIdx.x >> 5; j < m1; j += blockDim.x >> 5) {
+    const int off = j * (j + 1) / 2;
+    for (int i = threadIdx.x & 31; i <= j; i += 32) Rs[off + i] = H[(int64_t)j * ld + i];
+  }
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  const double* e = a.e + (int64_t)slot * ld;
+  const double* eta = a.eta + (int64_t)slot * ld;
+  double yv[CTRL_RMAX];
 #pragma unroll
   for (int r = 0; r < CTRL_RMAX; ++r) {
     const int i = lane + 32 * r;
     yv[r] = (i < m1) ? e[i] : 0.0;
-    hv[r] = (i <= m) ? hs[i] : 0.0;  // column m lives in shared memory
   }
-  for (int j = m; j >= 0; --j) {
-    if (j > 0) {
-      const double* Hj = H + (int64_t)(j - 1) * ld;
-#pragma unroll
-      for (int r = 0; r < CTRL_RMAX; ++r) {
-        const int i = lane + 32 * r;
-        hn[r] = (i < j) ? Hj[i] : 0.0;
-      }
-    }
+  for (int j = m1 - 1; j >= 0; --j) {
+    const double* Rj = Rs + j * (j + 1) / 2;
     const int owner = j & 31, rj = j >> 5;
-    double yj = 0.0, dj = 0.0;
+    double yj = 0.0;
 #pragma unroll
     for (int r = 0; r < CTRL_RMAX; ++r)
-      if (r == rj) {
-        yj = yv[r];
-        dj = hv[r];
-      }
+      if (r == rj) yj = yv[r];
     yj = __shfl_sync(0xffffffffu, yj, owner);
-    dj = __shfl_sync(0xffffffffu, dj, owner);
+    const double dj = Rj[j];
     yj = dj != 0.0 ? yj / dj : 0.0;
 #pragma unroll
     for (int r = 0; r < CTRL_RMAX; ++r) {
       const int i = lane + 32 * r;
       if (i == j) yv[r] = yj;
-      else if (i < j) yv[r] -= hv[r] * yj;
+      else if (i < j) yv[r] -= Rj[i] * yj;
     }
-#pragma unroll
-    for (int r = 0; r < CTRL_RMAX; ++r) hv[r] = hn[r];
   }
   double* y = a.y + (int64_t)slot * a.mmax;
 #pragma unroll
   for (int r = 0; r < CTRL_RMAX; ++r) {
     const int i = lane + 32 * r;
     if (i < m1) y[i] = yv[r] / eta[i];
-  }
-  __syncwarp();
-  if (lane == 0) {
-    a.restarts[slot] += 1;
-    a.phase[slot] = PH_XUPD;
   }
 }
 

@@ -129,19 +129,21 @@ int auto_batch(const lyap_ctx* ctx, int64_t nv) {
   const Seed& s = ctx->seed;
   int b = ctx->opts.batch;
   if (b <= 0) {
-    // aim for ~8 waves of 128x128 K1 tiles on 148 SMs
+    // two slot groups, each aiming for ~8 waves of K1 tiles (16 for the small-tile config) on 148
+    // SMs, but at least ~4 v per slot so the cost-ordered queue can balance the slots
     const int64_t mt = s.npad / tile_m(s);
     const int64_t waves = s.n <= SMALL_N ? 16 * 148 : 8 * 148;
     const int64_t target_cols = (waves + mt - 1) / mt * tile_n(s);
-    b = (int)std::max<int64_t>(32, std::min<int64_t>(1024, target_cols / (s.k * s.k)));
+    const int64_t per_group = std::max<int64_t>(32, std::min<int64_t>(1024, target_cols / (s.k * s.k)));
+    b = (int)std::min<int64_t>(2 * per_group, std::max<int64_t>(64, nv / 4));
   }
   b = (int)std::min<int64_t>(b, std::max<int64_t>(nv, 1));
-  b = std::max(1, std::min(b, 1024));
+  b = std::max(1, std::min(b, 2048));  // <= 1024 per slot group (k_assign is one block)
   return b;
 }
 
 int auto_mmax(const lyap_ctx* ctx) {
-  if (ctx->opts.max_dim > 0) return std::min(ctx->opts.max_dim, 32 * CTRL_RMAX);
+  if (ctx->opts.max_dim > 0) return std::min(ctx->opts.max_dim, 224);  // k_backsub stages R (<= 201 KB smem)
   return 160;
 }
 
@@ -153,10 +155,12 @@ void ensure_engine(lyap_ctx* ctx, int b, int mmax) {
   g.b = b;
   g.mmax = mmax;
   g.L = s.k * s.npad;
-  g.ncol = roundup((int64_t)b * s.k * s.k, tile_n(s));
+  g.groups = b >= 64 ? 2 : 1;
+  if (const char* ev = std::getenv("LYAP_GROUPS")) g.groups = std::max(1, std::min(2, std::atoi(ev)));  // experiments
+  g.ncol = roundup((int64_t)((b + g.groups - 1) / g.groups) * s.k * s.k, tile_n(s));
   g.nchunk = (int)((g.L + RED_CE - 1) / RED_CE);
-  g.Bop = dalloc<double>(ctx, (size_t)s.npad * g.ncol);
-  g.U = dalloc<double>(ctx, (size_t)s.npad * g.ncol);
+  g.Bop = dalloc<double>(ctx, (size_t)g.groups * s.npad * g.ncol);
+  g.U = dalloc<double>(ctx, (size_t)g.groups * s.npad * g.ncol);
   g.Xin = dalloc<double>(ctx, (size_t)b * g.L);
   g.X = dalloc<double>(ctx, (size_t)b * g.L);
   g.Qb = dalloc<double>(ctx, (size_t)b * (mmax + 1) * g.L);
@@ -165,7 +169,7 @@ void ensure_engine(lyap_ctx* ctx, int b, int mmax) {
   g.mask = dalloc<double>(ctx, (size_t)b * s.k);
   g.eta = dalloc<double>(ctx, (size_t)b * (mmax + 1));
   g.H = dalloc<double>(ctx, (size_t)b * (mmax + 1) * mmax);
-  g.e = dalloc<double>(ctx, (size_t)b * (mmax + 1) + 2 * (size_t)b * mmax);  // e | cs | sn
+  g.e = dalloc<double>(ctx, (size_t)b * (mmax + 1) + 2 * (size_t)b * mmax);  // e | cs | sn (b x mmax each)
   g.y = dalloc<double>(ctx, (size_t)b * mmax);
   g.bnorm = dalloc<double>(ctx, b);
   g.part = dalloc<double>(ctx, (size_t)b * (mmax + 2) * g.nchunk);
@@ -179,8 +183,8 @@ void ensure_engine(lyap_ctx* ctx, int b, int mmax) {
   g.vidx = dalloc<int>(ctx, b);
   g.applies = dalloc<int>(ctx, b);
   g.restarts = dalloc<int>(ctx, 3 * (size_t)b);  // restarts | newv | alist
-  g.ctrl = dalloc<int>(ctx, 8);
-  CK(cudaMallocHost(&g.h_ctrl, 8 * sizeof(int)));
+  g.ctrl = dalloc<int>(ctx, 8 * (g.groups + 1));
+  CK(cudaMallocHost(&g.h_ctrl, 8 * (g.groups + 1) * sizeof(int)));
   ctx->info.batch = b;
   ctx->info.max_dim = mmax;
 }
@@ -191,9 +195,11 @@ struct EvPool {
   int used = 0;
 };
 
-void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, EvPool* pool) {
+void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, EvPool* pool, int group = 0) {
   const Seed& s = ctx->seed;
-  const Engine& g = ctx->eng;
+  Engine g = ctx->eng;  // copy: operand buffers of this slot group
+  g.Bop += (size_t)group * s.npad * g.ncol;
+  g.U += (size_t)group * s.npad * g.ncol;
   const int two_np = (int)(2 * s.npairs);
   K_DISPATCH(s.k, {
     dim3 grid((unsigned)(s.npad / K1_TILE_C), (unsigned)((a.nslot + K1Tile<KK>::TS - 1) / K1Tile<KK>::TS));
@@ -229,9 +235,9 @@ void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, EvPool* pool) {
 
 void drain_pool(lyap_ctx* ctx, EvPool& pool) {
   if (!pool.used) return;
-  CK(cudaEventSynchronize(pool.ev[2 * pool.used - 1]));
   for (int i = 0; i < pool.used; ++i) {
     float ms = 0.f;
+    CK(cudaEventSynchronize(pool.ev[2 * i + 1]));  // the pairs live on different group streams
     CK(cudaEventElapsedTime(&ms, pool.ev[2 * i], pool.ev[2 * i + 1]));
     ctx->stats.k1_ms += ms;
   }
@@ -245,8 +251,9 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   const int b = auto_batch(ctx, nv), mmax = auto_mmax(ctx);
   ensure_engine(ctx, b, mmax);
   Engine& g = ctx->eng;
+  const int G = g.groups;
   CK(cudaMemsetAsync(g.phase, 0, sizeof(int) * b, st));  // PH_FREE
-  CK(cudaMemsetAsync(g.ctrl, 0, sizeof(int) * 8, st));
+  CK(cudaMemsetAsync(g.ctrl, 0, sizeof(int) * 8 * (G + 1), st));
   CK(cudaMemsetAsync(g.X, 0, sizeof(double) * (size_t)b * g.L, st));
   CK(cudaMemsetAsync(g.restarts, 0, sizeof(int) * 3 * (size_t)b, st));
 
@@ -272,49 +279,68 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   a.g0 = s.g0;
   a.hf = s.hf;
   a.F = s.F;
-  a.X = g.X;
-  a.Xin = g.Xin;
-  a.Qb = g.Qb;
-  a.Minv = g.Minv;
-  a.sigma = g.sigma;
-  a.mask = g.mask;
-  a.eta = g.eta;
-  a.H = g.H;
-  a.e = g.e;
-  a.y = g.y;
-  a.bnorm = g.bnorm;
-  a.part = g.part;
-  a.part3 = g.part3;
-  a.part2 = g.part2;
-  a.Rc = g.Rc;
-  a.Rr = g.Rr;
-  a.cf = g.cf;
-  a.phase = g.phase;
-  a.m = g.m;
-  a.vidx = g.vidx;
-  a.applies = g.applies;
-  a.restarts = g.restarts;
-  a.newv = g.restarts + b;
-  a.alist = g.restarts + 2 * b;
-  a.ctrl = g.ctrl;
   a.traces = dtr;
   a.status = dst;
   a.out_applies = dap;
   a.out_resid = dres;
+  a.qctr = g.ctrl + 8 * G;
+  a.Rr = g.Rr;
 
-  K1Args k1{};
-  k1.Xin = g.Xin;
-  k1.L = g.L;
-  k1.nslot = b;
-  k1.mode = 1;
-  k1.mask = g.mask;
-  k1.sigma = g.sigma;
-  k1.phase = g.phase;
-  k1.m = g.m;
-  k1.Qb = g.Qb;
-  k1.qstride = (int64_t)(mmax + 1) * g.L;
-  k1.nactive = g.ctrl + 2;
-  k1.alist = g.restarts + 2 * b;
+  // slot group gi owns slots [s0, s0 + bg): every per-slot array is offset, so the kernels see a
+  // self-contained engine of bg slots; only the v queue and the done counter are shared
+  const int bg0 = (b + G - 1) / G;
+  std::vector<EngArgs> ga(G);
+  std::vector<K1Args> gk(G);
+  std::vector<int> gb(G);
+  for (int gi = 0; gi < G; ++gi) {
+    const int64_t s0 = (int64_t)gi * bg0;
+    const int bg = (int)std::min<int64_t>(bg0, b - s0);
+    gb[gi] = bg;
+    EngArgs x = a;
+    x.b = bg;
+    const int64_t ld = mmax + 1;
+    x.X = g.X + s0 * g.L;
+    x.Xin = g.Xin + s0 * g.L;
+    x.Qb = g.Qb + s0 * ld * g.L;
+    x.Minv = g.Minv + s0 * s.nrep * s.k * s.k * 2;
+    x.sigma = g.sigma + s0 * s.k;
+    x.mask = g.mask + s0 * s.k;
+    x.eta = g.eta + s0 * ld;
+    x.H = g.H + s0 * ld * mmax;
+    x.e = g.e + s0 * ld;
+    x.cs = g.e + (int64_t)b * ld + s0 * mmax;
+    x.sn = g.e + (int64_t)b * ld + (int64_t)b * mmax + s0 * mmax;
+    x.y = g.y + s0 * mmax;
+    x.bnorm = g.bnorm + s0;
+    x.part = g.part + s0 * (mmax + 2) * g.nchunk;
+    x.part2 = g.part2 + s0 * (mmax + 2) * g.nchunk;
+    x.part3 = g.part3 + s0 * g.nchunk * 3;
+    x.Rc = g.Rc + s0 * ld * ld;
+    x.cf = g.cf + s0 * ld;
+    x.phase = g.phase + s0;
+    x.m = g.m + s0;
+    x.vidx = g.vidx + s0;
+    x.applies = g.applies + s0;
+    x.restarts = g.restarts + s0;
+    x.newv = g.restarts + b + s0;
+    x.alist = g.restarts + 2 * b + s0;
+    x.ctrl = g.ctrl + 8 * gi;
+    ga[gi] = x;
+    K1Args k1{};
+    k1.Xin = x.Xin;
+    k1.L = g.L;
+    k1.nslot = bg;
+    k1.mode = 1;
+    k1.mask = x.mask;
+    k1.sigma = x.sigma;
+    k1.phase = x.phase;
+    k1.m = x.m;
+    k1.Qb = x.Qb;
+    k1.qstride = ld * g.L;
+    k1.nactive = x.ctrl + 2;
+    k1.alist = x.alist;
+    gk[gi] = k1;
+  }
 
   EvPool pool;
   EvPool* pp = nullptr;
@@ -323,65 +349,90 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
     for (auto& e : pool.ev) CK(cudaEventCreate(&e));
     pp = &pool;
   }
-  const dim3 grep((unsigned)((s.nrep + 127) / 128), (unsigned)b);
-  const dim3 gred((unsigned)g.nchunk, (unsigned)b);
-  const int assign_threads = (int)roundup(b, 32);
   const size_t upd_smem = sizeof(double) * (mmax + 1);
   const size_t ctrl_smem = sizeof(double) * 16 * (size_t)(mmax + 2);
   const size_t gram_smem = sizeof(double) * (size_t)(mmax + 1);
-  const dim3 gxc((unsigned)std::min<int64_t>((g.L + 255) / 256, 64), (unsigned)b);
+  const size_t bs_smem = sizeof(double) * (size_t)mmax * (mmax + 1) / 2;
+  if (bs_smem > 48 * 1024) CK(cudaFuncSetAttribute(k_backsub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bs_smem));
   if (gram_smem > 48 * 1024) CK(cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_smem));
   if (ctrl_smem > 48 * 1024) CK(cudaFuncSetAttribute(k_ctrl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctrl_smem));
   if (upd_smem > 48 * 1024) CK(cudaFuncSetAttribute(k_upd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem));
   const int64_t per_v = (int64_t)(ctx->opts.max_restarts + 1) * (mmax + 2);
-  const int64_t max_iter = ((nv + b - 1) / b) * per_v + 64;
-  const int poll = 4;
+  const int64_t max_iter = ((nv + bg0 - 1) / bg0) * per_v + 64;
+  const int poll = 8;
+  std::vector<cudaStream_t> sts(G);
+  sts[0] = st;
   CK(cudaEventRecord(ctx->ev0, st));
+  if (G > 1) {
+    if (!ctx->stream2) CK(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
+    if (!ctx->evfork) CK(cudaEventCreateWithFlags(&ctx->evfork, cudaEventDisableTiming));
+    if (!ctx->evjoin) CK(cudaEventCreateWithFlags(&ctx->evjoin, cudaEventDisableTiming));
+    sts[1] = ctx->stream2;
+    CK(cudaEventRecord(ctx->evfork, st));
+    CK(cudaStreamWaitEvent(ctx->stream2, ctx->evfork, 0));
+  }
   int64_t it = 0;
   int rc = LYAP_OK;
   for (;;) {
-    k_assign<<<1, assign_threads, 0, st>>>(a);
-    LAUNCHED();
-    K_DISPATCH(s.k, (k_pfactor<KK><<<grep, 128, 0, st>>>(a)));
-    LAUNCHED();
-    K_DISPATCH(s.k, (k_prec<KK><<<grep, 128, 0, st>>>(a)));
-    LAUNCHED();
-    launch_k1(ctx, k1, st, pp);
-    k_dots<<<gred, 256, 0, st>>>(a);
-    LAUNCHED();
-    k_gram<<<b, 128, gram_smem, st>>>(a);
-    LAUNCHED();
-    k_upd<<<gred, 256, upd_smem, st>>>(a);
-    LAUNCHED();
-    k_ctrl<<<(b + 3) / 4, 128, ctrl_smem, st>>>(a);
-    LAUNCHED();
-    k_xcomb<<<gxc, 256, 0, st>>>(a);
-    LAUNCHED();
-    K_DISPATCH(s.k, (k_xupd<KK><<<grep, 128, 0, st>>>(a)));
-    LAUNCHED();
+    for (int gi = 0; gi < G; ++gi) {
+      const EngArgs& x = ga[gi];
+      const cudaStream_t sg = sts[gi];
+      const int bg = gb[gi];
+      const dim3 grep((unsigned)((s.nrep + 127) / 128), (unsigned)bg);
+      const dim3 gred((unsigned)g.nchunk, (unsigned)bg);
+      const dim3 gxc((unsigned)std::min<int64_t>((g.L + 255) / 256, 64), (unsigned)bg);
+      k_assign<<<1, (int)roundup(bg, 32), 0, sg>>>(x);
+      LAUNCHED();
+      K_DISPATCH(s.k, (k_pfactor<KK><<<grep, 128, 0, sg>>>(x)));
+      LAUNCHED();
+      K_DISPATCH(s.k, (k_prec<KK><<<grep, 128, 0, sg>>>(x)));
+      LAUNCHED();
+      launch_k1(ctx, gk[gi], sg, pp, gi);
+      k_dots<<<gred, 256, 0, sg>>>(x);
+      LAUNCHED();
+      k_gram<<<bg, 128, gram_smem, sg>>>(x);
+      LAUNCHED();
+      k_upd<<<gred, 256, upd_smem, sg>>>(x);
+      LAUNCHED();
+      k_ctrl<<<(bg + 3) / 4, 128, ctrl_smem, sg>>>(x);
+      LAUNCHED();
+      k_backsub<<<bg, 256, bs_smem, sg>>>(x);
+      LAUNCHED();
+      k_xcomb<<<gxc, 256, 0, sg>>>(x);
+      LAUNCHED();
+      K_DISPATCH(s.k, (k_xupd<KK><<<grep, 128, 0, sg>>>(x)));
+      LAUNCHED();
+    }
     ++it;
-    if (pp && pool.used == 512) drain_pool(ctx, pool);
+    if (pp && pool.used >= 512 - G) drain_pool(ctx, pool);
     if (it % poll == 0) {
-      CK(cudaMemcpyAsync(g.h_ctrl, g.ctrl, 8 * sizeof(int), cudaMemcpyDeviceToHost, st));
+      for (int gi = 1; gi < G; ++gi) CK(cudaStreamSynchronize(sts[gi]));
+      CK(cudaMemcpyAsync(g.h_ctrl, g.ctrl, 8 * (G + 1) * sizeof(int), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
-      if (g.h_ctrl[1] >= nv) break;
+      const int done = g.h_ctrl[8 * G + 1];
+      if (done >= nv) break;
       if (it > max_iter) {
-        set_err(ctx, "engine did not finish after %lld iterations (%d of %lld done)", (long long)it, g.h_ctrl[1],
+        set_err(ctx, "engine did not finish after %lld iterations (%d of %lld done)", (long long)it, done,
                 (long long)nv);
         rc = LYAP_ECUDA;
         break;
       }
     }
   }
+  if (G > 1) {
+    CK(cudaEventRecord(ctx->evjoin, ctx->stream2));
+    CK(cudaStreamWaitEvent(st, ctx->evjoin, 0));
+  }
+  CK(cudaMemcpyAsync(g.h_ctrl, g.ctrl, 8 * (G + 1) * sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaEventRecord(ctx->ev1, st));
   CK(cudaEventSynchronize(ctx->ev1));
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
   ctx->stats.batch_ms = ms;
   ctx->stats.iterations += it;
-  {
+  for (int gi = 0; gi < G; ++gi) {
     unsigned long long nvec = 0;
-    std::memcpy(&nvec, g.h_ctrl + 4, 8);
+    std::memcpy(&nvec, g.h_ctrl + 8 * gi + 4, 8);
     ctx->stats.k1_vectors += (int64_t)nvec;
     ctx->stats.k1_flops += 2.0 * (double)s.n * s.n * s.k * s.k * (double)nvec;
   }
@@ -404,7 +455,7 @@ void lyap_default_opts(lyap_opts* o) {
   o->max_dim = 0;
   o->max_restarts = 30;
   o->batch = 0;
-  o->warm_start = 1;
+  o->warm_start = 0;
   o->max_cond_S = 1e8;
   o->device = -1;
   o->profile = 0;
@@ -425,6 +476,9 @@ static void destroy_impl(lyap_ctx* c) {
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->stream2) cudaStreamDestroy(c->stream2);
+  if (c->evfork) cudaEventDestroy(c->evfork);
+  if (c->evjoin) cudaEventDestroy(c->evjoin);
   delete c;
 }
 
@@ -850,8 +904,9 @@ int lyap_apply_C(lyap_ctx* ctx, int64_t nvec, const double* X, const double* sig
     const int b = auto_batch(ctx, std::max<int64_t>(nvec, 1));
     ensure_engine(ctx, std::max(b, ctx->eng.b), ctx->eng.mmax > 0 ? ctx->eng.mmax : auto_mmax(ctx));
     const Engine& g = ctx->eng;
-    for (int64_t v0 = 0; v0 < nvec; v0 += g.b) {
-      const int nb = (int)std::min<int64_t>(g.b, nvec - v0);
+    const int64_t cap = g.ncol / (ctx->seed.k * ctx->seed.k);  // vectors per K1 launch (group 0 buffers)
+    for (int64_t v0 = 0; v0 < nvec; v0 += cap) {
+      const int nb = (int)std::min<int64_t>(cap, nvec - v0);
       K1Args a{};
       a.Xin = X + v0 * g.L;
       a.L = g.L;
@@ -861,7 +916,6 @@ int lyap_apply_C(lyap_ctx* ctx, int64_t nvec, const double* X, const double* sig
       a.Yout = Y + v0 * g.L;
       a.nactive = nullptr;
       a.alist = nullptr;
-      if (nb < g.b) CK(cudaMemsetAsync(g.Bop, 0, sizeof(double) * ctx->seed.npad * g.ncol, st));
       launch_k1(ctx, a, st, nullptr);
       ctx->stats.k1_vectors += nb;
       ctx->stats.k1_flops += 2.0 * (double)ctx->seed.n * ctx->seed.n * ctx->seed.k * ctx->seed.k * nb;

@@ -36,7 +36,7 @@ def test_library_exports_every_declared_symbol():
 def test_default_opts():
     from paper_2312_08201_b200 import default_opts
     o = default_opts()
-    assert o.tol == 1e-12 and o.warm_start == 1 and o.max_restarts == 30 and o.max_cond_S == 1e8
+    assert o.tol == 1e-12 and o.warm_start == 0 and o.max_restarts == 30 and o.max_cond_S == 1e8
 
 
 def test_invalid_args_rejected_before_device():

@@ -1,0 +1,79 @@
+"""The multi-GPU sweep logic (sharding, all-gather of traces, argmin tie-break) on CPU with gloo,
+world_size 2 and 3, against a fake analytic solver; plus shard properties.  (The CUDA engine is
+per-rank and needs no collective; the real NCCL path is the same code in bench.py.)"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2312_08201_b200.sweep import Sweep, shard_indices
+
+
+def fake_tau(v):
+    """Analytic stand-in for trace(E X(v)): the 1-DOF closed form 2/c + c/(2 w^2) with c = 0.1 + v0
+    (minimum at c = 2w, i.e. v0 = 2w - 0.1), plus a small coupling to the other parameters."""
+    w = 1.3
+    c = 0.1 + v[..., 0]
+    return 2.0 / c + c / (2 * w * w) + 1e-3 * np.sum(v[..., 1:] ** 2, axis=-1)
+
+
+@pytest.mark.parametrize("nv,world", [(1, 2), (63, 2), (64, 2), (257, 2), (4096, 3), (5, 4)])
+def test_shards_partition_the_grid(nv, world):
+    parts = [shard_indices(nv, r, world) for r in range(world)]
+    allidx = np.sort(np.concatenate(parts))
+    np.testing.assert_array_equal(allidx, np.arange(nv))
+    sizes = [len(p) for p in parts]
+    assert max(sizes) - min(sizes) <= 64
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, V, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sw = Sweep(len(V), rank, world, torch.device("cpu"))
+        full, am = sw.run(lambda rows: torch.tensor(fake_tau(V[rows]), dtype=torch.float64))
+        out_q.put((rank, full.numpy().copy(), int(am)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_sweep_matches_serial(world):
+    rng = np.random.default_rng(world)
+    g = np.geomspace(0.1, 10.0, 23)
+    V = np.array([[a, b] for a in g for b in (0.5, 1.0, 2.0)])  # 69 rows: ragged over chunks of 64
+    V = np.concatenate([V, V[:5]])  # exact ties: the first occurrence must win
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, V, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ref = fake_tau(V)
+    for rank, full, am in res:
+        np.testing.assert_array_equal(full, ref)  # bitwise: no arithmetic on the gathered values
+        assert am == int(np.argmin(ref))
+    _ = rng
+
+
+def test_single_rank_sweep_no_collective():
+    V = np.random.default_rng(0).uniform(0.1, 5.0, (100, 3))
+    sw = Sweep(len(V), 0, 1, torch.device("cpu"))
+    full, am = sw.run(lambda rows: torch.tensor(fake_tau(V[rows]), dtype=torch.float64))
+    np.testing.assert_array_equal(full.numpy(), fake_tau(V))
+    assert int(am) == int(np.argmin(fake_tau(V)))

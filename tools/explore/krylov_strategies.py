@@ -129,7 +129,7 @@ def main():
         print("  ".join(row), flush=True)
 
 
-if __name__ == "__main__" and sys.argv[1:2] not in (["tiles"], ["seq"], ["var"]):
+if __name__ == "__main__" and sys.argv[1:2] not in (["tiles"], ["seq"], ["var"], ["fixed"]):
     main()
 
 
@@ -464,3 +464,33 @@ def var_main():
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "var":
     var_main()
+
+
+def fixed_main():
+    """One recycle space from a GCRO-DR solve at the grid corner (all v max), reused unchanged."""
+    name, s = sys.argv[2], int(sys.argv[3])
+    sel = sys.argv[4] if len(sys.argv) > 4 else "svd"
+    W = workloads.make(name)
+    sm = Sys(W)
+    shp = W.grid_shape
+    corner = W.V[int(np.ravel_multi_index(tuple(x - 1 for x in shp), shp))]
+    a0, U, TU = gcro_variant(sm, corner, None, None, s=s, sel=sel)
+    a1, U, TU = gcro_variant(sm, corner * 0.9, U, TU, s=s, sel=sel)  # one refinement solve
+    print(f"{name}: building U cost {a0}+{a1} applies", flush=True)
+    lines = {"high": [x - 1 for x in shp], "mixed": [x - 1 if i == 0 else 0 for i, x in enumerate(shp)],
+             "mixed2": [0 if i == 0 else x - 1 for i, x in enumerate(shp)], "mid": [x // 2 for x in shp],
+             "low": [0 for x in shp]}
+    for label, base in lines.items():
+        out = []
+        for q in range(int(__import__("os").environ.get("NSEQ", "4"))):
+            p = list(base)
+            p[-1] = (shp[-1] - 1 - q) if base[-1] == shp[-1] - 1 else min(shp[-1] - 1, base[-1] + q)
+            v = W.V[int(np.ravel_multi_index(tuple(p), shp))]
+            a, _, _ = gcro_variant(sm, v, U, TU, s=s, sel=sel)
+            _, ac = gmres(sm, v, np.zeros_like(sm.g0))
+            out.append(f"{a}/{ac}")
+        print(f"{name} fixed-U {label} (recycled/cold): " + " ".join(out), flush=True)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "fixed":
+    fixed_main()
