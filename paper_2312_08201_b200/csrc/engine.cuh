@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(256) k_dots(EngArgs a) {
 // G = I + E with ||E|| ~ 1e-14, so G^{-1} d = (2I - G) d + O(||E||^2) -- the coefficient CGS2's
 // second pass would produce, computed from the Gram row instead of a second sweep over the basis.
 // c_i (w.r.t. the normalised q_i) is the Hessenberg column; cf_i = c_i / eta_i multiplies q^_i.
-__global__ void __launch_bounds__(128) k_gram(EngArgs a) {
+__global__ void __launch_bounds__(256) k_gram(EngArgs a) {
   extern __shared__ double ds[];  // mmax + 1
   const int slot = blockIdx.x;
   if (a.phase[slot] != PH_ITER) return;
@@ -346,22 +346,20 @@ __global__ void __launch_bounds__(128) k_gram(EngArgs a) {
     }
   }
   __syncthreads();
-  // c = 2 d - G d : thread owns rows i = tid + 128 r; row j of G is contiguous across threads
+  // c = 2 d - G d : one warp per row, the row read coalesced across the lanes
   double* Hc = a.H + (int64_t)slot * ld * a.mmax + (int64_t)m * ld;
   double* cf = a.cf + (int64_t)slot * ld;
-  for (int i = threadIdx.x; i <= m; i += blockDim.x) {
-    double c0 = 2.0 * ds[i], c1 = 0.0, c2 = 0.0, c3 = 0.0;
-    int j = 0;
-    for (; j + 3 <= m; j += 4) {
-      c0 -= G[(int64_t)j * ld + i] * ds[j];
-      c1 -= G[(int64_t)(j + 1) * ld + i] * ds[j + 1];
-      c2 -= G[(int64_t)(j + 2) * ld + i] * ds[j + 2];
-      c3 -= G[(int64_t)(j + 3) * ld + i] * ds[j + 3];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int i = warp; i <= m; i += nw) {
+    const double* Gi = G + (int64_t)i * ld;
+    double acc = 0.0;
+    for (int j = lane; j <= m; j += 32) acc += Gi[j] * ds[j];
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      const double c = 2.0 * ds[i] - acc;
+      Hc[i] = c;
+      cf[i] = c / eta[i];
     }
-    for (; j <= m; ++j) c0 -= G[(int64_t)j * ld + i] * ds[j];
-    const double c = (c0 + c1) + (c2 + c3);
-    Hc[i] = c;
-    cf[i] = c / eta[i];
   }
 }
 
@@ -509,15 +507,20 @@ __global__ void __launch_bounds__(128) k_ctrl(EngArgs a) {
 // triangular R, m1 x m1, packed by columns) is staged in shared memory with one coalesced load,
 // then one warp runs the back substitution with y distributed over the lanes (shuffle broadcast).
 __global__ void __launch_bounds__(256) k_backsub(EngArgs a) {
-  extern __shared__ double Rs[];  // m1 (m1 + 1) / 2
+  extern __shared__ double Rs[];  // m1 (m1 + 1) / 2, then m1 reciprocal diagonal entries
   const int slot = blockIdx.x;
   if (a.phase[slot] != PH_XUPD) return;
   const int ld = a.mmax + 1;
   const int m1 = a.m[slot];
   const double* H = a.H + (int64_t)slot * ld * a.mmax;
+  double* dinv = Rs + m1 * (m1 + 1) / 2;
   for (int j = threadIdx.x >> 5; j < m1; j += blockDim.x >> 5) {
     const int off = j * (j + 1) / 2;
-    for (int i = threadIdx.x & 31; i <= j; i += 32) Rs[off + i] = H[(int64_t)j * ld + i];
+    for (int i = threadIdx.x & 31; i <= j; i += 32) {
+      const double h = H[(int64_t)j * ld + i];
+      Rs[off + i] = h;
+      if (i == j) dinv[j] = h != 0.0 ? 1.0 / h : 0.0;
+    }
   }
   __syncthreads();
   if (threadIdx.x >= 32) return;
@@ -537,9 +540,7 @@ __global__ void __launch_bounds__(256) k_backsub(EngArgs a) {
 #pragma unroll
     for (int r = 0; r < CTRL_RMAX; ++r)
       if (r == rj) yj = yv[r];
-    yj = __shfl_sync(0xffffffffu, yj, owner);
-    const double dj = Rj[j];
-    yj = dj != 0.0 ? yj / dj : 0.0;
+    yj = __shfl_sync(0xffffffffu, yj, owner) * dinv[j];
 #pragma unroll
     for (int r = 0; r < CTRL_RMAX; ++r) {
       const int i = lane + 32 * r;
@@ -561,24 +562,31 @@ __global__ void __launch_bounds__(256) k_backsub(EngArgs a) {
 // P^{-1} blocks then act per representative.  Xin (consumed by K1 earlier in the iteration) holds
 // the combination in between.
 __global__ void __launch_bounds__(256) k_xcomb(EngArgs a) {
+  // 64 elements x 4 slices of the basis index per block; slices reduced in shared memory
   __shared__ double ys[1024];
+  __shared__ double red[4][64];
   const int slot = blockIdx.y;
   if (a.phase[slot] != PH_XUPD) return;
   const int m1 = a.m[slot];
   for (int i = threadIdx.x; i < m1; i += blockDim.x) ys[i] = a.y[(int64_t)slot * a.mmax + i];
   __syncthreads();
   const double* Q = a.Qb + (int64_t)slot * (a.mmax + 1) * a.L;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < a.L; e += (int64_t)gridDim.x * blockDim.x) {
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int i = 0;
-    for (; i + 3 < m1; i += 4) {
-      s0 += ys[i] * Q[(int64_t)i * a.L + e];
-      s1 += ys[i + 1] * Q[(int64_t)(i + 1) * a.L + e];
-      s2 += ys[i + 2] * Q[(int64_t)(i + 2) * a.L + e];
-      s3 += ys[i + 3] * Q[(int64_t)(i + 3) * a.L + e];
+  const int el = threadIdx.x & 63, sl = threadIdx.x >> 6;
+  for (int64_t e0 = (int64_t)blockIdx.x * 64; e0 < a.L; e0 += (int64_t)gridDim.x * 64) {
+    const int64_t e = e0 + el;
+    double s0 = 0.0, s1 = 0.0;
+    if (e < a.L) {
+      int i = sl;
+      for (; i + 4 < m1; i += 8) {
+        s0 += ys[i] * Q[(int64_t)i * a.L + e];
+        s1 += ys[i + 4] * Q[(int64_t)(i + 4) * a.L + e];
+      }
+      for (; i < m1; i += 4) s0 += ys[i] * Q[(int64_t)i * a.L + e];
     }
-    for (; i < m1; ++i) s0 += ys[i] * Q[(int64_t)i * a.L + e];
-    a.Xin[(int64_t)slot * a.L + e] = (s0 + s1) + (s2 + s3);
+    red[sl][el] = s0 + s1;
+    __syncthreads();
+    if (sl == 0 && e < a.L) a.Xin[(int64_t)slot * a.L + e] = (red[0][el] + red[1][el]) + (red[2][el] + red[3][el]);
+    __syncthreads();
   }
 }
 

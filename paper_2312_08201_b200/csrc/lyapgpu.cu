@@ -352,7 +352,7 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   const size_t upd_smem = sizeof(double) * (mmax + 1);
   const size_t ctrl_smem = sizeof(double) * 16 * (size_t)(mmax + 2);
   const size_t gram_smem = sizeof(double) * (size_t)(mmax + 1);
-  const size_t bs_smem = sizeof(double) * (size_t)mmax * (mmax + 1) / 2;
+  const size_t bs_smem = sizeof(double) * ((size_t)mmax * (mmax + 1) / 2 + mmax);
   if (bs_smem > 48 * 1024) CK(cudaFuncSetAttribute(k_backsub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bs_smem));
   if (gram_smem > 48 * 1024) CK(cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_smem));
   if (ctrl_smem > 48 * 1024) CK(cudaFuncSetAttribute(k_ctrl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctrl_smem));
@@ -380,7 +380,7 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
       const int bg = gb[gi];
       const dim3 grep((unsigned)((s.nrep + 127) / 128), (unsigned)bg);
       const dim3 gred((unsigned)g.nchunk, (unsigned)bg);
-      const dim3 gxc((unsigned)std::min<int64_t>((g.L + 255) / 256, 64), (unsigned)bg);
+      const dim3 gxc((unsigned)std::min<int64_t>((g.L + 63) / 64, 128), (unsigned)bg);
       k_assign<<<1, (int)roundup(bg, 32), 0, sg>>>(x);
       LAUNCHED();
       K_DISPATCH(s.k, (k_pfactor<KK><<<grep, 128, 0, sg>>>(x)));
@@ -390,7 +390,7 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
       launch_k1(ctx, gk[gi], sg, pp, gi);
       k_dots<<<gred, 256, 0, sg>>>(x);
       LAUNCHED();
-      k_gram<<<bg, 128, gram_smem, sg>>>(x);
+      k_gram<<<bg, 256, gram_smem, sg>>>(x);
       LAUNCHED();
       k_upd<<<gred, 256, upd_smem, sg>>>(x);
       LAUNCHED();
