@@ -190,12 +190,9 @@ void ensure_engine(lyap_ctx* ctx, int b, int mmax) {
 }
 
 // ------------------------------------------------------------------ K1 launch (prologue, GEMM, epilogue)
-struct EvPool {
-  std::vector<cudaEvent_t> ev;
-  int used = 0;
-};
 
-void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, EvPool* pool, int group = 0) {
+void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, cudaEvent_t evb = nullptr, cudaEvent_t eve = nullptr,
+               unsigned evflags = 0, int group = 0) {
   const Seed& s = ctx->seed;
   Engine g = ctx->eng;  // copy: operand buffers of this slot group
   g.Bop += (size_t)group * s.npad * g.ncol;
@@ -208,7 +205,7 @@ void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, EvPool* pool, in
   LAUNCHED();
   {
     const int kpad = (int)roundup(s.n, 16);  // Lf / Bop rows >= n are zero: skip them in K
-    if (pool) CK(cudaEventRecord(pool->ev[2 * pool->used], st));
+    if (evb) CK(cudaEventRecordWithFlags(evb, st, evflags));
     if (s.n <= SMALL_N) {
       dim3 grid((unsigned)(g.ncol / S_BN), (unsigned)(s.npad / S_BM));
       k1_dgemm<S_BM, S_BN, S_WM, S_WN, S_ST><<<grid, SCfg::THREADS, SCfg::SMEM, st>>>(
@@ -219,11 +216,7 @@ void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, EvPool* pool, in
           s.Lf, g.Bop, g.U, (int)s.npad, (int)g.ncol, kpad, (int)s.npad, a.nactive, (int)(s.k * s.k));
     }
     LAUNCHED();
-    if (pool) {
-      CK(cudaEventRecord(pool->ev[2 * pool->used + 1], st));
-      pool->used++;
-    }
-    ctx->stats.k1_launches++;
+    if (eve) CK(cudaEventRecordWithFlags(eve, st, evflags));
   }
   K_DISPATCH(s.k, {
     dim3 grid((unsigned)(s.npad / K1_TILE_C), (unsigned)((a.nslot + K1Tile<KK>::TS - 1) / K1Tile<KK>::TS));
@@ -233,20 +226,19 @@ void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, EvPool* pool, in
   LAUNCHED();
 }
 
-void drain_pool(lyap_ctx* ctx, EvPool& pool) {
-  if (!pool.used) return;
-  for (int i = 0; i < pool.used; ++i) {
-    float ms = 0.f;
-    CK(cudaEventSynchronize(pool.ev[2 * i + 1]));  // the pairs live on different group streams
-    CK(cudaEventElapsedTime(&ms, pool.ev[2 * i], pool.ev[2 * i + 1]));
-    ctx->stats.k1_ms += ms;
-  }
-  pool.used = 0;
-}
 
 // ------------------------------------------------------------------ the batched engine
 int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, double* dtr, int32_t* dst,
-              int32_t* dap, double* dres, cudaStream_t st) {
+              int32_t* dap, double* dres, cudaStream_t user_st) {
+  // the engine runs on the library's own streams (graph capture is illegal on the legacy default
+  // stream a caller may pass); it is ordered after, and the caller's stream after it, by events
+  cudaStream_t st = ctx->stream;
+  if (!ctx->evfork) CK(cudaEventCreateWithFlags(&ctx->evfork, cudaEventDisableTiming));
+  if (!ctx->evjoin) CK(cudaEventCreateWithFlags(&ctx->evjoin, cudaEventDisableTiming));
+  if (user_st != st) {
+    CK(cudaEventRecord(ctx->evfork, user_st));
+    CK(cudaStreamWaitEvent(st, ctx->evfork, 0));
+  }
   const Seed& s = ctx->seed;
   const int b = auto_batch(ctx, nv), mmax = auto_mmax(ctx);
   ensure_engine(ctx, b, mmax);
@@ -342,13 +334,6 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
     gk[gi] = k1;
   }
 
-  EvPool pool;
-  EvPool* pp = nullptr;
-  if (ctx->opts.profile) {
-    pool.ev.resize(2 * 512);
-    for (auto& e : pool.ev) CK(cudaEventCreate(&e));
-    pp = &pool;
-  }
   const size_t upd_smem = sizeof(double) * (mmax + 1);
   const size_t ctrl_smem = sizeof(double) * 16 * (size_t)(mmax + 2);
   const size_t gram_smem = sizeof(double) * (size_t)(mmax + 1);
@@ -365,60 +350,93 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   CK(cudaEventRecord(ctx->ev0, st));
   if (G > 1) {
     if (!ctx->stream2) CK(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
-    if (!ctx->evfork) CK(cudaEventCreateWithFlags(&ctx->evfork, cudaEventDisableTiming));
-    if (!ctx->evjoin) CK(cudaEventCreateWithFlags(&ctx->evjoin, cudaEventDisableTiming));
     sts[1] = ctx->stream2;
     CK(cudaEventRecord(ctx->evfork, st));
     CK(cudaStreamWaitEvent(ctx->stream2, ctx->evfork, 0));
   }
+  // one engine iteration of slot group gi on stream sg (optionally with events around the GEMM)
+  auto issue = [&](int gi, cudaStream_t sg, cudaEvent_t evb, cudaEvent_t eve, unsigned evflags) -> int64_t {
+    const int64_t l0 = ctx->stats.kernel_launches;
+    const EngArgs& x = ga[gi];
+    const int bg = gb[gi];
+    const dim3 grep((unsigned)((s.nrep + 127) / 128), (unsigned)bg);
+    const dim3 gred((unsigned)g.nchunk, (unsigned)bg);
+    const dim3 gxc((unsigned)std::min<int64_t>((g.L + 63) / 64, 128), (unsigned)bg);
+    k_assign<<<1, (int)roundup(bg, 32), 0, sg>>>(x);
+    LAUNCHED();
+    K_DISPATCH(s.k, (k_pfactor<KK><<<grep, 128, 0, sg>>>(x)));
+    LAUNCHED();
+    K_DISPATCH(s.k, (k_prec<KK><<<grep, 128, 0, sg>>>(x)));
+    LAUNCHED();
+    launch_k1(ctx, gk[gi], sg, evb, eve, evflags, gi);
+    k_dots<<<gred, 256, 0, sg>>>(x);
+    LAUNCHED();
+    k_gram<<<bg, 256, gram_smem, sg>>>(x);
+    LAUNCHED();
+    k_upd<<<gred, 256, upd_smem, sg>>>(x);
+    LAUNCHED();
+    k_ctrl<<<(bg + 3) / 4, 128, ctrl_smem, sg>>>(x);
+    LAUNCHED();
+    k_backsub<<<bg, 256, bs_smem, sg>>>(x);
+    LAUNCHED();
+    k_xcomb<<<gxc, 256, 0, sg>>>(x);
+    LAUNCHED();
+    K_DISPATCH(s.k, (k_xupd<KK><<<grep, 128, 0, sg>>>(x)));
+    LAUNCHED();
+    return ctx->stats.kernel_launches - l0;
+  };
+  // CUDA graphs: `poll` iterations per group are captured once (each with its own GEMM event pair
+  // when profiling) and replayed; the host only polls the done counter between replays.
+  const bool prof = ctx->opts.profile != 0;
+  std::vector<cudaEvent_t> evs;
+  if (prof) {
+    evs.resize((size_t)2 * G * poll);
+    for (auto& e : evs) CK(cudaEventCreate(&e));
+  }
+  std::vector<cudaGraphExec_t> gexec(G, nullptr);
+  int64_t launches_per_replay = 0;
+  for (int gi = 0; gi < G; ++gi) {
+    cudaGraph_t graph;
+    CK(cudaStreamBeginCapture(sts[gi], cudaStreamCaptureModeThreadLocal));
+    for (int p = 0; p < poll; ++p) {
+      cudaEvent_t eb = prof ? evs[(size_t)2 * (gi * poll + p)] : nullptr;
+      cudaEvent_t ee = prof ? evs[(size_t)2 * (gi * poll + p) + 1] : nullptr;
+      launches_per_replay += issue(gi, sts[gi], eb, ee, cudaEventRecordExternal);
+    }
+    CK(cudaStreamEndCapture(sts[gi], &graph));
+    CK(cudaGraphInstantiate(&gexec[gi], graph, 0));
+    CK(cudaGraphDestroy(graph));
+  }
+  ctx->stats.kernel_launches -= launches_per_replay;  // counted per replay below
   int64_t it = 0;
   int rc = LYAP_OK;
   for (;;) {
-    for (int gi = 0; gi < G; ++gi) {
-      const EngArgs& x = ga[gi];
-      const cudaStream_t sg = sts[gi];
-      const int bg = gb[gi];
-      const dim3 grep((unsigned)((s.nrep + 127) / 128), (unsigned)bg);
-      const dim3 gred((unsigned)g.nchunk, (unsigned)bg);
-      const dim3 gxc((unsigned)std::min<int64_t>((g.L + 63) / 64, 128), (unsigned)bg);
-      k_assign<<<1, (int)roundup(bg, 32), 0, sg>>>(x);
-      LAUNCHED();
-      K_DISPATCH(s.k, (k_pfactor<KK><<<grep, 128, 0, sg>>>(x)));
-      LAUNCHED();
-      K_DISPATCH(s.k, (k_prec<KK><<<grep, 128, 0, sg>>>(x)));
-      LAUNCHED();
-      launch_k1(ctx, gk[gi], sg, pp, gi);
-      k_dots<<<gred, 256, 0, sg>>>(x);
-      LAUNCHED();
-      k_gram<<<bg, 256, gram_smem, sg>>>(x);
-      LAUNCHED();
-      k_upd<<<gred, 256, upd_smem, sg>>>(x);
-      LAUNCHED();
-      k_ctrl<<<(bg + 3) / 4, 128, ctrl_smem, sg>>>(x);
-      LAUNCHED();
-      k_backsub<<<bg, 256, bs_smem, sg>>>(x);
-      LAUNCHED();
-      k_xcomb<<<gxc, 256, 0, sg>>>(x);
-      LAUNCHED();
-      K_DISPATCH(s.k, (k_xupd<KK><<<grep, 128, 0, sg>>>(x)));
-      LAUNCHED();
-    }
-    ++it;
-    if (pp && pool.used >= 512 - G) drain_pool(ctx, pool);
-    if (it % poll == 0) {
-      for (int gi = 1; gi < G; ++gi) CK(cudaStreamSynchronize(sts[gi]));
-      CK(cudaMemcpyAsync(g.h_ctrl, g.ctrl, 8 * (G + 1) * sizeof(int), cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      const int done = g.h_ctrl[8 * G + 1];
-      if (done >= nv) break;
-      if (it > max_iter) {
-        set_err(ctx, "engine did not finish after %lld iterations (%d of %lld done)", (long long)it, done,
-                (long long)nv);
-        rc = LYAP_ECUDA;
-        break;
+    for (int gi = 0; gi < G; ++gi) CK(cudaGraphLaunch(gexec[gi], sts[gi]));
+    it += poll;
+    ctx->stats.kernel_launches += launches_per_replay;
+    ctx->stats.k1_launches += (int64_t)G * poll;
+    for (int gi = 1; gi < G; ++gi) CK(cudaStreamSynchronize(sts[gi]));
+    CK(cudaMemcpyAsync(g.h_ctrl, g.ctrl, 8 * (G + 1) * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (prof) {
+      for (size_t i = 0; i < evs.size(); i += 2) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, evs[i], evs[i + 1]));
+        ctx->stats.k1_ms += ms;
       }
     }
+    const int done = g.h_ctrl[8 * G + 1];
+    if (done >= nv) break;
+    if (it > max_iter) {
+      set_err(ctx, "engine did not finish after %lld iterations (%d of %lld done)", (long long)it, done,
+              (long long)nv);
+      rc = LYAP_ECUDA;
+      break;
+    }
   }
+  for (auto& ge : gexec)
+    if (ge) cudaGraphExecDestroy(ge);
+  for (auto& e : evs) cudaEventDestroy(e);
   if (G > 1) {
     CK(cudaEventRecord(ctx->evjoin, ctx->stream2));
     CK(cudaStreamWaitEvent(st, ctx->evjoin, 0));
@@ -426,6 +444,10 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   CK(cudaMemcpyAsync(g.h_ctrl, g.ctrl, 8 * (G + 1) * sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaEventRecord(ctx->ev1, st));
   CK(cudaEventSynchronize(ctx->ev1));
+  if (user_st != st) {
+    CK(cudaEventRecord(ctx->evjoin, st));
+    CK(cudaStreamWaitEvent(user_st, ctx->evjoin, 0));
+  }
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
   ctx->stats.batch_ms = ms;
@@ -435,10 +457,6 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
     std::memcpy(&nvec, g.h_ctrl + 8 * gi + 4, 8);
     ctx->stats.k1_vectors += (int64_t)nvec;
     ctx->stats.k1_flops += 2.0 * (double)s.n * s.n * s.k * s.k * (double)nvec;
-  }
-  if (pp) {
-    drain_pool(ctx, pool);
-    for (auto& e : pool.ev) cudaEventDestroy(e);
   }
   return rc;
 }
@@ -916,7 +934,8 @@ int lyap_apply_C(lyap_ctx* ctx, int64_t nvec, const double* X, const double* sig
       a.Yout = Y + v0 * g.L;
       a.nactive = nullptr;
       a.alist = nullptr;
-      launch_k1(ctx, a, st, nullptr);
+      launch_k1(ctx, a, st);
+      ctx->stats.k1_launches++;
       ctx->stats.k1_vectors += nb;
       ctx->stats.k1_flops += 2.0 * (double)ctx->seed.n * ctx->seed.n * ctx->seed.k * ctx->seed.k * nb;
     }
