@@ -39,6 +39,7 @@ def build(force: bool = False, verbose: bool = False) -> pathlib.Path:
         "-gencode", "arch=compute_100a,code=sm_100a",
         "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v" if verbose else "-O3",
         "-I", str(PKG.parent / "include"),
+        *os.environ.get("LYAP_NVCC_EXTRA", "").split(),
         "-o", str(LIB), *map(str, SOURCES),
         "-lcublas", "-lcusolver",
     ]

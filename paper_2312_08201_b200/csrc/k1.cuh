@@ -86,20 +86,20 @@ __global__ void __launch_bounds__(256) k1_gen(K1Args a, const double* __restrict
 // tile WM x WN of m8n8k4 DMMA fragments.  Shared-memory strides 20 / BN+4 doubles make every
 // fragment load conflict-free (lane -> (row l/4, k l%4) maps onto 16 distinct 8-byte banks per
 // half-warp).
-template <int BM, int BN, int WM, int WN, int STAGES>
+template <int BM, int BN, int WM, int WN, int STAGES, int BK_ = 16>
 struct DgemmCfg {
-  static constexpr int BK = 16, AST = BK + 4, BST = BN + 4;
+  static constexpr int BK = BK_, AST = BK + 4, BST = BN + 4;
   static constexpr int WARPS_N = BN / WN, WARPS = (BM / WM) * (BN / WN), THREADS = WARPS * 32;
   static constexpr int A_STAGE = BM * AST, B_STAGE = BK * BST;
   static constexpr size_t SMEM = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double);
 };
 
-template <int BM, int BN, int WM, int WN, int STAGES>
-__global__ void __launch_bounds__(DgemmCfg<BM, BN, WM, WN, STAGES>::THREADS,
-                                  DgemmCfg<BM, BN, WM, WN, STAGES>::THREADS <= 128 ? 3 : 1)
+template <int BM, int BN, int WM, int WN, int STAGES, int BK_ = 16>
+__global__ void __launch_bounds__(DgemmCfg<BM, BN, WM, WN, STAGES, BK_>::THREADS,
+                                  DgemmCfg<BM, BN, WM, WN, STAGES, BK_>::THREADS <= 128 ? 3 : 1)
     k1_dgemm(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C, int M,
              int N, int Kd, int lda, const int* __restrict__ nactive, int cols_per_active) {
-  using Cfg = DgemmCfg<BM, BN, WM, WN, STAGES>;
+  using Cfg = DgemmCfg<BM, BN, WM, WN, STAGES, BK_>;
   constexpr int BK = Cfg::BK, AST = Cfg::AST, BST = Cfg::BST, NT = Cfg::THREADS;
   constexpr int MT = WM / 8, NTL = WN / 8;
   if (nactive && (int)blockIdx.x * BN >= (*nactive) * cols_per_active) return;  // no active column

@@ -84,13 +84,16 @@ void dfree(void* p) {
 int64_t roundup(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 // K1 GEMM configuration
+#ifndef SMALL_BK
+#define SMALL_BK 16
+#endif
 // large n: 128 x 128 CTA tiles (8 warps of 64 x 32), one CTA per SM
-constexpr int G_BM = 128, G_BN = 128, G_WM = 64, G_WN = 32, G_ST = 4;
-using GCfg = DgemmCfg<G_BM, G_BN, G_WM, G_WN, G_ST>;
+constexpr int G_BM = 128, G_BN = 128, G_WM = 64, G_WN = 32, G_ST = 3, G_BK = 32;
+using GCfg = DgemmCfg<G_BM, G_BN, G_WM, G_WN, G_ST, G_BK>;
 // small n (<= SMALL_N): 64 x 64 tiles (4 warps of 32 x 32), several CTAs per SM -> less padding
 // and finer wave quantisation
-constexpr int S_BM = 64, S_BN = 64, S_WM = 32, S_WN = 32, S_ST = 3;
-using SCfg = DgemmCfg<S_BM, S_BN, S_WM, S_WN, S_ST>;
+constexpr int S_BM = 64, S_BN = 64, S_WM = 32, S_WN = 32, S_ST = 3, S_BK = SMALL_BK;
+using SCfg = DgemmCfg<S_BM, S_BN, S_WM, S_WN, S_ST, S_BK>;
 constexpr int64_t SMALL_N = 1536;
 inline int tile_m(const Seed& s) { return s.n <= SMALL_N ? S_BM : G_BM; }
 inline int tile_n(const Seed& s) { return s.n <= SMALL_N ? S_BN : G_BN; }
@@ -204,15 +207,15 @@ void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, cudaEvent_t evb 
   });
   LAUNCHED();
   {
-    const int kpad = (int)roundup(s.n, 16);  // Lf / Bop rows >= n are zero: skip them in K
+    const int kpad = (int)std::min<int64_t>(roundup(s.n, s.n <= SMALL_N ? S_BK : G_BK), s.npad);  // skip zero rows
     if (evb) CK(cudaEventRecordWithFlags(evb, st, evflags));
     if (s.n <= SMALL_N) {
       dim3 grid((unsigned)(g.ncol / S_BN), (unsigned)(s.npad / S_BM));
-      k1_dgemm<S_BM, S_BN, S_WM, S_WN, S_ST><<<grid, SCfg::THREADS, SCfg::SMEM, st>>>(
+      k1_dgemm<S_BM, S_BN, S_WM, S_WN, S_ST, S_BK><<<grid, SCfg::THREADS, SCfg::SMEM, st>>>(
           s.Lf, g.Bop, g.U, (int)s.npad, (int)g.ncol, kpad, (int)s.npad, a.nactive, (int)(s.k * s.k));
     } else {
       dim3 grid((unsigned)(g.ncol / G_BN), (unsigned)(s.npad / G_BM));
-      k1_dgemm<G_BM, G_BN, G_WM, G_WN, G_ST><<<grid, GCfg::THREADS, GCfg::SMEM, st>>>(
+      k1_dgemm<G_BM, G_BN, G_WM, G_WN, G_ST, G_BK><<<grid, GCfg::THREADS, GCfg::SMEM, st>>>(
           s.Lf, g.Bop, g.U, (int)s.npad, (int)g.ncol, kpad, (int)s.npad, a.nactive, (int)(s.k * s.k));
     }
     LAUNCHED();
@@ -560,9 +563,9 @@ int lyap_setup(int64_t n, int64_t k, const double* A0, const double* Bl, const d
     CKB(cublasSetStream(ctx->cublas, ctx->stream));
     CKS(cusolverDnCreate(&ctx->cusolver));
     CKS(cusolverDnSetStream(ctx->cusolver, ctx->stream));
-    CK(cudaFuncSetAttribute(k1_dgemm<G_BM, G_BN, G_WM, G_WN, G_ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(k1_dgemm<G_BM, G_BN, G_WM, G_WN, G_ST, G_BK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)GCfg::SMEM));
-    CK(cudaFuncSetAttribute(k1_dgemm<S_BM, S_BN, S_WM, S_WN, S_ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(k1_dgemm<S_BM, S_BN, S_WM, S_WN, S_ST, S_BK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)SCfg::SMEM));
     cudaStream_t st = ctx->stream;
     CK(cudaEventRecord(ctx->ev0, st));

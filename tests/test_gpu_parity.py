@@ -213,3 +213,63 @@ def test_slot_groups_deterministic():
     np.testing.assert_array_equal(a, b)
     c = _problem(W.A0, W.Bl, W.Br, W.Q, W.E, batch=32).trace_batch(W.V)  # one group
     assert rel_err(a, c).max() <= 1e-11
+
+
+# ----------------------------------------------------------------------------- edge cases
+def test_all_real_spectrum():
+    """Symmetric A0: every eigenvalue real, no conjugate pairs (n_pairs = 0 folding path)."""
+    rng = np.random.default_rng(21)
+    n, k = 30, 2
+    G = rng.standard_normal((n, n)) / np.sqrt(n)
+    A0 = -(G @ G.T) - 0.5 * np.eye(n)
+    B = rng.standard_normal((n, k)) / np.sqrt(n)
+    Q, E = np.eye(n), np.diag(rng.uniform(0, 1, n))
+    P = _problem(A0, B, B, Q, E)
+    assert P.info["n_pairs"] == 0
+    V = rng.uniform(0.1, 3.0, (19, k))
+    assert rel_err(P.trace_batch(V), oracle.trace_batch(A0, B, B, Q, E, V)).max() <= RTOL
+
+
+def test_kmax_and_asymmetric_E():
+    """k = LYAP_KMAX = 8 and a non-symmetric E (only its symmetric part matters, X = X^T)."""
+    rng = np.random.default_rng(22)
+    n, k = 24, 8
+    A0, Bl, Br, Q, E = workloads.random_stable(n, k, rng, shift=1.5)
+    E = E + 0.3 * np.triu(rng.standard_normal((n, n)), 1)
+    V = rng.uniform(0.05, 1.0, (11, k))
+    P = _problem(A0, Bl, Br, Q, E)
+    assert rel_err(P.trace_batch(V), oracle.trace_batch(A0, Bl, Br, Q, E, V)).max() <= RTOL
+
+
+def test_forced_restarts_still_converge():
+    """A short restart length (m_max = 40, below the ~80 iterations c1's hardest corner needs)
+    forces several GMRES cycles; restarts re-verify the true residual."""
+    W = workloads.make("c1")
+    idx = W.corner_indices()
+    tau, st, ap, rs = _problem(W.A0, W.Bl, W.Br, W.Q, W.E, max_dim=40, max_restarts=100).trace_batch(
+        W.V[idx], return_diagnostics=True)
+    g = _golden("c1")
+    ref = dict(zip(g["indices"], g["traces"]))
+    assert np.all(st == 0) and ap.max() > 42
+    assert rel_err(tau, np.array([ref[i] for i in idx])).max() <= RTOL
+
+
+def test_error_paths():
+    from paper_2312_08201_b200 import LyapError
+    # purely imaginary pair: lambda + conj(lambda) = 0 -> seed Lyapunov operator singular
+    A0 = np.array([[0.0, 1.0], [-1.0, 0.0]])
+    B = np.array([[0.0], [1.0]])
+    with pytest.raises(LyapError) as ei:
+        _problem(A0, B, B, np.eye(2), np.eye(2))
+    assert ei.value.code == 5  # LYAP_ESINGULAR
+    # nearly defective A0 (eigenvector matrix ill-conditioned) with a strict cond(S) limit
+    A1 = np.array([[-1.0, 1e6], [0.0, -1.0 - 1e-9]])
+    with pytest.raises(LyapError) as ei:
+        _problem(A1, B, B, np.eye(2), np.eye(2), max_cond_S=1e4)
+    assert ei.value.code == 4  # LYAP_EEIG
+    # a loose tolerance is honoured (fewer applies, still close)
+    W = workloads.make("c1")
+    tight = _problem(W.A0, W.Bl, W.Br, W.Q, W.E).trace_batch(W.V[:20], return_diagnostics=True)
+    loose = _problem(W.A0, W.Bl, W.Br, W.Q, W.E, tol=1e-6).trace_batch(W.V[:20], return_diagnostics=True)
+    assert loose[2].sum() < tight[2].sum()
+    assert rel_err(loose[0], tight[0]).max() <= 1e-4
