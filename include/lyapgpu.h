@@ -124,6 +124,13 @@ int lyap_get_info(const lyap_ctx* ctx, lyap_info* info);
 int lyap_get_stats(const lyap_ctx* ctx, lyap_stats* stats);
 int lyap_reset_stats(lyap_ctx* ctx);
 
+/* NEXT row f2: the full solution X(v) (n x n, row-major; X is symmetric) for each
+ * of the nv rows of V, eq. (Xsmalllastline): the batch is solved as in
+ * lyap_trace_batch, then X = S X~ S^T with X~ = X~0 + L o (B~l G + G^T B~l^T) generated entrywise
+ * on the device and two n^3 DGEMMs per v (cuBLAS).  Host pointers; X holds nv * n * n doubles;
+ * traces (nullable) as in lyap_trace_batch.  Meant for a few v's (O(n^3) per v). */
+int lyap_solution(lyap_ctx* ctx, int64_t nv, const double* V, double* X, double* traces);
+
 /* K1 alone, for kernel tests and the roofline bench: Y = C(sigma) X = sigma o X - T X for nvec
  * folded real vectors (each k x npad, row-major; the layout of DESIGN.md §3).  X, Y, sigma are
  * DEVICE pointers; sigma is nvec x k (NULL: sigma = 0, i.e. Y = -T X).  Ordered on cuda_stream. */

@@ -126,6 +126,17 @@ class Problem:
             self._check(rc)
         return (tau, st, ap, rs) if return_diagnostics else tau
 
+    def solution(self, V, return_traces: bool = False):
+        """Full X(v) (n x n) for each row of V (NEXT row f2; O(n^3) per v).  Returns (nv, n, n)."""
+        V = _f64(V)
+        if V.ndim == 1:
+            V = V.reshape(-1, self.k)
+        nv = V.shape[0]
+        X = np.empty((nv, self.n, self.n))
+        tau = np.empty(nv)
+        self._check(lib.lyap_solution(self._ctx, nv, V.ctypes.data, X.ctypes.data, tau.ctypes.data))
+        return (X, tau) if return_traces else X
+
     def apply_C(self, X, sigma=None, stream=None):
         """K1 alone: Y = sigma o X - T X for folded vectors X (CUDA tensor, (nvec, k, npad))."""
         import torch

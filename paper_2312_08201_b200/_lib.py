@@ -18,7 +18,7 @@ LYAP_KMAX = 8
 # every symbol include/lyapgpu.h declares (checked by tests/test_abi.py)
 EXPORTED = ("lyap_default_opts", "lyap_setup", "lyap_trace_batch", "lyap_trace_batch_ex", "lyap_get_info",
             "lyap_get_stats", "lyap_reset_stats", "lyap_apply_C", "lyap_export_state", "lyap_destroy",
-            "lyap_last_error")
+            "lyap_last_error", "lyap_solution")
 
 
 class Opts(C.Structure):
@@ -42,7 +42,7 @@ class Stats(C.Structure):
 
 def _load():
     if not LIB_PATH.exists():
-        raise ImportError(f"{LIB_PATH} is not built; run `python -m paper_2312_08201_b200.build` "
+        raise ImportError(f"{LIB_PATH} is not built; run `python paper_2312_08201_b200/build.py` "
                           "(there is no CPU fallback)")
     lib = C.CDLL(str(LIB_PATH))
     P = C.c_void_p
@@ -65,6 +65,8 @@ def _load():
     lib.lyap_apply_C.restype = C.c_int
     lib.lyap_export_state.argtypes = [P, P, P, P, P, P, P]
     lib.lyap_export_state.restype = C.c_int
+    lib.lyap_solution.argtypes = [P, C.c_int64, P, P, P]
+    lib.lyap_solution.restype = C.c_int
     lib.lyap_destroy.argtypes = [P]
     lib.lyap_destroy.restype = None
     lib.lyap_last_error.argtypes = [P]

@@ -1,6 +1,7 @@
 """Build the in-tree CUDA library liblyapgpu.so for sm_100a (explicit nvcc; no JIT cache).
 
-python -m paper_2312_08201_b200.build   (also called by __graft_entry__.build()).
+python paper_2312_08201_b200/build.py [--force] [-v]   (also loaded by path from __graft_entry__.build();
+importing the package would load the library this script builds).
 """
 from __future__ import annotations
 

@@ -24,6 +24,8 @@ struct Seed {
   double* g0 = nullptr;   // k x npad folded right-hand side G0 = B^r^T X~0
   double* hf = nullptr;   // k x npad folded trace weights (tau = t0 + 2 <g, hf>)
   double* Lf = nullptr;   // npad x npad folded Cauchy matrix (K1's A operand), row-major
+  double* Sr = nullptr;   // n x n real eigenvector basis (column-major), kept for lyap_solution
+  double* Qr = nullptr;   // n x n S_r^{-1} Q S_r^{-T} (column-major), kept for lyap_solution
   double t0 = 0.0;
   double wcost[LYAP_KMAX] = {};  // ||B~l_t|| ||B^r_t||: weights of the scheduling cost proxy
 };

@@ -34,6 +34,7 @@ struct EngArgs {
   int* qctr;      // shared by all slot groups: [0] next queue position, [1] finished v's
   double *cs, *sn;  // Givens rotations (b x mmax each)
   double* traces;
+  double* gout;  // optional (lyap_solution): nv x L, the solved folded g of every v
   int32_t* status;
   int32_t* out_applies;
   double* out_resid;
@@ -500,6 +501,16 @@ __global__ void __launch_bounds__(128) k_ctrl(EngArgs a) {
     a.restarts[slot] += 1;
     a.phase[slot] = PH_XUPD;
   }
+}
+
+// k_gout (lyap_solution only): a slot that finished its v in this iteration's k_ctrl is FREE until
+// the next k_assign; copy its solution g to gout[vidx].
+__global__ void __launch_bounds__(256) k_gout(EngArgs a) {
+  const int slot = blockIdx.y;
+  if (a.phase[slot] != PH_FREE) return;
+  const int64_t idx = a.vidx[slot];
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < a.L; e += (int64_t)gridDim.x * blockDim.x)
+    a.gout[idx * a.L + e] = a.X[(int64_t)slot * a.L + e];
 }
 
 // ---------------------------------------------------------------- cycle end: R y = e

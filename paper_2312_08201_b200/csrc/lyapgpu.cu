@@ -232,7 +232,7 @@ void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, cudaEvent_t evb 
 
 // ------------------------------------------------------------------ the batched engine
 int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, double* dtr, int32_t* dst,
-              int32_t* dap, double* dres, cudaStream_t user_st) {
+              int32_t* dap, double* dres, cudaStream_t user_st, double* gout = nullptr) {
   // the engine runs on the library's own streams (graph capture is illegal on the legacy default
   // stream a caller may pass); it is ordered after, and the caller's stream after it, by events
   cudaStream_t st = ctx->stream;
@@ -278,6 +278,7 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   a.status = dst;
   a.out_applies = dap;
   a.out_resid = dres;
+  a.gout = gout;
   a.qctr = g.ctrl + 8 * G;
   a.Rr = g.Rr;
 
@@ -380,6 +381,10 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
     LAUNCHED();
     k_ctrl<<<(bg + 3) / 4, 128, ctrl_smem, sg>>>(x);
     LAUNCHED();
+    if (x.gout) {
+      k_gout<<<dim3((unsigned)std::min<int64_t>((g.L + 255) / 256, 64), (unsigned)bg), 256, 0, sg>>>(x);
+      LAUNCHED();
+    }
     k_backsub<<<bg, 256, bs_smem, sg>>>(x);
     LAUNCHED();
     k_xcomb<<<gxc, 256, 0, sg>>>(x);
@@ -490,7 +495,7 @@ static void destroy_impl(lyap_ctx* c) {
   cudaSetDevice(c->device);
   free_engine(c->eng, false);
   Seed& s = c->seed;
-  void* ps[] = {s.lam, s.bhr, s.btl, s.F, s.g0, s.hf, s.Lf};
+  void* ps[] = {s.lam, s.bhr, s.btl, s.F, s.g0, s.hf, s.Lf, s.Sr, s.Qr};
   for (void* p : ps) dfree(p);
   if (c->cublas) cublasDestroy(c->cublas);
   if (c->cusolver) cusolverDnDestroy(c->cusolver);
@@ -793,6 +798,11 @@ int lyap_setup(int64_t n, int64_t k, const double* A0, const double* Bl, const d
   } catch (Fail f) {
     rc = f.code;
   }
+  if (rc == LYAP_OK) {  // kept for lyap_solution (X = S_r Y S_r^T)
+    ctx->seed.Sr = Sr;
+    ctx->seed.Qr = Qr;
+    Sr = Qr = nullptr;
+  }
   void* tmp[] = {dA, dBl, dBr, dQ, dE, Acm, Qs, Es, Blc, Brc, VR, Sr, Sinv, LU, T1, Qr, Er, Blr, Brr, W, work,
                  t0part, t0d, perm, ipiv, dinfo, ext};
   for (void* p : tmp) dfree(p);
@@ -912,6 +922,59 @@ int lyap_trace_batch_ex(lyap_ctx* ctx, int64_t nv, const double* V, double* trac
 int lyap_trace_batch(lyap_ctx* ctx, int64_t nv, const double* V, double* traces, int32_t* status,
                      int v_on_device, void* cuda_stream) {
   return lyap_trace_batch_ex(ctx, nv, V, traces, status, nullptr, nullptr, v_on_device, cuda_stream);
+}
+
+int lyap_solution(lyap_ctx* ctx, int64_t nv, const double* V, double* X, double* traces) {
+  if (!ctx || nv < 0 || (nv > 0 && (!V || !X))) {
+    set_err(ctx, "lyap_solution: invalid arguments");
+    return LYAP_EINVAL;
+  }
+  if (nv == 0) return LYAP_OK;
+  const Seed& s = ctx->seed;
+  double *dV = nullptr, *dtr = nullptr, *gout = nullptr, *Y = nullptr, *T1 = nullptr, *Xd = nullptr;
+  int32_t* dst = nullptr;
+  int rc = LYAP_OK;
+  try {
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    const int64_t n = s.n, L = s.k * s.npad;
+    dV = dalloc<double>(ctx, (size_t)nv * s.k, false);
+    dtr = dalloc<double>(ctx, nv, false);
+    dst = dalloc<int32_t>(ctx, nv, false);
+    gout = dalloc<double>(ctx, (size_t)nv * L);
+    Y = dalloc<double>(ctx, (size_t)n * n, false);
+    T1 = dalloc<double>(ctx, (size_t)n * n, false);
+    Xd = dalloc<double>(ctx, (size_t)n * n, false);
+    CK(cudaMemcpyAsync(dV, V, (size_t)nv * s.k * 8, cudaMemcpyHostToDevice, st));
+    rc = run_batch(ctx, nv, dV, nullptr, dtr, dst, nullptr, nullptr, st, gout);
+    if (rc == LYAP_OK) {
+      std::vector<int32_t> hs(nv);
+      CK(cudaMemcpyAsync(hs.data(), dst, nv * 4, cudaMemcpyDeviceToHost, st));
+      if (traces) CK(cudaMemcpyAsync(traces, dtr, nv * 8, cudaMemcpyDeviceToHost, st));
+      const double one = 1.0, zero = 0.0;
+      const int ni = (int)n;
+      for (int64_t v = 0; v < nv; ++v) {
+        k_solution_Y<<<dim3((unsigned)((n + 127) / 128), (unsigned)n), 128, 0, st>>>(
+            s.lam, s.Qr, s.btl, gout + v * L, n, s.npad, s.k, 2 * s.npairs, Y);
+        LAUNCHED();
+        CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, ni, ni, ni, &one, s.Sr, ni, Y, ni, &zero, T1, ni));
+        CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_T, ni, ni, ni, &one, T1, ni, s.Sr, ni, &zero, Xd, ni));
+        CK(cudaMemcpyAsync(X + v * n * n, Xd, (size_t)n * n * 8, cudaMemcpyDeviceToHost, st));
+      }
+      CK(cudaStreamSynchronize(st));
+      for (int64_t v = 0; v < nv; ++v)
+        if (hs[v] != 0) {
+          rc = LYAP_EPARTIAL;
+          set_err(ctx, "v %lld: status %d", (long long)v, (int)hs[v]);
+          break;
+        }
+    }
+  } catch (Fail f) {
+    rc = f.code;
+  }
+  void* ps[] = {dV, dtr, gout, Y, T1, Xd, dst};
+  for (void* p : ps) dfree(p);
+  return rc;
 }
 
 int lyap_apply_C(lyap_ctx* ctx, int64_t nvec, const double* X, const double* sigma, double* Y, void* cuda_stream) {

@@ -273,3 +273,36 @@ def test_error_paths():
     loose = _problem(W.A0, W.Bl, W.Br, W.Q, W.E, tol=1e-6).trace_batch(W.V[:20], return_diagnostics=True)
     assert loose[2].sum() < tight[2].sum()
     assert rel_err(loose[0], tight[0]).max() <= 1e-4
+
+
+# ----------------------------------------------------------------------------- NEXT row f2
+@pytest.mark.parametrize("case", ["c1", "random_mixed", "random_real"])
+def test_full_solution_matches_oracle(case):
+    """lyap_solution: X(v) elementwise against the oracle's Bartels-Stewart X."""
+    rng = np.random.default_rng(31)
+    if case == "c1":
+        W = workloads.make("c1")
+        A0, Bl, Br, Q, E = W.A0, W.Bl, W.Br, W.Q, W.E
+        V = W.V[W.corner_indices()]
+    elif case == "random_mixed":
+        A0, Bl, Br, Q, E = workloads.random_stable(23, 3, rng)
+        V = rng.uniform(0.1, 2.0, (4, 3))
+    else:
+        n = 17
+        G = rng.standard_normal((n, n)) / np.sqrt(n)
+        A0 = -(G @ G.T) - 0.5 * np.eye(n)
+        Bl = rng.standard_normal((n, 2)) / np.sqrt(n)
+        Br = rng.standard_normal((n, 2)) / np.sqrt(n)
+        Q, E = np.eye(n), np.eye(n)
+        V = rng.uniform(0.1, 1.0, (3, 2))
+    P = _problem(A0, Bl, Br, Q, E)
+    X, tau = P.solution(V, return_traces=True)
+    for i, v in enumerate(V):
+        _, d = oracle.trace_EX(A0, Bl, Br, Q, E, v, diagnostics=True)
+        Xo = d["X"]
+        assert np.abs(X[i] - Xo).max() <= 1e-9 * np.abs(Xo).max()
+        A = oracle.form_A(A0, Bl, Br, v)
+        R = A @ X[i] + X[i] @ A.T + Q
+        assert np.linalg.norm(R) <= 1e-9 * np.linalg.norm(Q) * max(1.0, np.linalg.norm(X[i]))
+        assert tau[i] == pytest.approx(float(np.sum(0.5 * (E + E.T) * X[i])), rel=1e-9)
+    P.close()
