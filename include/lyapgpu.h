@@ -101,6 +101,14 @@ void lyap_default_opts(lyap_opts* opts);
 int lyap_setup(int64_t n, int64_t k, const double* A0, const double* Bl, const double* Br,
                const double* Q, const double* E, const lyap_opts* opts, lyap_ctx** out);
 
+/* NEXT row f4: a new context for the same A0, Q, E with other damper / edge
+ * configurations (Bl, Br: n x k, k may differ from base's).  Reuses base's eigendecomposition,
+ * S_r^{-1}, Q_r, E_r and folded Cauchy matrix (shared, reference-counted: base may be destroyed
+ * first); costs two n x n x k DGEMMs plus O(n^2 k^2) instead of the O(n^3) eig.  opts NULL: base's.
+ * Errors: LYAP_EINVAL, LYAP_ENOMEM, LYAP_ECUDA. */
+int lyap_setup_like(const lyap_ctx* base, int64_t k, const double* Bl, const double* Br, const lyap_opts* opts,
+                    lyap_ctx** out);
+
 /* Online stage: traces[i] = trace(E X(V[i,:])) for the nv rows of V (nv x k, row-major).
  * v_on_device = 0: V, traces, status are host pointers; the call is synchronous.
  * v_on_device = 1: all three are device pointers (e.g. torch data_ptr()) and the work is

@@ -61,6 +61,21 @@ class Problem:
             raise LyapError(rc, lib.lyap_last_error(None).decode())
         self.n, self.k = n, k
 
+    def like(self, Bl, Br=None) -> "Problem":
+        """Same A0, Q, E with another (Bl, Br) configuration (NEXT row f4): reuses this problem's
+        eigendecomposition and seed basis (lyap_setup_like)."""
+        Bl = _f64(Bl)
+        if Bl.ndim == 1:
+            Bl = Bl[:, None]
+        Br = Bl if Br is None else _f64(Br).reshape(Bl.shape)
+        new = Problem.__new__(Problem)
+        new._ctx = C.c_void_p()
+        rc = lib.lyap_setup_like(self._ctx, Bl.shape[1], _dp(Bl), _dp(Br), None, C.byref(new._ctx))
+        if rc != LYAP_OK:
+            raise LyapError(rc, lib.lyap_last_error(None).decode())
+        new.n, new.k = self.n, Bl.shape[1]
+        return new
+
     # ------------------------------------------------------------------ queries
     @property
     def info(self) -> dict:

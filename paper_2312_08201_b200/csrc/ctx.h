@@ -4,11 +4,29 @@
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
 
+#include <memory>
 #include <string>
 
 #include "../../include/lyapgpu.h"
 
 namespace lyap {
+
+// Everything that depends on A0 (and Q, E) only: shared by every lyap_ctx made with
+// lyap_setup_like from one base (NEXT row f4: several (Bl, Br) configurations for one seed A0).
+struct Basis {
+  int device = 0;
+  double* lam = nullptr;   // npad x 2
+  double* Lf = nullptr;    // npad x npad folded Cauchy matrix
+  double* Sr = nullptr;    // n x n real eigenvector basis (column-major)
+  double* Sinv = nullptr;  // S_r^{-1}
+  double* Qr = nullptr;    // S_r^{-1} Q S_r^{-T}
+  double* Er = nullptr;    // S_r^T E S_r
+  ~Basis() {
+    cudaSetDevice(device);
+    for (double* p : {lam, Lf, Sr, Sinv, Qr, Er})
+      if (p) cudaFree(p);
+  }
+};
 
 // Folded seed state that the per-v engine reads.  Folded real coordinates:
 // eigen index == coordinate; a conjugate pair occupies coords (2r, 2r+1) = (Re, Im) of the
@@ -71,6 +89,7 @@ struct lyap_ctx {
   cusolverDnHandle_t cusolver = nullptr;
   lyap::Seed seed;
   lyap::Engine eng;
+  std::shared_ptr<lyap::Basis> basis;  // lam, Lf, Sr, Qr of `seed` point into it
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evfork = nullptr, evjoin = nullptr;
   cudaStream_t stream2 = nullptr;  // second slot group
 };

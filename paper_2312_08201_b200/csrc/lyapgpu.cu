@@ -469,6 +469,62 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   return rc;
 }
 
+// (Bl, Br)-dependent seed state on top of ctx->basis (NEXT row f4): B~l = S_r^{-1} Bl,
+// B^r = S_r^T Br (DGEMM), then G0, H, F, t0 per representative (k_seed_rep), folding, scheduling
+// weights.  Blc, Brc: device column-major n x k.  Throws Fail.
+void build_config(lyap_ctx* ctx, const double* Blc, const double* Brc) {
+  Seed& s = ctx->seed;
+  const Basis& B = *ctx->basis;
+  cudaStream_t st = ctx->stream;
+  const int64_t n = s.n, k = s.k, two_np = 2 * s.npairs;
+  const int ni = (int)n, ki = (int)k;
+  const double one = 1.0, zero = 0.0;
+  double *Blr = nullptr, *Brr = nullptr, *t0part = nullptr, *t0d = nullptr;
+  try {
+    Blr = dalloc<double>(ctx, (size_t)n * k, false);
+    Brr = dalloc<double>(ctx, (size_t)n * k, false);
+    t0part = dalloc<double>(ctx, s.nrep);
+    t0d = dalloc<double>(ctx, 1);
+    CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, ni, ki, ni, &one, B.Sinv, ni, Blc, ni, &zero, Blr, ni));
+    CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_T, CUBLAS_OP_N, ni, ki, ni, &one, B.Sr, ni, Brc, ni, &zero, Brr, ni));
+    s.g0 = dalloc<double>(ctx, (size_t)k * s.npad);
+    s.hf = dalloc<double>(ctx, (size_t)k * s.npad);
+    s.F = dalloc<double>(ctx, (size_t)s.nrep * k * k * 2);
+    s.bhr = dalloc<double>(ctx, (size_t)s.npad * k);
+    s.btl = dalloc<double>(ctx, (size_t)s.npad * k);
+    K_DISPATCH(k, (k_seed_rep<KK><<<(unsigned)s.nrep, 128, 0, st>>>(B.lam, B.Qr, B.Er, Blr, Brr, n, s.npad, two_np,
+                                                                       s.npairs, s.g0, s.hf, s.F, t0part)));
+    LAUNCHED();
+    k_fold_b<<<(unsigned)((s.npad * k + 255) / 256), 256, 0, st>>>(Blr, Brr, n, s.npad, k, two_np, s.btl, s.bhr);
+    LAUNCHED();
+    k_sum<<<1, 1024, 0, st>>>(t0part, s.nrep, t0d);
+    LAUNCHED();
+    CK(cudaMemcpyAsync(&s.t0, t0d, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    // scheduling weights ||B~l_t|| ||B^r_t|| (folded coordinates)
+    std::vector<double> hb((size_t)s.npad * k), hr((size_t)s.npad * k);
+    CK(cudaMemcpy(hb.data(), s.btl, hb.size() * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(hr.data(), s.bhr, hr.size() * 8, cudaMemcpyDeviceToHost));
+    for (int64_t t = 0; t < k; ++t) {
+      double nb = 0.0, nr = 0.0;
+      for (int64_t c = 0; c < s.npad; ++c) {
+        nb += hb[c * k + t] * hb[c * k + t];
+        nr += hr[c * k + t] * hr[c * k + t];
+      }
+      s.wcost[t] = std::sqrt(nb * nr);
+    }
+    ctx->info.t0 = s.t0;
+    if (!std::isfinite(s.t0)) {
+      set_err(ctx, "seed trace t0 is not finite");
+      throw Fail{LYAP_EEIG};
+    }
+  } catch (Fail) {
+    for (void* p : {(void*)Blr, (void*)Brr, (void*)t0part, (void*)t0d}) dfree(p);
+    throw;
+  }
+  for (void* p : {(void*)Blr, (void*)Brr, (void*)t0part, (void*)t0d}) dfree(p);
+}
+
 }  // namespace
 
 // ====================================================================== C-ABI
@@ -495,12 +551,17 @@ static void destroy_impl(lyap_ctx* c) {
   cudaSetDevice(c->device);
   free_engine(c->eng, false);
   Seed& s = c->seed;
-  void* ps[] = {s.lam, s.bhr, s.btl, s.F, s.g0, s.hf, s.Lf, s.Sr, s.Qr};
+  void* ps[] = {s.bhr, s.btl, s.F, s.g0, s.hf};  // lam, Lf, Sr, Qr belong to the shared Basis
+  if (!c->basis) {  // setup failed before the Basis took ownership
+    dfree(s.lam);
+    dfree(s.Lf);
+  }
   for (void* p : ps) dfree(p);
   if (c->cublas) cublasDestroy(c->cublas);
   if (c->cusolver) cusolverDnDestroy(c->cusolver);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  c->basis.reset();
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->stream2) cudaStreamDestroy(c->stream2);
   if (c->evfork) cudaEventDestroy(c->evfork);
@@ -717,8 +778,6 @@ int lyap_setup(int64_t n, int64_t k, const double* A0, const double* Bl, const d
     CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_T, ni, ni, ni, &one, T1, ni, Sinv, ni, &zero, Qr, ni));
     CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_T, CUBLAS_OP_N, ni, ni, ni, &one, Sr, ni, Es, ni, &zero, T1, ni));
     CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, ni, ni, ni, &one, T1, ni, Sr, ni, &zero, Er, ni));
-    CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, ni, ki, ni, &one, Sinv, ni, Blc, ni, &zero, Blr, ni));
-    CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_T, CUBLAS_OP_N, ni, ki, ni, &one, Sr, ni, Brc, ni, &zero, Brr, ni));
     // ---- eigenvalue extremes
     {
       unsigned long long big = 0x7fefffffffffffffULL;  // DBL_MAX bits
@@ -727,28 +786,25 @@ int lyap_setup(int64_t n, int64_t k, const double* A0, const double* Bl, const d
           s.lam, n, two_np, ext + 2, ext + 3);
       LAUNCHED();
     }
-    // ---- S6-S7: seed quantities per representative, folded
-    s.g0 = dalloc<double>(ctx, (size_t)k * s.npad);
-    s.hf = dalloc<double>(ctx, (size_t)k * s.npad);
-    s.F = dalloc<double>(ctx, (size_t)s.nrep * k * k * 2);
-    s.bhr = dalloc<double>(ctx, (size_t)s.npad * k);
-    s.btl = dalloc<double>(ctx, (size_t)s.npad * k);
     s.Lf = dalloc<double>(ctx, (size_t)s.npad * s.npad, false);
-    t0part = dalloc<double>(ctx, s.nrep);
-    t0d = dalloc<double>(ctx, 1);
-    K_DISPATCH(k, (k_seed_rep<KK><<<(unsigned)s.nrep, 128, 0, st>>>(s.lam, Qr, Er, Blr, Brr, n, s.npad, two_np,
-                                                                       s.npairs, s.g0, s.hf, s.F, t0part)));
-    LAUNCHED();
-    k_fold_b<<<(unsigned)((s.npad * k + 255) / 256), 256, 0, st>>>(Blr, Brr, n, s.npad, k, two_np, s.btl, s.bhr);
-    LAUNCHED();
     k_build_Lf<<<dim3((unsigned)((s.npad + 255) / 256), (unsigned)s.npad), 256, 0, st>>>(s.lam, n, s.npad, two_np,
                                                                                         s.Lf);
     LAUNCHED();
-    k_sum<<<1, 1024, 0, st>>>(t0part, s.nrep, t0d);
-    LAUNCHED();
+    // the A0-only state becomes a shared Basis (lyap_setup_like reuses it)
+    ctx->basis = std::make_shared<Basis>();
+    ctx->basis->device = ctx->device;
+    ctx->basis->lam = s.lam;
+    ctx->basis->Lf = s.Lf;
+    ctx->basis->Sr = Sr;
+    ctx->basis->Sinv = Sinv;
+    ctx->basis->Qr = Qr;
+    ctx->basis->Er = Er;
+    s.Sr = Sr;
+    s.Qr = Qr;
+    Sr = Sinv = Qr = Er = nullptr;
+    (void)ki;
     unsigned long long hext[4];
     CK(cudaMemcpyAsync(hext, ext, sizeof hext, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&s.t0, t0d, 8, cudaMemcpyDeviceToHost, st));
     CK(cudaEventRecord(ctx->ev1, st));
     CK(cudaStreamSynchronize(st));
     double n1S, n1Si, mins, maxl;
@@ -778,35 +834,89 @@ int lyap_setup(int64_t n, int64_t k, const double* A0, const double* Bl, const d
               maxl);
       throw Fail{LYAP_ESINGULAR};
     }
-    {  // scheduling weights ||B~l_t|| ||B^r_t|| (folded coordinates)
-      std::vector<double> hb((size_t)s.npad * k), hr((size_t)s.npad * k);
-      CK(cudaMemcpy(hb.data(), s.btl, hb.size() * 8, cudaMemcpyDeviceToHost));
-      CK(cudaMemcpy(hr.data(), s.bhr, hr.size() * 8, cudaMemcpyDeviceToHost));
-      for (int64_t t = 0; t < k; ++t) {
-        double nb = 0.0, nr = 0.0;
-        for (int64_t c = 0; c < s.npad; ++c) {
-          nb += hb[c * k + t] * hb[c * k + t];
-          nr += hr[c * k + t] * hr[c * k + t];
-        }
-        s.wcost[t] = std::sqrt(nb * nr);
-      }
-    }
-    if (!std::isfinite(s.t0)) {
-      set_err(ctx, "seed trace t0 is not finite");
-      throw Fail{LYAP_EEIG};
-    }
+    build_config(ctx, Blc, Brc);  // (Bl, Br)-dependent part
+    CK(cudaEventRecord(ctx->ev1, st));
+    CK(cudaEventSynchronize(ctx->ev1));
+    CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    in.setup_ms = ms;
   } catch (Fail f) {
     rc = f.code;
-  }
-  if (rc == LYAP_OK) {  // kept for lyap_solution (X = S_r Y S_r^T)
-    ctx->seed.Sr = Sr;
-    ctx->seed.Qr = Qr;
-    Sr = Qr = nullptr;
   }
   void* tmp[] = {dA, dBl, dBr, dQ, dE, Acm, Qs, Es, Blc, Brc, VR, Sr, Sinv, LU, T1, Qr, Er, Blr, Brr, W, work,
                  t0part, t0d, perm, ipiv, dinfo, ext};
   for (void* p : tmp) dfree(p);
   std::free(hwork);
+  if (rc != LYAP_OK) {
+    g_last_error = ctx->err;
+    destroy_impl(ctx);
+    return rc;
+  }
+  *out = ctx;
+  return LYAP_OK;
+}
+
+int lyap_setup_like(const lyap_ctx* base, int64_t k, const double* Bl, const double* Br, const lyap_opts* opts,
+                    lyap_ctx** out) {
+  lyap_ctx* ctx = nullptr;
+  if (!out || !base || !base->basis || k < 1 || k > LYAP_KMAX || !Bl || !Br) {
+    set_err(nullptr, "lyap_setup_like: invalid arguments (base with a basis, k = 1..%d, non-NULL Bl, Br)", LYAP_KMAX);
+    return LYAP_EINVAL;
+  }
+  *out = nullptr;
+  ctx = new lyap_ctx();
+  ctx->opts = opts ? *opts : base->opts;
+  if (!(ctx->opts.tol > 0)) ctx->opts.tol = 1e-12;
+  if (ctx->opts.max_restarts <= 0) ctx->opts.max_restarts = 30;
+  ctx->device = base->device;
+  ctx->basis = base->basis;
+  double *dBl = nullptr, *dBr = nullptr, *Blc = nullptr, *Brc = nullptr;
+  int rc = LYAP_OK;
+  try {
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&ctx->ev0));
+    CK(cudaEventCreate(&ctx->ev1));
+    CKB(cublasCreate(&ctx->cublas));
+    CKB(cublasSetStream(ctx->cublas, ctx->stream));
+    CKS(cusolverDnCreate(&ctx->cusolver));
+    CKS(cusolverDnSetStream(ctx->cusolver, ctx->stream));
+    cudaStream_t st = ctx->stream;
+    CK(cudaEventRecord(ctx->ev0, st));
+    Seed& s = ctx->seed;
+    const Seed& b = base->seed;
+    s.n = b.n;
+    s.k = k;
+    s.npad = b.npad;
+    s.npairs = b.npairs;
+    s.nrep = b.nrep;
+    s.lam = ctx->basis->lam;
+    s.Lf = ctx->basis->Lf;
+    s.Sr = ctx->basis->Sr;
+    s.Qr = ctx->basis->Qr;
+    const int64_t n = s.n;
+    dBl = dalloc<double>(ctx, (size_t)n * k, false);
+    dBr = dalloc<double>(ctx, (size_t)n * k, false);
+    Blc = dalloc<double>(ctx, (size_t)n * k, false);
+    Brc = dalloc<double>(ctx, (size_t)n * k, false);
+    CK(cudaMemcpyAsync(dBl, Bl, (size_t)n * k * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dBr, Br, (size_t)n * k * 8, cudaMemcpyHostToDevice, st));
+    const dim3 tb(32, 8);
+    k_transpose<<<dim3((unsigned)((k + 31) / 32), (unsigned)((n + 31) / 32)), tb, 0, st>>>(dBl, Blc, n, k);
+    LAUNCHED();
+    k_transpose<<<dim3((unsigned)((k + 31) / 32), (unsigned)((n + 31) / 32)), tb, 0, st>>>(dBr, Brc, n, k);
+    LAUNCHED();
+    ctx->info = base->info;
+    ctx->info.k = k;
+    build_config(ctx, Blc, Brc);
+    CK(cudaEventRecord(ctx->ev1, st));
+    CK(cudaEventSynchronize(ctx->ev1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    ctx->info.setup_ms = ms;
+  } catch (Fail f) {
+    rc = f.code;
+  }
+  for (void* p : {(void*)dBl, (void*)dBr, (void*)Blc, (void*)Brc}) dfree(p);
   if (rc != LYAP_OK) {
     g_last_error = ctx->err;
     destroy_impl(ctx);

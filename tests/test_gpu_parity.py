@@ -306,3 +306,27 @@ def test_full_solution_matches_oracle(case):
         assert np.linalg.norm(R) <= 1e-9 * np.linalg.norm(Q) * max(1.0, np.linalg.norm(X[i]))
         assert tau[i] == pytest.approx(float(np.sum(0.5 * (E + E.T) * X[i])), rel=1e-9)
     P.close()
+
+
+# ----------------------------------------------------------------------------- NEXT row f4
+def test_setup_like_other_configuration():
+    """lyap_setup_like: same A0/Q/E, other dampers (different positions and k); equals a fresh setup,
+    matches the oracle, survives destruction of the base (shared, reference-counted basis)."""
+    import gc
+    W = workloads.make("c1")
+    m = W.n // 2
+    base = _problem(W.A0, W.Bl, W.Br, W.Q, W.E)
+    A0c, B3, _, _, _, _ = workloads.chain(50, 100.0, 0.02, [5, 20, 44], modes_in_E=10)
+    np.testing.assert_allclose(A0c, W.A0)
+    other = base.like(B3)
+    assert other.info["setup_ms"] < base.info["setup_ms"]
+    del base
+    gc.collect()
+    rng = np.random.default_rng(41)
+    V = rng.uniform(0.1, 30.0, (12, 3))
+    tau = other.trace_batch(V)
+    fresh = _problem(W.A0, B3, B3, W.Q, W.E).trace_batch(V)
+    assert rel_err(tau, fresh).max() <= 1e-11
+    ref = oracle.trace_batch(W.A0, B3, B3, W.Q, W.E, V[:4])
+    assert rel_err(tau[:4], ref).max() <= RTOL
+    assert m == 50
