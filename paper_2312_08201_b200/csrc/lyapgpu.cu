@@ -210,11 +210,11 @@ void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, cudaEvent_t evb 
     const int kpad = (int)std::min<int64_t>(roundup(s.n, s.n <= SMALL_N ? S_BK : G_BK), s.npad);  // skip zero rows
     if (evb) CK(cudaEventRecordWithFlags(evb, st, evflags));
     if (s.n <= SMALL_N) {
-      dim3 grid((unsigned)(g.ncol / S_BN), (unsigned)(s.npad / S_BM));
+      dim3 grid((unsigned)((g.ncol / S_BN) * (s.npad / S_BM)));
       k1_dgemm<S_BM, S_BN, S_WM, S_WN, S_ST, S_BK><<<grid, SCfg::THREADS, SCfg::SMEM, st>>>(
           s.Lf, g.Bop, g.U, (int)s.npad, (int)g.ncol, kpad, (int)s.npad, a.nactive, (int)(s.k * s.k));
     } else {
-      dim3 grid((unsigned)(g.ncol / G_BN), (unsigned)(s.npad / G_BM));
+      dim3 grid((unsigned)((g.ncol / G_BN) * (s.npad / G_BM)));
       k1_dgemm<G_BM, G_BN, G_WM, G_WN, G_ST, G_BK><<<grid, GCfg::THREADS, GCfg::SMEM, st>>>(
           s.Lf, g.Bop, g.U, (int)s.npad, (int)g.ncol, kpad, (int)s.npad, a.nactive, (int)(s.k * s.k));
     }
