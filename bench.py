@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--max-dim", type=int, default=0)
+    ap.add_argument("--recycle", type=int, default=int(os.environ.get("BENCH_RECYCLE", "0")),
+                    help="recycle-space size s (0: off); spaces built from the 2^k grid corners before timing")
     return ap.parse_args()
 
 
@@ -215,6 +217,11 @@ def main():
     idx = sweep.mine
     P = Problem(W.A0, W.Bl, W.Br, W.Q, W.E, profile=True, device=local, batch=args.batch, max_dim=args.max_dim)
     setup_ms = P.info["setup_ms"]
+    recycle_ms = None
+    if args.recycle > 0:
+        t = time.perf_counter()
+        P.build_recycle(V=W.V, s=args.recycle)
+        recycle_ms = 1e3 * (time.perf_counter() - t)
     Vd = torch.tensor(W.V[idx], device=dev)
 
     def step():
@@ -289,6 +296,7 @@ def main():
               "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded workloads.make)",
               "config": config_dict(W, args, world, {"batch": P.info["batch"], "max_dim": P.info["max_dim"],
                                                      "setup_ms": setup_ms, "argmin_flat_index": argmin,
+                                                     "recycle_s": args.recycle, "recycle_build_ms": recycle_ms,
                                                      "applies_per_v": st["k1_vectors"] / (W.nv * args.steps / world)}),
               "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
               "gpu_launches": st["kernel_launches"]})

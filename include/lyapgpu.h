@@ -139,6 +139,23 @@ int lyap_reset_stats(lyap_ctx* ctx);
  * traces (nullable) as in lyap_trace_batch.  Meant for a few v's (O(n^3) per v). */
 int lyap_solution(lyap_ctx* ctx, int64_t nv, const double* V, double* X, double* traces);
 
+/* Recycling across neighbouring v: nreg shared recycle spaces of s folded x-space
+ * vectors each (U: HOST, nreg x s x k x npad, the layout of lyap_apply_C) and one seed parameter
+ * vector per space (seeds: HOST nreg x k).  T U is computed once here (K1).  In later
+ * lyap_trace_batch calls every v is assigned to the space whose seed is nearest in log|v|, and its
+ * flexible GMRES uses U as the first s search directions (C(v) u = Delta(v) u - T u costs no T-apply:
+ * equivalent to GCRO deflation with span U).  Any U gives the same traces (to the tolerance); a good
+ * U (lyap_build_recycle) saves iterations.  nreg = 0 turns recycling off.  Requires s <= m_max - 8. */
+int lyap_set_recycle(lyap_ctx* ctx, int32_t nreg, int32_t s, const double* U, const double* seeds);
+
+/* Builds the recycle spaces on the device (GCRO-DR-style selection): for each of
+ * the nseeds seed parameter vectors (HOST, nseeds x k, all entries non-zero; e.g. the 2^k corners of
+ * the grid) one right-preconditioned GMRES cycle is recorded; the s smallest singular directions of
+ * C(v_seed) on its search space Z (the generalised eigenproblem (Hbar^T Hbar) p = theta (Z^T Z) p,
+ * cuSOLVER sygvd) give U = Z P, and T U = Delta(v_seed) U - Q Hbar P comes from the Arnoldi relation
+ * without any T-apply.  Replaces the current spaces (as lyap_set_recycle).  s <= m_max - 8. */
+int lyap_build_recycle(lyap_ctx* ctx, int32_t nseeds, const double* seeds, int32_t s);
+
 /* K1 alone, for kernel tests and the roofline bench: Y = C(sigma) X = sigma o X - T X for nvec
  * folded real vectors (each k x npad, row-major; the layout of DESIGN.md §3).  X, Y, sigma are
  * DEVICE pointers; sigma is nvec x k (NULL: sigma = 0, i.e. Y = -T X).  Ordered on cuda_stream. */

@@ -152,6 +152,24 @@ class Problem:
         self._check(lib.lyap_solution(self._ctx, nv, V.ctypes.data, X.ctypes.data, tau.ctypes.data))
         return (X, tau) if return_traces else X
 
+    def build_recycle(self, seeds=None, V=None, s: int = 32):
+        """Recycle spaces from one recorded GMRES cycle per seed (lyap_build_recycle).  seeds (nseeds, k);
+        or V: use the 2^k corners of the bounding box of the rows of V (positive parameters)."""
+        if seeds is None:
+            V = _f64(V).reshape(-1, self.k)
+            lo, hi = V.min(axis=0), V.max(axis=0)
+            import itertools
+            seeds = np.array([[hi[t] if b else lo[t] for t, b in enumerate(bits)]
+                              for bits in itertools.product((0, 1), repeat=self.k)])
+        seeds = _f64(seeds).reshape(-1, self.k)
+        self._check(lib.lyap_build_recycle(self._ctx, seeds.shape[0], seeds.ctypes.data, s))
+
+    def set_recycle(self, U, seeds):
+        """Recycle spaces: U (nreg, s, k, npad) folded x-space vectors, seeds (nreg, k)."""
+        U = _f64(U)
+        seeds = _f64(seeds).reshape(U.shape[0], self.k)
+        self._check(lib.lyap_set_recycle(self._ctx, U.shape[0], U.shape[1], U.ctypes.data, seeds.ctypes.data))
+
     def apply_C(self, X, sigma=None, stream=None):
         """K1 alone: Y = sigma o X - T X for folded vectors X (CUDA tensor, (nvec, k, npad))."""
         import torch

@@ -18,7 +18,8 @@ LYAP_KMAX = 8
 # every symbol include/lyapgpu.h declares (checked by tests/test_abi.py)
 EXPORTED = ("lyap_default_opts", "lyap_setup", "lyap_trace_batch", "lyap_trace_batch_ex", "lyap_get_info",
             "lyap_get_stats", "lyap_reset_stats", "lyap_apply_C", "lyap_export_state", "lyap_destroy",
-            "lyap_last_error", "lyap_solution", "lyap_setup_like")
+            "lyap_last_error", "lyap_solution", "lyap_setup_like", "lyap_set_recycle",
+            "lyap_build_recycle")
 
 
 class Opts(C.Structure):
@@ -67,6 +68,10 @@ def _load():
     lib.lyap_export_state.restype = C.c_int
     lib.lyap_setup_like.argtypes = [P, C.c_int64, dp, dp, C.POINTER(Opts), C.POINTER(P)]
     lib.lyap_setup_like.restype = C.c_int
+    lib.lyap_build_recycle.argtypes = [P, C.c_int32, P, C.c_int32]
+    lib.lyap_build_recycle.restype = C.c_int
+    lib.lyap_set_recycle.argtypes = [P, C.c_int32, C.c_int32, P, P]
+    lib.lyap_set_recycle.restype = C.c_int
     lib.lyap_solution.argtypes = [P, C.c_int64, P, P, P]
     lib.lyap_solution.restype = C.c_int
     lib.lyap_destroy.argtypes = [P]

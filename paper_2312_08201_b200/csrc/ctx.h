@@ -68,12 +68,14 @@ struct Engine {
   double *part2 = nullptr;                        // b x (mmax+2) x nchunk  (Gram-row partials)
   double *Rc = nullptr, *Rr = nullptr;            // b x (mmax+1)^2 Cholesky factor of Q^T Q
   double *cf = nullptr;                           // b x (mmax+1) projection coefficients
+  double *Hraw = nullptr;                         // b x (mmax+1) x mmax unrotated Hessenberg (recycle build)
   int *phase = nullptr, *m = nullptr, *vidx = nullptr, *applies = nullptr, *restarts = nullptr;
   int* ctrl = nullptr;                            // per group 8 ints: [2]=active slots, [4..5]=applied vectors;
                                                   // then 8 shared: [0]=next queue position, [1]=done count
   int* h_ctrl = nullptr;                          // pinned mirror
   int* order = nullptr;                           // queue order (nv_cap)
   int64_t order_cap = 0;
+  int* regq = nullptr;                            // queue position -> recycle regime (nv_cap)
 };
 
 }  // namespace lyap
@@ -90,6 +92,11 @@ struct lyap_ctx {
   lyap::Seed seed;
   lyap::Engine eng;
   std::shared_ptr<lyap::Basis> basis;  // lam, Lf, Sr, Qr of `seed` point into it
+  // recycle spaces (lyap_set_recycle / lyap_build_recycle): nreg x s_rec folded vectors and T U
+  int nreg = 0, s_rec = 0;
+  double *Ureg = nullptr, *TUreg = nullptr;
+  int* sreg = nullptr;  // device: vectors per regime
+  std::string reg_seeds;  // nreg x k doubles (log |v| of each regime's seed), host copy
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evfork = nullptr, evjoin = nullptr;
   cudaStream_t stream2 = nullptr;  // second slot group
 };

@@ -28,6 +28,17 @@ struct EngArgs {
   int max_restarts, warm;
   const double *V, *g0, *hf, *F;
   const int* order;  // queue position -> row of V (null: identity)
+  // recycling: nreg shared spaces of s_rec x-space vectors U and their T U; a v
+  // whose queue position maps to regime r >= 0 runs flexible GMRES with U_r as its first search
+  // directions (C(v) u = Delta(v) u - T u: no T-apply).  regq: queue position -> regime (or -1).
+  int s_rec;                 // stride (max size) of a regime space
+  const int* sreg;           // per regime: number of vectors (<= s_rec)
+  const double *Ureg, *TUreg;
+  const int* regq;
+  int* su;      // per slot: recycle directions of the current v (0 = none)
+  int* reg;     // per slot: regime of the current v
+  int record;   // lyap_build_recycle: stop every slot after its first cycle (keep its Krylov data)
+  double* Hraw; // unrotated Hessenberg columns (b x (mmax+1) x mmax), written when record != 0
   double *X, *Xin, *Qb, *Minv, *sigma, *mask, *eta, *H, *e, *y, *bnorm, *part, *part3;
   double *part2, *Rc, *Rr, *cf;  // Gram-row partials, Gram matrix Q^T Q (Rc; Rr unused), coefficients
   int *phase, *m, *vidx, *applies, *restarts, *ctrl, *newv, *alist;
@@ -87,6 +98,12 @@ __global__ void k_assign(EngArgs a) {
       a.applies[tid] = 0;
       a.restarts[tid] = 0;
       a.newv[tid] = 1;
+      int r = a.regq ? a.regq[qpos] : -1;
+      bool nomask = true;
+      for (int t = 0; t < a.K; ++t) nomask = nomask && (a.V[(int64_t)idx * a.K + t] != 0.0);
+      if (!nomask || a.s_rec <= 0) r = -1;  // masked rows: C(v) u != Delta u - T u there
+      a.reg[tid] = r;
+      a.su[tid] = r >= 0 ? a.sreg[r] : 0;
       a.phase[tid] = PH_VERIFY;
     } else {
       a.phase[tid] = PH_IDLE;
@@ -94,7 +111,12 @@ __global__ void k_assign(EngArgs a) {
   }
   __syncthreads();
   // active slots after assignment (VERIFY or ITER), compacted in slot order for K1
-  int isact = (tid < a.b) ? (a.phase[tid] != PH_IDLE) : 0;
+  // K1-active: VERIFY, and ITER past the recycled directions (those steps need no T-apply)
+  int isact = 0;
+  if (tid < a.b) {
+    const int ph = a.phase[tid];
+    isact = (ph == PH_VERIFY) || (ph == PH_ITER && a.m[tid] >= a.su[tid]);
+  }
   int xa = isact;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -208,6 +230,7 @@ __global__ void __launch_bounds__(128) k_prec(EngArgs a) {
   const int slot = blockIdx.y;
   const int ph = a.phase[slot];
   if (ph != PH_ITER && ph != PH_VERIFY) return;
+  if (ph == PH_ITER && a.m[slot] < a.su[slot]) return;  // recycled direction: no K1 input
   const int64_t rep = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (rep >= a.nrep) return;
   const int64_t c = rep_coord(rep, a.npairs);
@@ -233,6 +256,56 @@ __global__ void __launch_bounds__(128) k_prec(EngArgs a) {
   for (int t = 0; t < K; ++t) {
     xin[t * a.npad + c] = z[t].re;
     if (pair) xin[t * a.npad + c + 1] = z[t].im;
+  }
+}
+
+// lyap_build_recycle helpers: Z[:, j] = P(v)^{-1} q^_j / eta_j (the search directions of the
+// recorded cycle), and TU = Delta(v) U - C(v) U.
+template <int K>
+__global__ void __launch_bounds__(128) k_rec_z(EngArgs a, int slot, int m1, double* __restrict__ Z) {
+  const int j = blockIdx.y;
+  if (j >= m1) return;
+  const int64_t rep = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (rep >= a.nrep) return;
+  const int64_t c = rep_coord(rep, a.npairs);
+  const bool pair = rep < a.npairs;
+  const double sc = 1.0 / a.eta[(int64_t)slot * (a.mmax + 1) + j];
+  const double* q = a.Qb + ((int64_t)slot * (a.mmax + 1) + j) * a.L;
+  cplx r[K], z[K];
+#pragma unroll
+  for (int t = 0; t < K; ++t) r[t] = mk(sc * q[t * a.npad + c], pair ? sc * q[t * a.npad + c + 1] : 0.0);
+  apply_minv<K>(a.Minv + (((int64_t)slot * a.nrep + rep) * K * K) * 2, r, z);
+  double* zo = Z + (int64_t)j * a.L;
+#pragma unroll
+  for (int t = 0; t < K; ++t) {
+    zo[t * a.npad + c] = z[t].re;
+    if (pair) zo[t * a.npad + c + 1] = z[t].im;
+  }
+}
+
+__global__ void k_rec_tu(const double* __restrict__ U, const double* __restrict__ CU, const double* __restrict__ sig,
+                         int64_t L, int64_t npad, int64_t cnt, double* __restrict__ TU) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt * L; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i % L;
+    TU[i] = sig[e / npad] * U[i] - CU[i];
+  }
+}
+
+// ---------------------------------------------------------------- recycled search directions
+// ITER step m < su: the search direction is u_m of the slot's regime space and the candidate is
+// C(v) u_m = sigma o u_m - (T u)_m, elementwise (the T-apply was paid once, when the space was built).
+__global__ void __launch_bounds__(256) k_uapply(EngArgs a) {
+  const int slot = blockIdx.y;
+  if (a.phase[slot] != PH_ITER) return;
+  const int m = a.m[slot];
+  if (m >= a.su[slot]) return;
+  const int r = a.reg[slot];
+  const double* u = a.Ureg + ((int64_t)r * a.s_rec + m) * a.L;
+  const double* tu = a.TUreg + ((int64_t)r * a.s_rec + m) * a.L;
+  double* w = a.Qb + (int64_t)slot * (a.mmax + 1) * a.L + (int64_t)(m + 1) * a.L;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < a.L; e += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(e / a.npad);
+    w[e] = a.sigma[slot * a.K + t] * u[e] - tu[e];
   }
 }
 
@@ -360,6 +433,7 @@ __global__ void __launch_bounds__(256) k_gram(EngArgs a) {
       const double c = 2.0 * ds[i] - acc;
       Hc[i] = c;
       cf[i] = c / eta[i];
+      if (a.record) a.Hraw[(int64_t)slot * ld * a.mmax + (int64_t)m * ld + i] = c;
     }
   }
 }
@@ -442,6 +516,8 @@ __global__ void __launch_bounds__(128) k_ctrl(EngArgs a) {
       a.phase[slot] = PH_FREE;
       atomicAdd(&a.qctr[1], 1);
     } else {
+      // safety net: a v whose recycled space has not helped within two cycles runs plain GMRES
+      if (a.restarts[slot] >= 2) a.su[slot] = 0;
       eta[0] = rho;
       e[0] = rho;
       a.m[slot] = 0;
@@ -473,6 +549,7 @@ __global__ void __launch_bounds__(128) k_ctrl(EngArgs a) {
     const double hn = sqrt(s);
     a.applies[slot] += 1;
     eta[m + 1] = hn > 0.0 ? hn : 1.0;
+    if (a.record) a.Hraw[(int64_t)slot * ld * a.mmax + (int64_t)m * ld + m + 1] = hn;
     double hi = hs[0];
     for (int i = 0; i < m; ++i) {  // apply the previous rotations to the new column
       const double hi1 = hs[i + 1];
@@ -489,8 +566,11 @@ __global__ void __launch_bounds__(128) k_ctrl(EngArgs a) {
     e[m + 1] = -sv * e[m];
     e[m] = c * e[m];
     const double est = fabs(e[m + 1]);
-    done = (est <= a.tol_inner * a.bnorm[slot]) || (m + 1 >= a.mmax) || !(hn > 1e-300 * a.bnorm[slot]) ||
-           !isfinite(est);
+    const bool breakdown = !(hn > 1e-300 * a.bnorm[slot]);
+    done = (est <= a.tol_inner * a.bnorm[slot]) || (m + 1 >= a.mmax) || breakdown || !isfinite(est);
+    // a recycled direction dependent on the current space is not a "lucky" breakdown: finish the
+    // cycle and run this v's restarts as plain GMRES
+    if (breakdown && m < a.su[slot]) a.su[slot] = 0;
     a.m[slot] = m + 1;
   }
   __syncwarp();
@@ -499,7 +579,12 @@ __global__ void __launch_bounds__(128) k_ctrl(EngArgs a) {
   if (!done) return;
   if (lane == 0) {
     a.restarts[slot] += 1;
-    a.phase[slot] = PH_XUPD;
+    if (a.record) {  // keep q^_0..q^_m1, H, eta, Minv of this cycle for the recycle-space build
+      a.phase[slot] = PH_IDLE;
+      atomicAdd(&a.qctr[1], 1);
+    } else {
+      a.phase[slot] = PH_XUPD;
+    }
   }
 }
 
@@ -563,7 +648,7 @@ __global__ void __launch_bounds__(256) k_backsub(EngArgs a) {
 #pragma unroll
   for (int r = 0; r < CTRL_RMAX; ++r) {
     const int i = lane + 32 * r;
-    if (i < m1) y[i] = yv[r] / eta[i];
+    if (i < m1) y[i] = i < a.su[slot] ? yv[r] : yv[r] / eta[i];  // u_i raw; P^{-1} q^_i / eta_i
   }
 }
 
@@ -579,8 +664,18 @@ __global__ void __launch_bounds__(256) k_xcomb(EngArgs a) {
   const int slot = blockIdx.y;
   if (a.phase[slot] != PH_XUPD) return;
   const int m1 = a.m[slot];
-  for (int i = threadIdx.x; i < m1; i += blockDim.x) ys[i] = a.y[(int64_t)slot * a.mmax + i];
+  const int su = min(a.su[slot], m1);
+  for (int i = threadIdx.x; i < m1; i += blockDim.x) ys[i] = i < su ? 0.0 : a.y[(int64_t)slot * a.mmax + i];
   __syncthreads();
+  if (su > 0) {  // recycled directions enter x directly (not through P^{-1})
+    const double* U = a.Ureg + (int64_t)a.reg[slot] * a.s_rec * a.L;
+    const double* ysl = a.y + (int64_t)slot * a.mmax;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < a.L; e += (int64_t)gridDim.x * blockDim.x) {
+      double acc = 0.0;
+      for (int i = 0; i < su; ++i) acc += ysl[i] * U[(int64_t)i * a.L + e];
+      a.X[(int64_t)slot * a.L + e] += acc;
+    }
+  }
   const double* Q = a.Qb + (int64_t)slot * (a.mmax + 1) * a.L;
   const int el = threadIdx.x & 63, sl = threadIdx.x >> 6;
   for (int64_t e0 = (int64_t)blockIdx.x * 64; e0 < a.L; e0 += (int64_t)gridDim.x * 64) {

@@ -115,15 +115,20 @@ inline int tile_n(const Seed& s) { return s.n <= SMALL_N ? S_BN : G_BN; }
 void free_engine(Engine& g, bool keep_order = true) {
   void* ps[] = {g.Bop, g.U, g.Xin, g.X, g.Qb, g.Minv, g.sigma, g.mask, g.eta, g.H, g.e, g.y,
                 g.bnorm, g.part, g.part3, g.phase, g.m, g.vidx, g.applies, g.restarts, g.ctrl,
-                g.part2, g.Rc, g.Rr, g.cf};
+                g.part2, g.Rc, g.Rr, g.cf, g.Hraw};
   for (void* p : ps) dfree(p);
   if (g.h_ctrl) cudaFreeHost(g.h_ctrl);
   int* order = g.order;
+  int* regq = g.regq;
   const int64_t cap = g.order_cap;
-  if (!keep_order) dfree(order);
+  if (!keep_order) {
+    dfree(order);
+    dfree(regq);
+  }
   g = Engine{};
   if (keep_order) {
     g.order = order;
+    g.regq = regq;
     g.order_cap = cap;
   }
 }
@@ -181,11 +186,12 @@ void ensure_engine(lyap_ctx* ctx, int b, int mmax) {
   g.Rc = dalloc<double>(ctx, (size_t)b * (mmax + 1) * (mmax + 1));
   g.Rr = dalloc<double>(ctx, 1);
   g.cf = dalloc<double>(ctx, (size_t)b * (mmax + 1));
+  g.Hraw = dalloc<double>(ctx, (size_t)b * (mmax + 1) * mmax);
   g.phase = dalloc<int>(ctx, b);
   g.m = dalloc<int>(ctx, b);
   g.vidx = dalloc<int>(ctx, b);
   g.applies = dalloc<int>(ctx, b);
-  g.restarts = dalloc<int>(ctx, 3 * (size_t)b);  // restarts | newv | alist
+  g.restarts = dalloc<int>(ctx, 5 * (size_t)b);  // restarts | newv | alist | su | reg
   g.ctrl = dalloc<int>(ctx, 8 * (g.groups + 1));
   CK(cudaMallocHost(&g.h_ctrl, 8 * (g.groups + 1) * sizeof(int)));
   ctx->info.batch = b;
@@ -232,7 +238,8 @@ void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, cudaEvent_t evb 
 
 // ------------------------------------------------------------------ the batched engine
 int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, double* dtr, int32_t* dst,
-              int32_t* dap, double* dres, cudaStream_t user_st, double* gout = nullptr) {
+              int32_t* dap, double* dres, cudaStream_t user_st, double* gout = nullptr, const int* dregq = nullptr,
+              int record = 0) {
   // the engine runs on the library's own streams (graph capture is illegal on the legacy default
   // stream a caller may pass); it is ordered after, and the caller's stream after it, by events
   cudaStream_t st = ctx->stream;
@@ -250,7 +257,8 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   CK(cudaMemsetAsync(g.phase, 0, sizeof(int) * b, st));  // PH_FREE
   CK(cudaMemsetAsync(g.ctrl, 0, sizeof(int) * 8 * (G + 1), st));
   CK(cudaMemsetAsync(g.X, 0, sizeof(double) * (size_t)b * g.L, st));
-  CK(cudaMemsetAsync(g.restarts, 0, sizeof(int) * 3 * (size_t)b, st));
+  CK(cudaMemsetAsync(g.restarts, 0, sizeof(int) * 5 * (size_t)b, st));
+  if (record) CK(cudaMemsetAsync(g.Hraw, 0, sizeof(double) * (size_t)b * (mmax + 1) * mmax, st));
 
   EngArgs a{};
   a.b = b;
@@ -279,6 +287,12 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   a.out_applies = dap;
   a.out_resid = dres;
   a.gout = gout;
+  a.record = record;
+  a.s_rec = (ctx->nreg > 0 && !record) ? ctx->s_rec : 0;
+  a.Ureg = ctx->Ureg;
+  a.sreg = ctx->sreg;
+  a.TUreg = ctx->TUreg;
+  a.regq = ctx->nreg > 0 ? dregq : nullptr;
   a.qctr = g.ctrl + 8 * G;
   a.Rr = g.Rr;
 
@@ -320,6 +334,9 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
     x.restarts = g.restarts + s0;
     x.newv = g.restarts + b + s0;
     x.alist = g.restarts + 2 * b + s0;
+    x.su = g.restarts + 3 * b + s0;
+    x.reg = g.restarts + 4 * b + s0;
+    x.Hraw = g.Hraw + s0 * ld * mmax;
     x.ctrl = g.ctrl + 8 * gi;
     ga[gi] = x;
     K1Args k1{};
@@ -372,6 +389,10 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
     LAUNCHED();
     K_DISPATCH(s.k, (k_prec<KK><<<grep, 128, 0, sg>>>(x)));
     LAUNCHED();
+    if (x.s_rec > 0) {
+      k_uapply<<<dim3((unsigned)std::min<int64_t>((g.L + 255) / 256, 64), (unsigned)bg), 256, 0, sg>>>(x);
+      LAUNCHED();
+    }
     launch_k1(ctx, gk[gi], sg, evb, eve, evflags, gi);
     k_dots<<<gred, 256, 0, sg>>>(x);
     LAUNCHED();
@@ -561,6 +582,9 @@ static void destroy_impl(lyap_ctx* c) {
   if (c->cusolver) cusolverDnDestroy(c->cusolver);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  dfree(c->Ureg);
+  dfree(c->TUreg);
+  dfree(c->sreg);
   c->basis.reset();
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->stream2) cudaStreamDestroy(c->stream2);
@@ -987,8 +1011,36 @@ int lyap_trace_batch_ex(lyap_ctx* ctx, int64_t nv, const double* V, double* trac
       CK(cudaMemcpyAsync(g.order, ord.data(), nv * sizeof(int), cudaMemcpyHostToDevice, st));
       CK(cudaStreamSynchronize(st));
       dorder = g.order;
+      if (ctx->nreg > 0) {  // nearest regime seed in log|v| (host scheduling logic)
+        std::vector<int> rq(nv);
+        const double* seeds = reinterpret_cast<const double*>(ctx->reg_seeds.data());
+        for (int64_t q = 0; q < nv; ++q) {
+          const double* v = &hV[(size_t)ord[q] * k];
+          double best = 1e300;
+          int arg = -1;
+          for (int r = 0; r < ctx->nreg; ++r) {
+            double d2 = 0.0;
+            for (int64_t t = 0; t < k; ++t) {
+              const double dv = std::log(std::fabs(v[t]) + 1e-300) - seeds[r * k + t];
+              d2 += dv * dv;
+            }
+            if (d2 < best) {
+              best = d2;
+              arg = r;
+            }
+          }
+          rq[q] = arg;
+        }
+        if (!g.regq || g.order_cap < nv) {
+          dfree(g.regq);
+          g.regq = dalloc<int>(ctx, std::max<int64_t>(nv, g.order_cap), false);
+        }
+        CK(cudaMemcpyAsync(g.regq, rq.data(), nv * sizeof(int), cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
+      }
     }
-    rc = run_batch(ctx, nv, dV, dorder, dtr, dst, dap, dres, st);
+    rc = run_batch(ctx, nv, dV, dorder, dtr, dst, dap, dres, st, nullptr,
+                   (ctx->nreg > 0 && dorder) ? ctx->eng.regq : nullptr);
     if (rc == LYAP_OK) {
       // any per-v failure -> LYAP_EPARTIAL
       std::vector<int32_t> hs;
@@ -1084,6 +1136,221 @@ int lyap_solution(lyap_ctx* ctx, int64_t nv, const double* V, double* X, double*
   }
   void* ps[] = {dV, dtr, gout, Y, T1, Xd, dst};
   for (void* p : ps) dfree(p);
+  return rc;
+}
+
+int lyap_set_recycle(lyap_ctx* ctx, int32_t nreg, int32_t s, const double* U, const double* seeds) {
+  if (!ctx || nreg < 0 || (nreg > 0 && (s < 1 || !U || !seeds))) {
+    set_err(ctx, "lyap_set_recycle: invalid arguments");
+    return LYAP_EINVAL;
+  }
+  try {
+    CK(cudaSetDevice(ctx->device));
+    dfree(ctx->Ureg);
+    dfree(ctx->TUreg);
+    ctx->Ureg = ctx->TUreg = nullptr;
+    ctx->nreg = ctx->s_rec = 0;
+    if (nreg == 0) return LYAP_OK;
+    const Seed& sd = ctx->seed;
+    const int mmax = auto_mmax(ctx);
+    if (s > mmax - 8) {
+      set_err(ctx, "lyap_set_recycle: s = %d must leave room in the restart length %d", s, mmax);
+      return LYAP_EINVAL;
+    }
+    const int64_t L = sd.k * sd.npad, tot = (int64_t)nreg * s;
+    cudaStream_t st = ctx->stream;
+    ctx->Ureg = dalloc<double>(ctx, (size_t)tot * L, false);
+    ctx->TUreg = dalloc<double>(ctx, (size_t)tot * L, false);
+    CK(cudaMemcpyAsync(ctx->Ureg, U, (size_t)tot * L * 8, cudaMemcpyHostToDevice, st));
+    // T U once (K1 with sigma = 0 gives -T U)
+    CK(lyap_apply_C(ctx, tot, ctx->Ureg, nullptr, ctx->TUreg, st) == LYAP_OK ? cudaSuccess : cudaErrorUnknown);
+    k_negate<<<(unsigned)std::min<int64_t>((tot * L + 255) / 256, 65535), 256, 0, st>>>(ctx->TUreg, tot * L);
+    LAUNCHED();
+    CK(cudaStreamSynchronize(st));
+    std::vector<double> ls((size_t)nreg * sd.k);
+    for (size_t i = 0; i < ls.size(); ++i) ls[i] = std::log(std::fabs(seeds[i]) + 1e-300);
+    ctx->reg_seeds.assign(reinterpret_cast<const char*>(ls.data()), ls.size() * sizeof(double));
+    dfree(ctx->sreg);
+    ctx->sreg = dalloc<int>(ctx, nreg, false);
+    std::vector<int> hsz(nreg, s);
+    CK(cudaMemcpy(ctx->sreg, hsz.data(), nreg * sizeof(int), cudaMemcpyHostToDevice));
+    ctx->nreg = nreg;
+    ctx->s_rec = s;
+  } catch (Fail f) {
+    return f.code;
+  }
+  return LYAP_OK;
+}
+
+int lyap_build_recycle(lyap_ctx* ctx, int32_t nseeds, const double* seeds, int32_t s) {
+  if (!ctx || nseeds < 1 || !seeds || s < 1) {
+    set_err(ctx, "lyap_build_recycle: invalid arguments");
+    return LYAP_EINVAL;
+  }
+  const Seed& sd = ctx->seed;
+  const int64_t k = sd.k, L = sd.k * sd.npad;
+  for (int64_t i = 0; i < (int64_t)nseeds * k; ++i)
+    if (!(seeds[i] != 0.0) || !std::isfinite(seeds[i])) {
+      set_err(ctx, "lyap_build_recycle: seed parameters must be finite and non-zero");
+      return LYAP_EINVAL;
+    }
+  const int mmax = auto_mmax(ctx);
+  if (s > mmax - 8) {
+    set_err(ctx, "lyap_build_recycle: s = %d must leave room in the restart length %d", s, mmax);
+    return LYAP_EINVAL;
+  }
+  double *dV = nullptr, *dtr = nullptr, *Z = nullptr, *Qn = nullptr, *Am = nullptr, *Bm = nullptr, *Wv = nullptr,
+         *work = nullptr, *HP = nullptr, *CU = nullptr, *sig = nullptr, *Unew = nullptr, *TUnew = nullptr;
+  int32_t* dst = nullptr;
+  int* dinfo = nullptr;
+  int rc = LYAP_OK;
+  try {
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    // 1. one recorded GMRES cycle per seed (recycling off while recording)
+    dfree(ctx->Ureg);
+    dfree(ctx->TUreg);
+    ctx->Ureg = ctx->TUreg = nullptr;
+    ctx->nreg = ctx->s_rec = 0;
+    dV = dalloc<double>(ctx, (size_t)nseeds * k, false);
+    dtr = dalloc<double>(ctx, nseeds, false);
+    dst = dalloc<int32_t>(ctx, nseeds, false);
+    CK(cudaMemcpyAsync(dV, seeds, (size_t)nseeds * k * 8, cudaMemcpyHostToDevice, st));
+    rc = run_batch(ctx, nseeds, dV, nullptr, dtr, dst, nullptr, nullptr, st, nullptr, nullptr, 1);
+    if (rc != LYAP_OK) throw Fail{rc};
+    const Engine& g = ctx->eng;
+    std::vector<int> hph(g.b), hm(g.b), hv(g.b);
+    CK(cudaMemcpy(hph.data(), g.phase, g.b * sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(hm.data(), g.m, g.b * sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(hv.data(), g.vidx, g.b * sizeof(int), cudaMemcpyDeviceToHost));
+    std::vector<int> slot_of(nseeds, -1);
+    int s_eff = 1;  // stride: the largest regime size
+    for (int sl = 0; sl < g.b; ++sl)
+      if (hph[sl] == PH_IDLE && hm[sl] >= 1 && hv[sl] >= 0 && hv[sl] < nseeds && slot_of[hv[sl]] < 0) {
+        slot_of[hv[sl]] = sl;
+        s_eff = std::max(s_eff, std::min(s, hm[sl]));
+      }
+    std::vector<int> used;
+    for (int r = 0; r < nseeds; ++r)
+      if (slot_of[r] >= 0) used.push_back(r);
+    if (used.empty()) {
+      set_err(ctx, "lyap_build_recycle: no seed produced a Krylov cycle (all converged immediately)");
+      throw Fail{LYAP_EINVAL};
+    }
+    const int nreg = (int)used.size();
+    const int ld = mmax + 1;
+    Z = dalloc<double>(ctx, (size_t)mmax * L);
+    Qn = dalloc<double>(ctx, (size_t)(mmax + 1) * L, false);
+    Am = dalloc<double>(ctx, (size_t)mmax * mmax, false);
+    Bm = dalloc<double>(ctx, (size_t)mmax * mmax, false);
+    Wv = dalloc<double>(ctx, mmax, false);
+    HP = dalloc<double>(ctx, (size_t)(mmax + 1) * s_eff, false);
+    CU = dalloc<double>(ctx, (size_t)s_eff * L, false);
+    sig = dalloc<double>(ctx, k, false);
+    dinfo = dalloc<int>(ctx, 1);
+    Unew = dalloc<double>(ctx, (size_t)nreg * s_eff * L);
+    TUnew = dalloc<double>(ctx, (size_t)nreg * s_eff * L);
+    std::vector<double> seeds_used;
+    const double one = 1.0, zero = 0.0;
+    // engine args for the helper kernels: slot-indexed arrays of the whole engine
+    EngArgs ea{};
+    ea.mmax = mmax;
+    ea.L = L;
+    ea.npad = sd.npad;
+    ea.nrep = sd.nrep;
+    ea.npairs = sd.npairs;
+    ea.Qb = g.Qb;
+    ea.eta = g.eta;
+    ea.Minv = g.Minv;
+    std::vector<int> sizes(nreg);
+    for (int ri = 0; ri < nreg; ++ri) {
+      const int r = used[ri], sl = slot_of[r], m1 = hm[sl];
+      const int sr = std::min(s, m1);  // this regime's space size (cheap seeds record short cycles)
+      sizes[ri] = sr;
+      // Z = P^{-1} q_j (search directions) and normalised Q (j <= m1)
+      const dim3 gz((unsigned)((sd.nrep + 127) / 128), (unsigned)m1);
+      CK(cudaMemsetAsync(Z, 0, (size_t)m1 * L * 8, st));
+      K_DISPATCH(k, (k_rec_z<KK><<<gz, 128, 0, st>>>(ea, sl, m1, Z)));
+      LAUNCHED();
+      std::vector<double> heta(m1 + 1);
+      CK(cudaMemcpy(heta.data(), g.eta + (int64_t)sl * ld, (m1 + 1) * 8, cudaMemcpyDeviceToHost));
+      for (int j = 0; j <= m1; ++j) {
+        const double inv = 1.0 / heta[j];
+        CKB(cublasDcopy(ctx->cublas, (int)L, g.Qb + ((int64_t)sl * ld + j) * L, 1, Qn + (int64_t)j * L, 1));
+        CKB(cublasDscal(ctx->cublas, (int)L, &inv, Qn + (int64_t)j * L, 1));
+      }
+      const double* Hb = g.Hraw + (int64_t)sl * ld * mmax;  // column-major (m1+1) x m1, ld = mmax + 1
+      // A = Hbar^T Hbar, B = Z^T Z (+ tiny ridge), generalised symmetric eigenproblem A p = theta B p
+      CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_T, CUBLAS_OP_N, m1, m1, m1 + 1, &one, Hb, ld, Hb, ld, &zero, Am, m1));
+      CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_T, CUBLAS_OP_N, m1, m1, (int)L, &one, Z, (int)L, Z, (int)L, &zero, Bm, m1));
+      {
+        std::vector<double> hb((size_t)m1 * m1);
+        CK(cudaMemcpy(hb.data(), Bm, hb.size() * 8, cudaMemcpyDeviceToHost));
+        double tr = 0.0;
+        for (int j = 0; j < m1; ++j) tr += hb[(size_t)j * m1 + j];
+        const double ridge = 1e-10 * tr / m1;
+        for (int j = 0; j < m1; ++j) hb[(size_t)j * m1 + j] += ridge;
+        CK(cudaMemcpy(Bm, hb.data(), hb.size() * 8, cudaMemcpyHostToDevice));
+      }
+      int lwork = 0;
+      CKS(cusolverDnDsygvd_bufferSize(ctx->cusolver, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
+                                      CUBLAS_FILL_MODE_UPPER, m1, Am, m1, Bm, m1, Wv, &lwork));
+      dfree(work);
+      work = dalloc<double>(ctx, std::max(lwork, 1), false);
+      CKS(cusolverDnDsygvd(ctx->cusolver, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, m1,
+                           Am, m1, Bm, m1, Wv, work, lwork, dinfo));
+      int hinfo = 0;
+      CK(cudaMemcpy(&hinfo, dinfo, sizeof(int), cudaMemcpyDeviceToHost));
+      if (hinfo != 0) {
+        // Z^T Z numerically singular: select in the Euclidean metric of the coefficients instead
+        // (smallest right singular vectors of Hbar; measured nearly as effective)
+        CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_T, CUBLAS_OP_N, m1, m1, m1 + 1, &one, Hb, ld, Hb, ld, &zero, Am, m1));
+        int lw2 = 0;
+        CKS(cusolverDnDsyevd_bufferSize(ctx->cusolver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, m1, Am, m1,
+                                        Wv, &lw2));
+        dfree(work);
+        work = dalloc<double>(ctx, std::max(lw2, 1), false);
+        CKS(cusolverDnDsyevd(ctx->cusolver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, m1, Am, m1, Wv, work,
+                             lw2, dinfo));
+        CK(cudaMemcpy(&hinfo, dinfo, sizeof(int), cudaMemcpyDeviceToHost));
+        if (hinfo != 0) {
+          set_err(ctx, "lyap_build_recycle: syevd info = %d for seed %d", hinfo, r);
+          throw Fail{LYAP_ECUDA};
+        }
+      }
+      // P = eigenvectors of the s_eff smallest eigenvalues (ascending: first columns of Am)
+      double* Ur = Unew + (int64_t)ri * s_eff * L;
+      double* TUr = TUnew + (int64_t)ri * s_eff * L;
+      CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)L, sr, m1, &one, Z, (int)L, Am, m1, &zero, Ur,
+                      (int)L));
+      CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, m1 + 1, sr, m1, &one, Hb, ld, Am, m1, &zero, HP,
+                      m1 + 1));
+      CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)L, sr, m1 + 1, &one, Qn, (int)L, HP, m1 + 1,
+                      &zero, CU, (int)L));
+      std::vector<double> hs(k);
+      for (int64_t t = 0; t < k; ++t) hs[t] = 1.0 / seeds[(int64_t)r * k + t];
+      CK(cudaMemcpy(sig, hs.data(), k * 8, cudaMemcpyHostToDevice));
+      k_rec_tu<<<(unsigned)std::min<int64_t>(((int64_t)sr * L + 255) / 256, 65535), 256, 0, st>>>(
+          Ur, CU, sig, L, sd.npad, sr, TUr);
+      LAUNCHED();
+      for (int64_t t = 0; t < k; ++t) seeds_used.push_back(std::log(std::fabs(seeds[(int64_t)r * k + t])));
+    }
+    CK(cudaStreamSynchronize(st));
+    ctx->Ureg = Unew;
+    ctx->TUreg = TUnew;
+    Unew = TUnew = nullptr;
+    dfree(ctx->sreg);
+    ctx->sreg = dalloc<int>(ctx, nreg, false);
+    CK(cudaMemcpy(ctx->sreg, sizes.data(), nreg * sizeof(int), cudaMemcpyHostToDevice));
+    ctx->reg_seeds.assign(reinterpret_cast<const char*>(seeds_used.data()), seeds_used.size() * sizeof(double));
+    ctx->nreg = nreg;
+    ctx->s_rec = s_eff;
+  } catch (Fail f) {
+    rc = f.code;
+  }
+  for (void* p : {(void*)dV, (void*)dtr, (void*)dst, (void*)Z, (void*)Qn, (void*)Am, (void*)Bm, (void*)Wv, (void*)work,
+                  (void*)HP, (void*)CU, (void*)sig, (void*)Unew, (void*)TUnew, (void*)dinfo})
+    dfree(p);
   return rc;
 }
 

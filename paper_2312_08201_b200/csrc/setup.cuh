@@ -350,6 +350,11 @@ __global__ void k_sum(const double* __restrict__ x, int64_t n, double* out) {
   if (threadIdx.x == 0) *out = s;
 }
 
+__global__ void k_negate(double* x, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = -x[i];
+}
+
 __global__ void k_set_identity(double* M, int64_t n) {
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx < n * n) M[idx] = (idx / n == idx % n) ? 1.0 : 0.0;

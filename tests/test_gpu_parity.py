@@ -330,3 +330,45 @@ def test_setup_like_other_configuration():
     ref = oracle.trace_batch(W.A0, B3, B3, W.Q, W.E, V[:4])
     assert rel_err(tau[:4], ref).max() <= RTOL
     assert m == 50
+
+
+# ----------------------------------------------------------------------------- recycling
+def test_recycle_any_space_keeps_parity():
+    """Flexible GMRES with recycled first directions is exact for ANY space: random U (two regimes)
+    must give the oracle's traces; the recycled steps spend no T-apply."""
+    W = workloads.make("c1")
+    P = _problem(W.A0, W.Bl, W.Br, W.Q, W.E)
+    npad, n = P.info["npad"], W.n
+    rng = np.random.default_rng(51)
+    U = rng.standard_normal((2, 12, W.k, npad))
+    U[..., n:] = 0.0
+    seeds = np.array([[0.1, 0.1], [100.0, 100.0]])
+    P.set_recycle(U, seeds)
+    tau, st, ap, rs = P.trace_batch(W.V, return_diagnostics=True)
+    g = _golden("c1")
+    idx = np.array(g["indices"])
+    assert np.all(st == 0)
+    assert rel_err(tau[idx], np.array(g["traces"])).max() <= RTOL
+    P.set_recycle(np.zeros((0, 1, W.k, npad)), np.zeros((0, W.k)))  # off again
+    tau2 = P.trace_batch(W.V)
+    assert rel_err(tau2, tau).max() <= 1e-10
+
+
+@pytest.mark.parametrize("name,s", [("c1", 24), ("c2", 48)])
+def test_recycle_built_spaces_parity_and_savings(name, s):
+    """lyap_build_recycle from the 2^k grid corners: traces still match the oracle samples and the
+    T-applies per v drop."""
+    W = workloads.make(name)
+    P = _problem(W.A0, W.Bl, W.Br, W.Q, W.E)
+    P.reset_stats()
+    P.trace_batch(W.V)
+    t0 = P.stats["k1_vectors"]  # T-applications (recycled steps need none)
+    P.build_recycle(V=W.V, s=s)
+    P.reset_stats()
+    tau, st, ap1, rs = P.trace_batch(W.V, return_diagnostics=True)
+    t1 = P.stats["k1_vectors"]
+    g = _golden(name)
+    idx = np.array(g["indices"])
+    assert np.all(st == 0)
+    assert rel_err(tau[idx], np.array(g["traces"])).max() <= RTOL
+    assert t1 < t0, (t0, t1)
