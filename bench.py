@@ -284,6 +284,28 @@ def main():
                            "MEASURED_PEAKS.json carries no FP64 figure",
             "avg_launch_ms": avg_k1_ms, "launches": st["k1_launches"],
             "k1_share_of_step": st["k1_ms"] / ms if ms > 0 else None}
+    # informational: K1 alone at full width (lyap_apply_C, outside the timed region, nothing else
+    # running), the figure ncu reports per launch; roofline.achieved above is the timed-region average
+    iso = None
+    try:
+        nvec = int(P.info["batch"] + 1) // 2
+        Xt = torch.randn(nvec, W.k, P.info["npad"], dtype=torch.float64, device=dev)
+        Xt[:, :, W.n:] = 0
+        P.apply_C(Xt)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            P.apply_C(Xt)
+        e1.record()
+        torch.cuda.synchronize()
+        t_iso = e0.elapsed_time(e1) / 5 * 1e-3
+        a_iso = 2.0 * W.n ** 2 * W.k ** 2 * nvec / t_iso / 1e12
+        iso = {"vectors": nvec, "ms_per_apply": t_iso * 1e3, "achieved": a_iso, "frac": a_iso / FP64_PEAK_TFLOPS,
+               "note": "whole K1 (prologue + GEMM + epilogue) alone at full width"}
+    except Exception as exc:  # informational only
+        iso = {"error": str(exc)}
+    roof["isolated_k1"] = iso
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         r, cores, cnt, el = oracle_rate(args.config, args.cpu_seconds)
