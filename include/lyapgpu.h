@@ -172,6 +172,25 @@ int lyap_export_state(const lyap_ctx* ctx, double* lam, double* bhr, double* btl
 
 void lyap_destroy(lyap_ctx* ctx);
 
+/* ---- NEXT row f1: extended-Krylov projection (§2.2, Alg. 1) ----------
+ * For large n where eig(A0) is unaffordable but solves with A0 are (Assumption 3): one basis of
+ * EK_m(A0, P), P = [X0 Br, Bl], for every v; the projected equation eq. (param_projected) is solved by
+ * the dense engine above (dimension 4mk; k instances, the right-hand side being linear in v); the
+ * space grows by 4k columns per step until the backward error of Prop. 2.1 is
+ * <= eps on a sample of the batch.  The result is an APPROXIMATION controlled by eps.
+ * lyap_ek_setup: A0 (n x n), Bl, Br (n x k), X0Br = X0 Br (n x k; the seed solution's action, from a
+ * closed form or any Lyapunov solver), E (n x n, symmetrised), trEX0 = trace(E X0); all host,
+ * row-major.  max_dim caps the basis (default 400 columns).  LU of A0 on the device (cuSOLVER).
+ * lyap_ek_trace_batch: host V (nv x k) -> traces (nv); dim_used / bwd_err (nullable): basis size
+ * and the largest sampled backward error.  max_steps bounds the expansions of this call. */
+typedef struct lyap_ek lyap_ek;
+int lyap_ek_setup(int64_t n, int64_t k, const double* A0, const double* Bl, const double* Br, const double* X0Br,
+                  const double* E, double trEX0, int32_t max_dim, lyap_ek** out);
+int lyap_ek_trace_batch(lyap_ek* ek, int64_t nv, const double* V, double eps, int32_t max_steps, double* traces,
+                        int32_t* dim_used, double* bwd_err);
+void lyap_ek_destroy(lyap_ek* ek);
+const char* lyap_ek_last_error(const lyap_ek* ek);
+
 /* Message of the last failure on this ctx; lyap_last_error(NULL) gives the last failure of the
  * calling thread when no ctx was produced (e.g. a failed lyap_setup).  Never NULL. */
 const char* lyap_last_error(const lyap_ctx* ctx);

@@ -16,7 +16,7 @@ import numpy as np
 
 from ._lib import (EXPORTED, LYAP_EPARTIAL, LYAP_KMAX, LYAP_OK, Info, LyapError, Opts, Stats, lib)
 
-__all__ = ["Problem", "LyapError", "lib", "EXPORTED", "LYAP_KMAX", "default_opts"]
+__all__ = ["Problem", "EKProblem", "LyapError", "lib", "EXPORTED", "LYAP_KMAX", "default_opts"]
 
 
 def default_opts() -> Opts:
@@ -211,3 +211,43 @@ class Problem:
 
     def __exit__(self, *exc):
         self.close()
+
+
+class EKProblem:
+    """NEXT row f1: extended-Krylov projection (§2.2, Alg. 1) for large n.  X0Br = X0 @ Br of
+    the seed solution, trEX0 = trace(E X0).  trace_batch(V, eps) -> approximate traces."""
+
+    def __init__(self, A0, Bl, Br, X0Br, E, trEX0: float, max_dim: int = 0):
+        A0 = _f64(A0)
+        n = A0.shape[0]
+        Bl = _f64(Bl).reshape(n, -1)
+        k = Bl.shape[1]
+        Br, X0Br, E = _f64(Br).reshape(n, k), _f64(X0Br).reshape(n, k), _f64(E, (n, n))
+        self._ek = C.c_void_p()
+        rc = lib.lyap_ek_setup(n, k, _dp(A0), _dp(Bl), _dp(Br), _dp(X0Br), _dp(E), float(trEX0), max_dim,
+                               C.byref(self._ek))
+        if rc != LYAP_OK:
+            raise LyapError(rc, lib.lyap_ek_last_error(None).decode())
+        self.n, self.k = n, k
+
+    def trace_batch(self, V, eps: float = 1e-8, max_steps: int = 200):
+        V = _f64(V).reshape(-1, self.k)
+        tau = np.empty(V.shape[0])
+        dim = C.c_int32()
+        err = C.c_double()
+        rc = lib.lyap_ek_trace_batch(self._ek, V.shape[0], V.ctypes.data, eps, max_steps, tau.ctypes.data,
+                                     C.byref(dim), C.byref(err))
+        if rc != LYAP_OK:
+            raise LyapError(rc, lib.lyap_ek_last_error(self._ek).decode())
+        return tau, int(dim.value), float(err.value)
+
+    def close(self):
+        if getattr(self, "_ek", None) and self._ek.value:
+            lib.lyap_ek_destroy(self._ek)
+            self._ek = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

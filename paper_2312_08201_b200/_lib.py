@@ -19,7 +19,7 @@ LYAP_KMAX = 8
 EXPORTED = ("lyap_default_opts", "lyap_setup", "lyap_trace_batch", "lyap_trace_batch_ex", "lyap_get_info",
             "lyap_get_stats", "lyap_reset_stats", "lyap_apply_C", "lyap_export_state", "lyap_destroy",
             "lyap_last_error", "lyap_solution", "lyap_setup_like", "lyap_set_recycle",
-            "lyap_build_recycle")
+            "lyap_build_recycle", "lyap_ek_setup", "lyap_ek_trace_batch", "lyap_ek_destroy", "lyap_ek_last_error")
 
 
 class Opts(C.Structure):
@@ -68,6 +68,14 @@ def _load():
     lib.lyap_export_state.restype = C.c_int
     lib.lyap_setup_like.argtypes = [P, C.c_int64, dp, dp, C.POINTER(Opts), C.POINTER(P)]
     lib.lyap_setup_like.restype = C.c_int
+    lib.lyap_ek_setup.argtypes = [C.c_int64, C.c_int64, dp, dp, dp, dp, dp, C.c_double, C.c_int32, C.POINTER(P)]
+    lib.lyap_ek_setup.restype = C.c_int
+    lib.lyap_ek_trace_batch.argtypes = [P, C.c_int64, P, C.c_double, C.c_int32, P, P, P]
+    lib.lyap_ek_trace_batch.restype = C.c_int
+    lib.lyap_ek_destroy.argtypes = [P]
+    lib.lyap_ek_destroy.restype = None
+    lib.lyap_ek_last_error.argtypes = [P]
+    lib.lyap_ek_last_error.restype = C.c_char_p
     lib.lyap_build_recycle.argtypes = [P, C.c_int32, P, C.c_int32]
     lib.lyap_build_recycle.restype = C.c_int
     lib.lyap_set_recycle.argtypes = [P, C.c_int32, C.c_int32, P, P]

@@ -1426,3 +1426,5 @@ int lyap_export_state(const lyap_ctx* cctx, double* lam, double* bhr, double* bt
 }
 
 }  // extern "C"
+
+#include "ek.inc"

@@ -372,3 +372,27 @@ def test_recycle_built_spaces_parity_and_savings(name, s):
     assert np.all(st == 0)
     assert rel_err(tau[idx], np.array(g["traces"])).max() <= RTOL
     assert t1 < t0, (t0, t1)
+
+
+# ----------------------------------------------------------------------------- NEXT row f1
+@pytest.mark.parametrize("name,nsub", [("c1", 256), ("c2", 40)])
+def test_extended_krylov_projection(name, nsub):
+    """EKProblem (PAPER.md §2.2, Alg. 1): an approximation controlled by the backward-error target;
+    against the oracle samples it converges as eps shrinks."""
+    from paper_2312_08201_b200 import EKProblem
+    W = workloads.make(name)
+    X0 = scipy.linalg.solve_continuous_lyapunov(W.A0, -W.Q)  # seed solution (independent LAPACK)
+    t0 = float(np.sum(W.E * X0))
+    g = _golden(name)
+    idx = np.array(g["indices"])[:nsub]
+    ref = np.array(g["traces"])[:nsub]
+    errs, info = [], []
+    for eps in (1e-6, 1e-10):
+        ek = EKProblem(W.A0, W.Bl, W.Br, X0 @ W.Br, W.E, t0, max_dim=800)
+        tau, dim, bwd = ek.trace_batch(W.V[idx], eps=eps)
+        errs.append(rel_err(tau, ref).max())
+        info.append((eps, dim, bwd, errs[-1]))
+        assert dim % (4 * W.k) == 0 and dim <= min(W.n, 800)
+        ek.close()
+    assert errs[1] <= max(1e-7, errs[0]), info
+    assert errs[1] <= 1e-6, info
