@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--scaling", default=os.environ.get("BENCH_SCALING", "weak"), choices=["weak", "strong"],
+                    help="weak: every rank solves a full-size grid of its own (axis 0 refined world-fold and "
+                         "interleaved; N=1 is the configuration itself); strong: the one grid is sharded")
     ap.add_argument("--max-dim", type=int, default=0)
     ap.add_argument("--recycle", type=int, default=int(os.environ.get("BENCH_RECYCLE", "0")),
                     help="recycle-space size s (0: off); spaces built from the 2^k grid corners before timing")
@@ -183,7 +186,7 @@ def run_reference(args, rank, world):
     cores, cnt = rates[0][1], rates[0][2]
     emit({"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / max(args.steps, 1),
-          "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+          "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
           "data": "synthetic (seeded workloads.make)",
           "config": config_dict(W, args, world, {"sample_per_step": cnt}),
           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
@@ -213,8 +216,14 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     W = workloads.make(args.config)
-    sweep = Sweep(W.nv, rank, world, dev)
-    idx = sweep.mine
+    sweep = Sweep(W.nv, rank, world, dev, scaling=args.scaling)
+    if args.scaling == "weak":
+        Vrank = workloads.rank_grid(W, rank, world)
+        idx = np.arange(len(Vrank))
+    else:
+        Vrank = W.V
+        idx = sweep.mine
+    nv_total = sweep.nv
     P = Problem(W.A0, W.Bl, W.Br, W.Q, W.E, profile=True, device=local, batch=args.batch, max_dim=args.max_dim)
     setup_ms = P.info["setup_ms"]
     recycle_ms = None
@@ -222,7 +231,7 @@ def main():
         t = time.perf_counter()
         P.build_recycle(V=W.V, s=args.recycle)
         recycle_ms = 1e3 * (time.perf_counter() - t)
-    Vd = torch.tensor(W.V[idx], device=dev)
+    Vd = torch.tensor(Vrank[idx], device=dev)
 
     def step():
         return sweep.run(lambda rows: P.trace_batch(Vd))
@@ -250,13 +259,13 @@ def main():
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     ms_max = float(tmax.item())
     st = P.stats
-    value = W.nv * args.steps / (ms_max * 1e-3)
+    value = nv_total * args.steps / (ms_max * 1e-3)
     argmin = int(am.item())
 
     # e2e: host buffers through the public API (H2D of V and D2H of traces inside the timed region)
     e2e = None
     if not args.no_e2e:
-        Vh = np.ascontiguousarray(W.V[idx])
+        Vh = np.ascontiguousarray(Vrank[idx])
         P.trace_batch(Vh)
         torch.cuda.synchronize()
         if world > 1:
@@ -267,7 +276,7 @@ def main():
         el = torch.tensor([time.perf_counter() - t], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(el, op=dist.ReduceOp.MAX)
-        e2e = {"value": W.nv * args.steps / float(el.item()), "unit": UNIT,
+        e2e = {"value": nv_total * args.steps / float(el.item()), "unit": UNIT,
                "h2d_bytes_per_step": int(Vh.nbytes), "d2h_bytes_per_step": int(len(idx) * (8 + 4 + 4 + 8))}
 
     avg_k1_ms = st["k1_ms"] / max(st["k1_launches"], 1)
@@ -315,11 +324,12 @@ def main():
     if rank == 0:
         emit({"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
               "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-              "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded workloads.make)",
+              "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded workloads.make)",
               "config": config_dict(W, args, world, {"batch": P.info["batch"], "max_dim": P.info["max_dim"],
+                                                     "nv_total": nv_total,
                                                      "setup_ms": setup_ms, "argmin_flat_index": argmin,
                                                      "recycle_s": args.recycle, "recycle_build_ms": recycle_ms,
-                                                     "applies_per_v": st["k1_vectors"] / (W.nv * args.steps / world)}),
+                                                     "applies_per_v": st["k1_vectors"] / (len(idx) * args.steps)}),
               "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
               "gpu_launches": st["kernel_launches"]})
     P.close()

@@ -28,10 +28,18 @@ class Sweep:
 
     solve(shard_rows) -> traces for those rows (a torch tensor on `device`)."""
 
-    def __init__(self, nv: int, rank: int, world: int, device, group=None, chunk: int = CHUNK):
+    def __init__(self, nv: int, rank: int, world: int, device, group=None, chunk: int = CHUNK,
+                 scaling: str = "strong"):
+        """strong: one grid of nv rows sharded over the ranks; weak: every rank owns nv rows of its
+        own (rows [rank*nv, (rank+1)*nv) of the global world*nv batch)."""
         import torch
-        self.nv, self.rank, self.world, self.device, self.group = nv, rank, world, device, group
-        shards = [shard_indices(nv, r, world, chunk) for r in range(world)]
+        self.rank, self.world, self.device, self.group = rank, world, device, group
+        if scaling == "weak":
+            shards = [np.arange(r * nv, (r + 1) * nv) for r in range(world)]
+            nv = nv * world
+        else:
+            shards = [shard_indices(nv, r, world, chunk) for r in range(world)]
+        self.nv = nv
         self.mine = shards[rank]
         self.nmax = max((len(s) for s in shards), default=0)
         pad = [np.pad(s, (0, self.nmax - len(s)), constant_values=-1) for s in shards]

@@ -77,3 +77,53 @@ def test_single_rank_sweep_no_collective():
     full, am = sw.run(lambda rows: torch.tensor(fake_tau(V[rows]), dtype=torch.float64))
     np.testing.assert_array_equal(full.numpy(), fake_tau(V))
     assert int(am) == int(np.argmin(fake_tau(V)))
+
+
+def test_rank_grids_weak_scaling():
+    """Weak scaling: world = 1 is the configuration's own grid; for world > 1 every rank gets a grid of
+    the same size and the union is the world-fold refined grid (no row shared)."""
+    import workloads
+    W = workloads.make("c2")
+    np.testing.assert_array_equal(workloads.rank_grid(W, 0, 1), W.V)
+    for world in (2, 4, 8):
+        parts = [workloads.rank_grid(W, r, world) for r in range(world)]
+        assert all(p.shape == W.V.shape for p in parts)
+        allv = np.concatenate(parts)
+        assert len(np.unique(allv, axis=0)) == world * W.nv
+        lo, hi = W.V.min(axis=0), W.V.max(axis=0)
+        assert np.all(allv >= lo * (1 - 1e-12)) and np.all(allv <= hi * (1 + 1e-12))
+
+
+def _worker_weak(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        nv = 37
+        sw = Sweep(nv, rank, world, torch.device("cpu"), scaling="weak")
+        V = np.linspace(0.1, 5.0, nv * world).reshape(-1, 1)
+        mine = V[rank * nv:(rank + 1) * nv]
+        assert np.array_equal(V[sw.mine], mine)  # weak: global rows of this rank
+        full, am = sw.run(lambda rows: torch.tensor(fake_tau(V[rows]), dtype=torch.float64))
+        out_q.put((rank, full.numpy().copy(), int(am)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_weak_sweep():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_weak, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    V = np.linspace(0.1, 5.0, 37 * world).reshape(-1, 1)
+    ref = fake_tau(V)
+    for _, full, am in res:
+        np.testing.assert_array_equal(full, ref)
+        assert am == int(np.argmin(ref))

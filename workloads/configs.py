@@ -30,7 +30,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import scipy.linalg
 
-__all__ = ["Workload", "make", "CONFIG_NAMES", "grid", "chain", "multi_agent", "random_stable"]
+__all__ = ["Workload", "make", "CONFIG_NAMES", "grid", "chain", "multi_agent", "random_stable", "rank_grid"]
 
 CONFIG_NAMES = ("c1", "c2", "c3", "c4", "c5")
 
@@ -191,26 +191,45 @@ def make(name: str, seed: int | None = None) -> Workload:
     rng = np.random.default_rng(s)
     if name == "c1":
         A0, Bl, Br, Q, E, meta = chain(50, 100.0, 0.02, [10, 35], modes_in_E=10)
-        V, shp = grid(0.1, 100.0, 16, 2, log=True), (16, 16)
+        gspec = (0.1, 100.0, 16, 2, True)
+        V, shp = grid(*gspec[:4], log=gspec[4]), (16, 16)
         meta["positions"] = [10, 35]
     elif name == "c2":
         pos = sorted(int(x) + 1 for x in rng.choice(400, 2, replace=False))
         A0, Bl, Br, Q, E, meta = chain(400, 500.0, 0.01, pos, modes_in_E=40)
-        V, shp = grid(0.01, 1000.0, 64, 2, log=True), (64, 64)
+        gspec = (0.01, 1000.0, 64, 2, True)
+        V, shp = grid(*gspec[:4], log=gspec[4]), (64, 64)
         meta["positions"] = pos
     elif name == "c3":
         A0, Bl, Br, Q, E, meta = multi_agent(200, 4, 0.03, 3, rng)
-        V, shp = grid(0.05, 5.0, 16, 3, log=False), (16, 16, 16)
+        gspec = (0.05, 5.0, 16, 3, False)
+        V, shp = grid(*gspec[:4], log=gspec[4]), (16, 16, 16)
     elif name == "c4":
         masses = rng.uniform(1.0, 3.0, 1000)
         pos = sorted(int(x) + 1 for x in rng.choice(1000, 3, replace=False))
         A0, Bl, Br, Q, E, meta = chain(1000, 1000.0, 0.02, pos, masses=masses, modes_in_E=50)
-        V, shp = grid(0.1, 500.0, 20, 3, log=True), (20, 20, 20)
+        gspec = (0.1, 500.0, 20, 3, True)
+        V, shp = grid(*gspec[:4], log=gspec[4]), (20, 20, 20)
         meta["positions"] = pos
     else:  # c5
         pos = sorted(int(x) + 1 for x in rng.choice(2000, 4, replace=False))
         A0, Bl, Br, Q, E, meta = chain(2000, 2000.0, 0.005, pos, modes_in_E=100)
-        V, shp = grid(0.1, 1000.0, 8, 4, log=True), (8, 8, 8, 8)
+        gspec = (0.1, 1000.0, 8, 4, True)
+        V, shp = grid(*gspec[:4], log=gspec[4]), (8, 8, 8, 8)
         meta["positions"] = pos
     meta["seed"] = s
+    meta["grid_spec"] = gspec  # (lo, hi, points per axis, k, log-spaced)
     return Workload(name, A0, Bl, Br, Q, E, V, shp, meta)
+
+
+def rank_grid(W: Workload, rank: int, world: int) -> np.ndarray:
+    """Weak-scaling grid of one rank: the configuration's grid with axis 0 refined world-fold and
+    interleaved (rank r takes refined points r, r + world, ...).  Same size and value distribution
+    as W.V on every rank; world = 1 returns W.V exactly."""
+    lo, hi, g, k, log = W.meta["grid_spec"]
+    if world == 1:
+        return W.V
+    fine = np.geomspace(lo, hi, g * world) if log else np.linspace(lo, hi, g * world)
+    axis0 = fine[rank::world]
+    base = np.geomspace(lo, hi, g) if log else np.linspace(lo, hi, g)
+    return np.array(list(itertools.product(axis0, *([base] * (k - 1)))), dtype=np.float64)
