@@ -66,7 +66,7 @@ struct Engine {
   double *part = nullptr;                         // b x (mmax+2) x nchunk
   double *part3 = nullptr;                        // b x nchunk x 3
   double *part2 = nullptr;                        // b x (mmax+2) x nchunk  (Gram-row partials)
-  double *Rc = nullptr, *Rr = nullptr;            // b x (mmax+1)^2 Cholesky factor of Q^T Q
+  double *Gq = nullptr;                           // b x (mmax+1)^2 Gram matrix Q^T Q of the basis
   double *cf = nullptr;                           // b x (mmax+1) projection coefficients
   double *Hraw = nullptr;                         // b x (mmax+1) x mmax unrotated Hessenberg (recycle build)
   int *phase = nullptr, *m = nullptr, *vidx = nullptr, *applies = nullptr, *restarts = nullptr;

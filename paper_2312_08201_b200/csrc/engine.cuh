@@ -40,7 +40,7 @@ struct EngArgs {
   int record;   // lyap_build_recycle: stop every slot after its first cycle (keep its Krylov data)
   double* Hraw; // unrotated Hessenberg columns (b x (mmax+1) x mmax), written when record != 0
   double *X, *Xin, *Qb, *Minv, *sigma, *mask, *eta, *H, *e, *y, *bnorm, *part, *part3;
-  double *part2, *Rc, *Rr, *cf;  // Gram-row partials, Gram matrix Q^T Q (Rc; Rr unused), coefficients
+  double *part2, *Gq, *cf;  // Gram-row partials, Gram matrix Q^T Q of the basis, projection coefficients
   int *phase, *m, *vidx, *applies, *restarts, *ctrl, *newv, *alist;
   int* qctr;      // shared by all slot groups: [0] next queue position, [1] finished v's
   double *cs, *sn;  // Givens rotations (b x mmax each)
@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(256) k_gram(EngArgs a) {
   const int ld = a.mmax + 1;
   const int m = a.m[slot];
   const double* eta = a.eta + (int64_t)slot * ld;
-  double* G = a.Rc + (int64_t)slot * ld * ld;  // G[i * ld + j], symmetric
+  double* G = a.Gq + (int64_t)slot * ld * ld;  // G[i * ld + j], symmetric
   const double* pd = a.part + (int64_t)slot * (a.mmax + 2) * a.nchunk;
   const double* pg = a.part2 + (int64_t)slot * (a.mmax + 2) * a.nchunk;
   for (int i = threadIdx.x; i <= m; i += blockDim.x) {

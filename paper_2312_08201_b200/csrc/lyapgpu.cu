@@ -115,7 +115,7 @@ inline int tile_n(const Seed& s) { return s.n <= SMALL_N ? S_BN : G_BN; }
 void free_engine(Engine& g, bool keep_order = true) {
   void* ps[] = {g.Bop, g.U, g.Xin, g.X, g.Qb, g.Minv, g.sigma, g.mask, g.eta, g.H, g.e, g.y,
                 g.bnorm, g.part, g.part3, g.phase, g.m, g.vidx, g.applies, g.restarts, g.ctrl,
-                g.part2, g.Rc, g.Rr, g.cf, g.Hraw};
+                g.part2, g.Gq, g.cf, g.Hraw};
   for (void* p : ps) dfree(p);
   if (g.h_ctrl) cudaFreeHost(g.h_ctrl);
   int* order = g.order;
@@ -183,8 +183,7 @@ void ensure_engine(lyap_ctx* ctx, int b, int mmax) {
   g.part = dalloc<double>(ctx, (size_t)b * (mmax + 2) * g.nchunk);
   g.part3 = dalloc<double>(ctx, (size_t)b * g.nchunk * 3);
   g.part2 = dalloc<double>(ctx, (size_t)b * (mmax + 2) * g.nchunk);
-  g.Rc = dalloc<double>(ctx, (size_t)b * (mmax + 1) * (mmax + 1));
-  g.Rr = dalloc<double>(ctx, 1);
+  g.Gq = dalloc<double>(ctx, (size_t)b * (mmax + 1) * (mmax + 1));
   g.cf = dalloc<double>(ctx, (size_t)b * (mmax + 1));
   g.Hraw = dalloc<double>(ctx, (size_t)b * (mmax + 1) * mmax);
   g.phase = dalloc<int>(ctx, b);
@@ -294,7 +293,6 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   a.TUreg = ctx->TUreg;
   a.regq = ctx->nreg > 0 ? dregq : nullptr;
   a.qctr = g.ctrl + 8 * G;
-  a.Rr = g.Rr;
 
   // slot group gi owns slots [s0, s0 + bg): every per-slot array is offset, so the kernels see a
   // self-contained engine of bg slots; only the v queue and the done counter are shared
@@ -325,7 +323,7 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
     x.part = g.part + s0 * (mmax + 2) * g.nchunk;
     x.part2 = g.part2 + s0 * (mmax + 2) * g.nchunk;
     x.part3 = g.part3 + s0 * g.nchunk * 3;
-    x.Rc = g.Rc + s0 * ld * ld;
+    x.Gq = g.Gq + s0 * ld * ld;
     x.cf = g.cf + s0 * ld;
     x.phase = g.phase + s0;
     x.m = g.m + s0;
