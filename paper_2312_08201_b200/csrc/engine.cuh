@@ -610,12 +610,30 @@ __global__ void __launch_bounds__(256) k_backsub(EngArgs a) {
   const int m1 = a.m[slot];
   const double* H = a.H + (int64_t)slot * ld * a.mmax;
   double* dinv = Rs + m1 * (m1 + 1) / 2;
-  for (int j = threadIdx.x >> 5; j < m1; j += blockDim.x >> 5) {
-    const int off = j * (j + 1) / 2;
-    for (int i = threadIdx.x & 31; i <= j; i += 32) {
-      const double h = H[(int64_t)j * ld + i];
-      Rs[off + i] = h;
-      if (i == j) dinv[j] = h != 0.0 ? 1.0 / h : 0.0;
+  // flat loop over the packed triangle, 8 independent loads in flight per thread (latency-bound
+  // otherwise: one dependent L2 round trip per element)
+  const int tot = m1 * (m1 + 1) / 2;
+  constexpr int UNR = 8;
+  for (int base = threadIdx.x; base < tot; base += blockDim.x * UNR) {
+    double v[UNR];
+    int jj[UNR], ii[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int idx = base + u * blockDim.x;
+      int j = (int)((sqrt(8.0 * idx + 1.0) - 1.0) * 0.5);
+      if ((j + 1) * (j + 2) / 2 <= idx) ++j;  // guard the float rounding of the inversion
+      if (j * (j + 1) / 2 > idx) --j;
+      jj[u] = j;
+      ii[u] = idx - j * (j + 1) / 2;
+      v[u] = idx < tot ? H[(int64_t)j * ld + ii[u]] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int idx = base + u * blockDim.x;
+      if (idx < tot) {
+        Rs[idx] = v[u];
+        if (ii[u] == jj[u]) dinv[jj[u]] = v[u] != 0.0 ? 1.0 / v[u] : 0.0;
+      }
     }
   }
   __syncthreads();
