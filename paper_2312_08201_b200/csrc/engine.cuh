@@ -17,7 +17,10 @@
 
 namespace lyap {
 
-constexpr int RED_CE = 1024;  // vector elements per reduction chunk
+#ifndef LYAP_RED_CE
+#define LYAP_RED_CE 1024
+#endif
+constexpr int RED_CE = LYAP_RED_CE;  // vector elements per reduction chunk (blocks of k_dots / k_upd)
 constexpr int CTRL_RMAX = 8;  // k_ctrl back substitution: m_max <= 32 * CTRL_RMAX = 256
 
 struct EngArgs {
