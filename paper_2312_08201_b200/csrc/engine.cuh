@@ -101,13 +101,15 @@ __global__ void k_assign(EngArgs a) {
       a.applies[tid] = 0;
       a.restarts[tid] = 0;
       a.newv[tid] = 1;
+      // cold start (g = 0): the first residual is the right-hand side itself -- START forms it
+      // without a T-apply; a warm start must verify its initial iterate through K1
+      a.phase[tid] = a.warm ? PH_VERIFY : PH_START;
       int r = a.regq ? a.regq[qpos] : -1;
       bool nomask = true;
       for (int t = 0; t < a.K; ++t) nomask = nomask && (a.V[(int64_t)idx * a.K + t] != 0.0);
       if (!nomask || a.s_rec <= 0) r = -1;  // masked rows: C(v) u != Delta u - T u there
       a.reg[tid] = r;
       a.su[tid] = r >= 0 ? a.sreg[r] : 0;
-      a.phase[tid] = PH_VERIFY;
     } else {
       a.phase[tid] = PH_IDLE;
     }
@@ -331,19 +333,26 @@ __global__ void __launch_bounds__(256) k_dots(EngArgs a) {
   const int ph = a.phase[slot];
   const int64_t e0 = (int64_t)chunk * RED_CE;
   const int64_t qs = (int64_t)(a.mmax + 1) * a.L;
-  if (ph == PH_VERIFY) {
-    const double* R = a.Qb + slot * qs;
+  if (ph == PH_VERIFY || ph == PH_START) {
+    double* R = a.Qb + slot * qs;
     const double* X = a.X + (int64_t)slot * a.L;
+    const bool start = ph == PH_START;  // g = 0: R = rhs, written here as q^_0
     double s0 = 0.0, s1 = 0.0, s2 = 0.0;
     for (int i = threadIdx.x; i < RED_CE; i += blockDim.x) {
       const int64_t e = e0 + i;
       if (e < a.L) {
-        const double r = R[e];
         const int t = (int)(e / a.npad);
         const double rh = a.mask[slot * a.K + t] * a.g0[e];
+        double r;
+        if (start) {
+          r = rh;
+          R[e] = rh;
+        } else {
+          r = R[e];
+          s2 += a.hf[e] * X[e];
+        }
         s0 += r * r;
         s1 += rh * rh;
-        s2 += a.hf[e] * X[e];
       }
     }
     s0 = block_sum(s0, red);
@@ -498,7 +507,7 @@ __global__ void __launch_bounds__(128) k_ctrl(EngArgs a) {
   double* cs = a.cs + (int64_t)slot * a.mmax;
   double* sn = a.sn + (int64_t)slot * a.mmax;
   const double* p3 = a.part3 + (int64_t)slot * a.nchunk * 3;
-  if (ph == PH_VERIFY) {
+  if (ph == PH_VERIFY || ph == PH_START) {
     if (lane != 0) return;
     double s0 = 0.0, s1 = 0.0, s2 = 0.0;
     for (int c = 0; c < a.nchunk; ++c) {
@@ -507,7 +516,7 @@ __global__ void __launch_bounds__(128) k_ctrl(EngArgs a) {
       s2 += p3[c * 3 + 2];
     }
     const double rho = sqrt(s0), bn = sqrt(s1), tr = a.t0 + 2.0 * s2;
-    const int ap = ++a.applies[slot];
+    const int ap = (ph == PH_VERIFY) ? ++a.applies[slot] : a.applies[slot];  // START needs no T-apply
     const bool bad = !isfinite(rho) || !isfinite(tr);
     const bool conv = rho <= a.tol * bn;
     if (bad || conv || a.restarts[slot] >= a.max_restarts) {

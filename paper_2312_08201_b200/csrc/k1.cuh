@@ -43,7 +43,7 @@ struct K1Args {
 __device__ __forceinline__ int k1_nact(const K1Args& a) { return a.nactive ? *a.nactive : a.nslot; }
 __device__ __forceinline__ int k1_slot(const K1Args& a, int pos) { return a.alist ? a.alist[pos] : pos; }
 
-enum : int { PH_FREE = 0, PH_IDLE = 1, PH_VERIFY = 2, PH_ITER = 3, PH_XUPD = 4 };
+enum : int { PH_FREE = 0, PH_IDLE = 1, PH_VERIFY = 2, PH_ITER = 3, PH_XUPD = 4, PH_START = 5 };
 
 // ------------------------------------------------------------------------------------------
 // K1a prologue: Bop[i][(slot*k + s)*k + t] = folded (B^r_is * X_ti)   (the Hadamard B operand)
