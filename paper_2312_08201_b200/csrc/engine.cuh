@@ -21,7 +21,7 @@ namespace lyap {
 #define LYAP_RED_CE 1024
 #endif
 constexpr int RED_CE = LYAP_RED_CE;  // vector elements per reduction chunk (blocks of k_dots / k_upd)
-constexpr int CTRL_RMAX = 8;  // k_ctrl back substitution: m_max <= 32 * CTRL_RMAX = 256
+constexpr int CTRL_RMAX = 16;  // back substitution keeps y in registers: m_max <= 32 * CTRL_RMAX = 512
 
 struct EngArgs {
   int b, mmax, K, nv;
@@ -614,13 +614,60 @@ __global__ void __launch_bounds__(256) k_gout(EngArgs a) {
 // One block per slot that just finished a cycle (phase XUPD): the rotated Hessenberg (upper
 // triangular R, m1 x m1, packed by columns) is staged in shared memory with one coalesced load,
 // then one warp runs the back substitution with y distributed over the lanes (shuffle broadcast).
-__global__ void __launch_bounds__(256) k_backsub(EngArgs a) {
+__global__ void __launch_bounds__(256) k_backsub(EngArgs a, int smem_doubles) {
   extern __shared__ double Rs[];  // m1 (m1 + 1) / 2, then m1 reciprocal diagonal entries
   const int slot = blockIdx.x;
   if (a.phase[slot] != PH_XUPD) return;
   const int ld = a.mmax + 1;
   const int m1 = a.m[slot];
   const double* H = a.H + (int64_t)slot * ld * a.mmax;
+  if (m1 * (m1 + 1) / 2 + m1 > smem_doubles) {  // long cycle: R from global, one column ahead
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    const double* e = a.e + (int64_t)slot * ld;
+    const double* eta = a.eta + (int64_t)slot * ld;
+    double yv[CTRL_RMAX], hv[CTRL_RMAX], hn[CTRL_RMAX];
+#pragma unroll
+    for (int r = 0; r < CTRL_RMAX; ++r) {
+      const int i = lane + 32 * r;
+      yv[r] = (i < m1) ? e[i] : 0.0;
+      hv[r] = (i < m1) ? H[(int64_t)(m1 - 1) * ld + i] : 0.0;
+    }
+    for (int j = m1 - 1; j >= 0; --j) {
+      if (j > 0) {
+#pragma unroll
+        for (int r = 0; r < CTRL_RMAX; ++r) {
+          const int i = lane + 32 * r;
+          hn[r] = (i < j) ? H[(int64_t)(j - 1) * ld + i] : 0.0;
+        }
+      }
+      const int owner = j & 31, rj = j >> 5;
+      double yj = 0.0, dj = 0.0;
+#pragma unroll
+      for (int r = 0; r < CTRL_RMAX; ++r)
+        if (r == rj) {
+          yj = yv[r];
+          dj = hv[r];
+        }
+      yj = __shfl_sync(0xffffffffu, yj, owner);
+      dj = __shfl_sync(0xffffffffu, dj, owner);
+      yj = dj != 0.0 ? yj / dj : 0.0;
+#pragma unroll
+      for (int r = 0; r < CTRL_RMAX; ++r) {
+        const int i = lane + 32 * r;
+        if (i == j) yv[r] = yj;
+        else if (i < j) yv[r] -= hv[r] * yj;
+        hv[r] = hn[r];
+      }
+    }
+    double* y = a.y + (int64_t)slot * a.mmax;
+#pragma unroll
+    for (int r = 0; r < CTRL_RMAX; ++r) {
+      const int i = lane + 32 * r;
+      if (i < m1) y[i] = i < a.su[slot] ? yv[r] : yv[r] / eta[i];
+    }
+    return;
+  }
   double* dinv = Rs + m1 * (m1 + 1) / 2;
   // flat loop over the packed triangle, 8 independent loads in flight per thread (latency-bound
   // otherwise: one dependent L2 round trip per element)

@@ -151,8 +151,10 @@ int auto_batch(const lyap_ctx* ctx, int64_t nv) {
 }
 
 int auto_mmax(const lyap_ctx* ctx) {
-  if (ctx->opts.max_dim > 0) return std::min(ctx->opts.max_dim, 224);  // k_backsub stages R (<= 201 KB smem)
-  return 160;
+  if (ctx->opts.max_dim > 0) return std::min(ctx->opts.max_dim, 32 * CTRL_RMAX);
+  // long cycles where the T-apply dominates (restarts cost iterations: c5 224 vs 160 -> +20 % v/s),
+  // shorter where the HBM-bound orthogonalisation does
+  return ctx->seed.n * ctx->seed.k >= 12000 ? 384 : 160;
 }
 
 void ensure_engine(lyap_ctx* ctx, int b, int mmax) {
@@ -356,7 +358,8 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   const size_t upd_smem = sizeof(double) * (mmax + 1);
   const size_t ctrl_smem = sizeof(double) * 16 * (size_t)(mmax + 2);
   const size_t gram_smem = sizeof(double) * (size_t)(mmax + 1);
-  const size_t bs_smem = sizeof(double) * ((size_t)mmax * (mmax + 1) / 2 + mmax);
+  const size_t bs_smem = std::min<size_t>(sizeof(double) * ((size_t)mmax * (mmax + 1) / 2 + mmax), 220 * 1024);
+  const int bs_doubles = (int)(bs_smem / sizeof(double));
   if (bs_smem > 48 * 1024) CK(cudaFuncSetAttribute(k_backsub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bs_smem));
   if (gram_smem > 48 * 1024) CK(cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_smem));
   if (ctrl_smem > 48 * 1024) CK(cudaFuncSetAttribute(k_ctrl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctrl_smem));
@@ -404,7 +407,7 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
       k_gout<<<dim3((unsigned)std::min<int64_t>((g.L + 255) / 256, 64), (unsigned)bg), 256, 0, sg>>>(x);
       LAUNCHED();
     }
-    k_backsub<<<bg, 256, bs_smem, sg>>>(x);
+    k_backsub<<<bg, 256, bs_smem, sg>>>(x, bs_doubles);
     LAUNCHED();
     k_xcomb<<<gxc, 256, 0, sg>>>(x);
     LAUNCHED();
