@@ -239,6 +239,8 @@ def main():
     for _ in range(args.warmup):
         full, am = step()
     torch.cuda.synchronize()
+    if recycle_ms is None and P.stats["recycle_build_ms"] > 0:  # automatic spaces, built during warm-up
+        recycle_ms = P.stats["recycle_build_ms"]
     P.reset_stats()
     if world > 1:
         dist.barrier()
@@ -328,7 +330,8 @@ def main():
               "config": config_dict(W, args, world, {"batch": P.info["batch"], "max_dim": P.info["max_dim"],
                                                      "nv_total": nv_total,
                                                      "setup_ms": setup_ms, "argmin_flat_index": argmin,
-                                                     "recycle_s": args.recycle, "recycle_build_ms": recycle_ms,
+                                                     "recycle_s": args.recycle if args.recycle > 0 else ("auto" if recycle_ms else 0),
+                                                     "recycle_build_ms": recycle_ms,
                                                      "applies_per_v": st["k1_vectors"] / (len(idx) * args.steps)}),
               "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
               "gpu_launches": st["kernel_launches"]})

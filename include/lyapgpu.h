@@ -66,6 +66,11 @@ typedef struct {
                           sum_t |v_t| ||B~l_t|| ||B^r_t|| (largest perturbation first, so the slow
                           systems do not form a tail); 0: in row order of V.  Results are returned
                           in row order either way. */
+  int32_t recycle;     /* recycle-space size s: -1 (default) auto = 32 when n k >= 12000 (where the
+                          T-apply dominates; c5 443 -> 528 v/s), else off; 0 off; > 0 that size.
+                          With s > 0, lyap_trace_batch builds the spaces itself (lyap_build_recycle
+                          on the 2^k corners of the batch's bounding box, all v > 0) the first time
+                          and whenever the box changes; the build time is in lyap_stats. */
 } lyap_opts;
 
 typedef struct {
@@ -88,6 +93,7 @@ typedef struct {
   int64_t iterations;      /* engine iterations (one batched T-apply each) */
   int64_t kernel_launches; /* all kernels this library launched */
   double batch_ms;         /* device time of the last lyap_trace_batch */
+  double recycle_build_ms; /* time spent building recycle spaces (automatic or lyap_build_recycle) */
 } lyap_stats;
 
 /* Fills *opts with the defaults above. */

@@ -41,7 +41,7 @@ class Problem:
 
     def __init__(self, A0, Bl, Br, Q, E, *, tol: float = 1e-12, max_dim: int = 0, max_restarts: int = 30,
                  batch: int = 0, warm_start: bool = False, max_cond_S: float = 1e8, device: int = -1,
-                 profile: bool = False, schedule: bool = True):
+                 profile: bool = False, schedule: bool = True, recycle: int = -1):
         A0 = _f64(A0)
         n = A0.shape[0]
         Bl = _f64(Bl)
@@ -55,6 +55,7 @@ class Problem:
         o.tol, o.max_dim, o.max_restarts, o.batch = tol, max_dim, max_restarts, batch
         o.warm_start, o.max_cond_S, o.device, o.profile = int(warm_start), max_cond_S, device, int(profile)
         o.schedule = int(schedule)
+        o.recycle = int(recycle)
         self._ctx = C.c_void_p()
         rc = lib.lyap_setup(n, k, _dp(A0), _dp(Bl), _dp(Br), _dp(Q), _dp(E), C.byref(o), C.byref(self._ctx))
         if rc != LYAP_OK:

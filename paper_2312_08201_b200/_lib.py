@@ -25,7 +25,7 @@ EXPORTED = ("lyap_default_opts", "lyap_setup", "lyap_trace_batch", "lyap_trace_b
 class Opts(C.Structure):
     _fields_ = [("tol", C.c_double), ("max_dim", C.c_int32), ("max_restarts", C.c_int32),
                 ("batch", C.c_int32), ("warm_start", C.c_int32), ("max_cond_S", C.c_double),
-                ("device", C.c_int32), ("profile", C.c_int32), ("schedule", C.c_int32)]
+                ("device", C.c_int32), ("profile", C.c_int32), ("schedule", C.c_int32), ("recycle", C.c_int32)]
 
 
 class Info(C.Structure):
@@ -38,7 +38,7 @@ class Info(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("k1_launches", C.c_int64), ("k1_vectors", C.c_int64), ("k1_ms", C.c_double),
                 ("k1_flops", C.c_double), ("iterations", C.c_int64), ("kernel_launches", C.c_int64),
-                ("batch_ms", C.c_double)]
+                ("batch_ms", C.c_double), ("recycle_build_ms", C.c_double)]
 
 
 def _load():

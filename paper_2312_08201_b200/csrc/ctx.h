@@ -6,6 +6,7 @@
 
 #include <memory>
 #include <string>
+#include <vector>
 
 #include "../../include/lyapgpu.h"
 
@@ -97,6 +98,8 @@ struct lyap_ctx {
   double *Ureg = nullptr, *TUreg = nullptr;
   int* sreg = nullptr;  // device: vectors per regime
   std::string reg_seeds;  // nreg x k doubles (log |v| of each regime's seed), host copy
+  std::vector<double> auto_box;  // bounding box (lo, hi per parameter) the automatic spaces were built for
+  bool recycle_manual = false;   // spaces given by lyap_set_recycle / lyap_build_recycle: no automatic rebuild
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evfork = nullptr, evjoin = nullptr;
   cudaStream_t stream2 = nullptr;  // second slot group
 };

@@ -564,6 +564,7 @@ void lyap_default_opts(lyap_opts* o) {
   o->device = -1;
   o->profile = 0;
   o->schedule = 1;
+  o->recycle = -1;
 }
 
 const char* lyap_last_error(const lyap_ctx* c) { return c ? c->err.c_str() : g_last_error.c_str(); }
@@ -986,6 +987,39 @@ int lyap_trace_batch_ex(lyap_ctx* ctx, int64_t nv, const double* V, double* trac
     }
     // schedule: expensive (large-perturbation) v first, so slow systems do not form a tail
     const int* dorder = nullptr;
+    const int s_auto = ctx->opts.recycle < 0 ? (ctx->seed.n * ctx->seed.k >= 12000 ? 32 : 0) : ctx->opts.recycle;
+    if (ctx->opts.schedule || s_auto > 0) {
+      std::vector<double> hV((size_t)nv * k);
+      if (own) {
+        std::memcpy(hV.data(), V, hV.size() * 8);
+      } else {
+        CK(cudaMemcpyAsync(hV.data(), V, hV.size() * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+      }
+      if (s_auto > 0) {  // automatic recycle spaces from the corners of the batch's bounding box
+        std::vector<double> box(2 * k);
+        bool positive = true;
+        for (int64_t t = 0; t < k; ++t) {
+          double lo = 1e300, hi = -1e300;
+          for (int64_t i = 0; i < nv; ++i) {
+            lo = std::min(lo, hV[i * k + t]);
+            hi = std::max(hi, hV[i * k + t]);
+          }
+          box[2 * t] = lo;
+          box[2 * t + 1] = hi;
+          positive = positive && lo > 0.0;
+        }
+        if (positive && !ctx->recycle_manual && box != ctx->auto_box) {
+          std::vector<double> seeds;
+          for (int64_t c = 0; c < (int64_t(1) << k); ++c)
+            for (int64_t t = 0; t < k; ++t) seeds.push_back(box[2 * t + ((c >> (k - 1 - t)) & 1)]);
+          const int brc = lyap_build_recycle(ctx, (int32_t)(seeds.size() / k), seeds.data(), s_auto);
+          if (brc != LYAP_OK) throw Fail{brc};
+          ctx->recycle_manual = false;  // automatic: rebuilt when the box changes
+          ctx->auto_box = box;
+        }
+      }
+    }
     if (ctx->opts.schedule) {
       std::vector<double> hV((size_t)nv * k);
       if (own) {
@@ -1141,6 +1175,7 @@ int lyap_solution(lyap_ctx* ctx, int64_t nv, const double* V, double* X, double*
 }
 
 int lyap_set_recycle(lyap_ctx* ctx, int32_t nreg, int32_t s, const double* U, const double* seeds) {
+  if (ctx) ctx->recycle_manual = nreg > 0;  // user-managed spaces: no automatic rebuild
   if (!ctx || nreg < 0 || (nreg > 0 && (s < 1 || !U || !seeds))) {
     set_err(ctx, "lyap_set_recycle: invalid arguments");
     return LYAP_EINVAL;
@@ -1183,11 +1218,31 @@ int lyap_set_recycle(lyap_ctx* ctx, int32_t nreg, int32_t s, const double* U, co
   return LYAP_OK;
 }
 
+static int build_recycle_impl(lyap_ctx* ctx, int32_t nseeds, const double* seeds, int32_t s);
+
 int lyap_build_recycle(lyap_ctx* ctx, int32_t nseeds, const double* seeds, int32_t s) {
   if (!ctx || nseeds < 1 || !seeds || s < 1) {
     set_err(ctx, "lyap_build_recycle: invalid arguments");
     return LYAP_EINVAL;
   }
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, ctx->stream);
+  const int rc = build_recycle_impl(ctx, nseeds, seeds, s);
+  ctx->recycle_manual = rc == LYAP_OK;
+  cudaEventRecord(e1, ctx->stream);
+  cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  ctx->stats.recycle_build_ms += ms;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (rc != LYAP_OK) ctx->auto_box.clear();
+  return rc;
+}
+
+static int build_recycle_impl(lyap_ctx* ctx, int32_t nseeds, const double* seeds, int32_t s) {
   const Seed& sd = ctx->seed;
   const int64_t k = sd.k, L = sd.k * sd.npad;
   for (int64_t i = 0; i < (int64_t)nseeds * k; ++i)
