@@ -264,8 +264,8 @@ __global__ void __launch_bounds__(128) k_prec(EngArgs a) {
   }
 }
 
-// lyap_build_recycle helpers: Z[:, j] = P(v)^{-1} q^_j / eta_j (the search directions of the
-// recorded cycle), and TU = Delta(v) U - C(v) U.
+// lyap_build_recycle helpers: Z[:, j] = P(v)^{-1} q^_j / eta_j, or u_j for j < su (the search
+// directions of the recorded cycle), and TU = Delta(v) U - C(v) U.
 template <int K>
 __global__ void __launch_bounds__(128) k_rec_z(EngArgs a, int slot, int m1, double* __restrict__ Z) {
   const int j = blockIdx.y;
@@ -274,6 +274,14 @@ __global__ void __launch_bounds__(128) k_rec_z(EngArgs a, int slot, int m1, doub
   if (rep >= a.nrep) return;
   const int64_t c = rep_coord(rep, a.npairs);
   const bool pair = rep < a.npairs;
+  if (j < a.su[slot]) {  // FGMRES cycle with recycling: the search direction was u_j itself
+    const double* u = a.Ureg + ((int64_t)a.reg[slot] * a.s_rec + j) * a.L;
+    for (int t = 0; t < K; ++t) {
+      Z[(int64_t)j * a.L + t * a.npad + c] = u[t * a.npad + c];
+      if (pair) Z[(int64_t)j * a.L + t * a.npad + c + 1] = u[t * a.npad + c + 1];
+    }
+    return;
+  }
   const double sc = 1.0 / a.eta[(int64_t)slot * (a.mmax + 1) + j];
   const double* q = a.Qb + ((int64_t)slot * (a.mmax + 1) + j) * a.L;
   cplx r[K], z[K];
@@ -582,7 +590,9 @@ __global__ void __launch_bounds__(128) k_ctrl(EngArgs a) {
     done = (est <= a.tol_inner * a.bnorm[slot]) || (m + 1 >= a.mmax) || breakdown || !isfinite(est);
     // a recycled direction dependent on the current space is not a "lucky" breakdown: finish the
     // cycle and run this v's restarts as plain GMRES
-    if (breakdown && m < a.su[slot]) a.su[slot] = 0;
+    // (su itself must stay until this cycle's update: its first su search directions are u_i;
+    // counting the cycle twice makes the safety net below drop the space at the next restart)
+    if (breakdown && m < a.su[slot]) a.restarts[slot] = max(a.restarts[slot], 1);
     a.m[slot] = m + 1;
   }
   __syncwarp();

@@ -289,7 +289,7 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   a.out_resid = dres;
   a.gout = gout;
   a.record = record;
-  a.s_rec = (ctx->nreg > 0 && !record) ? ctx->s_rec : 0;
+  a.s_rec = ctx->nreg > 0 ? ctx->s_rec : 0;
   a.Ureg = ctx->Ureg;
   a.sreg = ctx->sreg;
   a.TUreg = ctx->TUreg;
@@ -1242,6 +1242,14 @@ int lyap_build_recycle(lyap_ctx* ctx, int32_t nseeds, const double* seeds, int32
   return rc;
 }
 
+// 1 = select from plain GMRES cycles; 2 = plus one refinement pass.  The environment
+// variable LYAP_RECYCLE_ROUNDS (1..4) overrides it, for measurements.
+static int recycle_rounds() {
+  const char* e = std::getenv("LYAP_RECYCLE_ROUNDS");
+  const int r = e ? std::atoi(e) : 2;
+  return r < 1 ? 1 : (r > 4 ? 4 : r);
+}
+
 static int build_recycle_impl(lyap_ctx* ctx, int32_t nseeds, const double* seeds, int32_t s) {
   const Seed& sd = ctx->seed;
   const int64_t k = sd.k, L = sd.k * sd.npad;
@@ -1258,154 +1266,207 @@ static int build_recycle_impl(lyap_ctx* ctx, int32_t nseeds, const double* seeds
   double *dV = nullptr, *dtr = nullptr, *Z = nullptr, *Qn = nullptr, *Am = nullptr, *Bm = nullptr, *Wv = nullptr,
          *work = nullptr, *HP = nullptr, *CU = nullptr, *sig = nullptr, *Unew = nullptr, *TUnew = nullptr;
   int32_t* dst = nullptr;
-  int* dinfo = nullptr;
+  int *dinfo = nullptr, *dreg = nullptr;
   int rc = LYAP_OK;
   try {
     CK(cudaSetDevice(ctx->device));
     cudaStream_t st = ctx->stream;
-    // 1. one recorded GMRES cycle per seed (recycling off while recording)
     dfree(ctx->Ureg);
     dfree(ctx->TUreg);
+    dfree(ctx->sreg);
     ctx->Ureg = ctx->TUreg = nullptr;
+    ctx->sreg = nullptr;
     ctx->nreg = ctx->s_rec = 0;
     dV = dalloc<double>(ctx, (size_t)nseeds * k, false);
     dtr = dalloc<double>(ctx, nseeds, false);
     dst = dalloc<int32_t>(ctx, nseeds, false);
-    CK(cudaMemcpyAsync(dV, seeds, (size_t)nseeds * k * 8, cudaMemcpyHostToDevice, st));
-    rc = run_batch(ctx, nseeds, dV, nullptr, dtr, dst, nullptr, nullptr, st, nullptr, nullptr, 1);
-    if (rc != LYAP_OK) throw Fail{rc};
-    const Engine& g = ctx->eng;
-    std::vector<int> hph(g.b), hm(g.b), hv(g.b);
-    CK(cudaMemcpy(hph.data(), g.phase, g.b * sizeof(int), cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(hm.data(), g.m, g.b * sizeof(int), cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(hv.data(), g.vidx, g.b * sizeof(int), cudaMemcpyDeviceToHost));
-    std::vector<int> slot_of(nseeds, -1);
-    int s_eff = 1;  // stride: the largest regime size
-    for (int sl = 0; sl < g.b; ++sl)
-      if (hph[sl] == PH_IDLE && hm[sl] >= 1 && hv[sl] >= 0 && hv[sl] < nseeds && slot_of[hv[sl]] < 0) {
-        slot_of[hv[sl]] = sl;
-        s_eff = std::max(s_eff, std::min(s, hm[sl]));
-      }
-    std::vector<int> used;
-    for (int r = 0; r < nseeds; ++r)
-      if (slot_of[r] >= 0) used.push_back(r);
-    if (used.empty()) {
-      set_err(ctx, "lyap_build_recycle: no seed produced a Krylov cycle (all converged immediately)");
-      throw Fail{LYAP_EINVAL};
-    }
-    const int nreg = (int)used.size();
+    dreg = dalloc<int>(ctx, nseeds, false);
     const int ld = mmax + 1;
     Z = dalloc<double>(ctx, (size_t)mmax * L);
     Qn = dalloc<double>(ctx, (size_t)(mmax + 1) * L, false);
     Am = dalloc<double>(ctx, (size_t)mmax * mmax, false);
     Bm = dalloc<double>(ctx, (size_t)mmax * mmax, false);
     Wv = dalloc<double>(ctx, mmax, false);
-    HP = dalloc<double>(ctx, (size_t)(mmax + 1) * s_eff, false);
-    CU = dalloc<double>(ctx, (size_t)s_eff * L, false);
+    HP = dalloc<double>(ctx, (size_t)(mmax + 1) * s, false);
+    CU = dalloc<double>(ctx, (size_t)s * L, false);
     sig = dalloc<double>(ctx, k, false);
     dinfo = dalloc<int>(ctx, 1);
-    Unew = dalloc<double>(ctx, (size_t)nreg * s_eff * L);
-    TUnew = dalloc<double>(ctx, (size_t)nreg * s_eff * L);
-    std::vector<double> seeds_used;
+    {
+      std::vector<int> ident(nseeds);
+      for (int i = 0; i < nseeds; ++i) ident[i] = i;
+      CK(cudaMemcpy(dreg, ident.data(), nseeds * sizeof(int), cudaMemcpyHostToDevice));
+    }
     const double one = 1.0, zero = 0.0;
-    // engine args for the helper kernels: slot-indexed arrays of the whole engine
-    EngArgs ea{};
-    ea.mmax = mmax;
-    ea.L = L;
-    ea.npad = sd.npad;
-    ea.nrep = sd.nrep;
-    ea.npairs = sd.npairs;
-    ea.Qb = g.Qb;
-    ea.eta = g.eta;
-    ea.Minv = g.Minv;
-    std::vector<int> sizes(nreg);
-    for (int ri = 0; ri < nreg; ++ri) {
-      const int r = used[ri], sl = slot_of[r], m1 = hm[sl];
-      const int sr = std::min(s, m1);  // this regime's space size (cheap seeds record short cycles)
-      sizes[ri] = sr;
-      // Z = P^{-1} q_j (search directions) and normalised Q (j <= m1)
-      const dim3 gz((unsigned)((sd.nrep + 127) / 128), (unsigned)m1);
-      CK(cudaMemsetAsync(Z, 0, (size_t)m1 * L * 8, st));
-      K_DISPATCH(k, (k_rec_z<KK><<<gz, 128, 0, st>>>(ea, sl, m1, Z)));
-      LAUNCHED();
-      std::vector<double> heta(m1 + 1);
-      CK(cudaMemcpy(heta.data(), g.eta + (int64_t)sl * ld, (m1 + 1) * 8, cudaMemcpyDeviceToHost));
-      for (int j = 0; j <= m1; ++j) {
-        const double inv = 1.0 / heta[j];
-        CKB(cublasDcopy(ctx->cublas, (int)L, g.Qb + ((int64_t)sl * ld + j) * L, 1, Qn + (int64_t)j * L, 1));
-        CKB(cublasDscal(ctx->cublas, (int)L, &inv, Qn + (int64_t)j * L, 1));
+    std::vector<int> used;        // seeds that own a regime (round 1 decides)
+    std::vector<int> sizes;       // per-regime space size
+    std::vector<double> run_v;    // the parameter rows recorded this round
+    const int rounds = recycle_rounds();
+    for (int round = 0; round < rounds; ++round) {
+      // round 0: one plain GMRES cycle per seed (no spaces yet).  round >= 1: every regime's seed
+      // again, as an FGMRES cycle whose first search directions are the current space; the new space
+      // is selected from span([U, Z]) -- a GCRO-DR-style refinement
+      const int nrun = round == 0 ? nseeds : (int)used.size();
+      if (round == 0) run_v.assign(seeds, seeds + (int64_t)nseeds * k);
+      else {
+        run_v.clear();
+        for (int r : used) run_v.insert(run_v.end(), seeds + (int64_t)r * k, seeds + (int64_t)(r + 1) * k);
       }
-      const double* Hb = g.Hraw + (int64_t)sl * ld * mmax;  // column-major (m1+1) x m1, ld = mmax + 1
-      // A = Hbar^T Hbar, B = Z^T Z (+ tiny ridge), generalised symmetric eigenproblem A p = theta B p
-      CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_T, CUBLAS_OP_N, m1, m1, m1 + 1, &one, Hb, ld, Hb, ld, &zero, Am, m1));
-      CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_T, CUBLAS_OP_N, m1, m1, (int)L, &one, Z, (int)L, Z, (int)L, &zero, Bm, m1));
-      {
-        std::vector<double> hb((size_t)m1 * m1);
-        CK(cudaMemcpy(hb.data(), Bm, hb.size() * 8, cudaMemcpyDeviceToHost));
-        double tr = 0.0;
-        for (int j = 0; j < m1; ++j) tr += hb[(size_t)j * m1 + j];
-        const double ridge = 1e-10 * tr / m1;
-        for (int j = 0; j < m1; ++j) hb[(size_t)j * m1 + j] += ridge;
-        CK(cudaMemcpy(Bm, hb.data(), hb.size() * 8, cudaMemcpyHostToDevice));
-      }
-      int lwork = 0;
-      CKS(cusolverDnDsygvd_bufferSize(ctx->cusolver, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
-                                      CUBLAS_FILL_MODE_UPPER, m1, Am, m1, Bm, m1, Wv, &lwork));
-      dfree(work);
-      work = dalloc<double>(ctx, std::max(lwork, 1), false);
-      CKS(cusolverDnDsygvd(ctx->cusolver, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, m1,
-                           Am, m1, Bm, m1, Wv, work, lwork, dinfo));
-      int hinfo = 0;
-      CK(cudaMemcpy(&hinfo, dinfo, sizeof(int), cudaMemcpyDeviceToHost));
-      if (hinfo != 0) {
-        // Z^T Z numerically singular: select in the Euclidean metric of the coefficients instead
-        // (smallest right singular vectors of Hbar; measured nearly as effective)
-        CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_T, CUBLAS_OP_N, m1, m1, m1 + 1, &one, Hb, ld, Hb, ld, &zero, Am, m1));
-        int lw2 = 0;
-        CKS(cusolverDnDsyevd_bufferSize(ctx->cusolver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, m1, Am, m1,
-                                        Wv, &lw2));
-        dfree(work);
-        work = dalloc<double>(ctx, std::max(lw2, 1), false);
-        CKS(cusolverDnDsyevd(ctx->cusolver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, m1, Am, m1, Wv, work,
-                             lw2, dinfo));
-        CK(cudaMemcpy(&hinfo, dinfo, sizeof(int), cudaMemcpyDeviceToHost));
-        if (hinfo != 0) {
-          set_err(ctx, "lyap_build_recycle: syevd info = %d for seed %d", hinfo, r);
-          throw Fail{LYAP_ECUDA};
+      CK(cudaMemcpyAsync(dV, run_v.data(), (size_t)nrun * k * 8, cudaMemcpyHostToDevice, st));
+      rc = run_batch(ctx, nrun, dV, nullptr, dtr, dst, nullptr, nullptr, st, nullptr, round ? dreg : nullptr, 1);
+      if (rc != LYAP_OK) throw Fail{rc};
+      const Engine& g = ctx->eng;
+      std::vector<int> hph(g.b), hm(g.b), hv(g.b);
+      CK(cudaMemcpy(hph.data(), g.phase, g.b * sizeof(int), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(hm.data(), g.m, g.b * sizeof(int), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(hv.data(), g.vidx, g.b * sizeof(int), cudaMemcpyDeviceToHost));
+      std::vector<int> slot_of(nrun, -1);
+      for (int sl = 0; sl < g.b; ++sl)
+        if (hph[sl] == PH_IDLE && hm[sl] >= 1 && hv[sl] >= 0 && hv[sl] < nrun && slot_of[hv[sl]] < 0)
+          slot_of[hv[sl]] = sl;
+      if (round == 0) {
+        for (int r = 0; r < nseeds; ++r)
+          if (slot_of[r] >= 0) used.push_back(r);
+        if (used.empty()) {
+          set_err(ctx, "lyap_build_recycle: no seed produced a Krylov cycle (all converged immediately)");
+          throw Fail{LYAP_EINVAL};
         }
       }
-      // P = eigenvectors of the s_eff smallest eigenvalues (ascending: first columns of Am)
-      double* Ur = Unew + (int64_t)ri * s_eff * L;
-      double* TUr = TUnew + (int64_t)ri * s_eff * L;
-      CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)L, sr, m1, &one, Z, (int)L, Am, m1, &zero, Ur,
-                      (int)L));
-      CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, m1 + 1, sr, m1, &one, Hb, ld, Am, m1, &zero, HP,
-                      m1 + 1));
-      CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)L, sr, m1 + 1, &one, Qn, (int)L, HP, m1 + 1,
-                      &zero, CU, (int)L));
-      std::vector<double> hs(k);
-      for (int64_t t = 0; t < k; ++t) hs[t] = 1.0 / seeds[(int64_t)r * k + t];
-      CK(cudaMemcpy(sig, hs.data(), k * 8, cudaMemcpyHostToDevice));
-      k_rec_tu<<<(unsigned)std::min<int64_t>(((int64_t)sr * L + 255) / 256, 65535), 256, 0, st>>>(
-          Ur, CU, sig, L, sd.npad, sr, TUr);
-      LAUNCHED();
-      for (int64_t t = 0; t < k; ++t) seeds_used.push_back(std::log(std::fabs(seeds[(int64_t)r * k + t])));
+      const int nreg = (int)used.size();
+      // a regime is re-selected when its cycle is at least as long as its current space (a seed the
+      // space already solves within fewer steps keeps the space it has)
+      std::vector<int> take(nreg), nsz(nreg);
+      int stride = 1;
+      for (int ri = 0; ri < nreg; ++ri) {
+        const int sl = slot_of[round == 0 ? used[ri] : ri];
+        const int cur = round == 0 ? 0 : sizes[ri];
+        take[ri] = sl >= 0 && std::min(s, hm[sl]) >= std::max(cur, 1);
+        nsz[ri] = take[ri] ? std::min(s, hm[sl]) : cur;
+        stride = std::max(stride, nsz[ri]);
+      }
+      Unew = dalloc<double>(ctx, (size_t)nreg * stride * L);
+      TUnew = dalloc<double>(ctx, (size_t)nreg * stride * L);
+      // engine args for the helper kernels: slot-indexed arrays of the whole engine
+      EngArgs ea{};
+      ea.mmax = mmax;
+      ea.L = L;
+      ea.npad = sd.npad;
+      ea.nrep = sd.nrep;
+      ea.npairs = sd.npairs;
+      ea.Qb = g.Qb;
+      ea.eta = g.eta;
+      ea.Minv = g.Minv;
+      ea.su = g.restarts + 3 * g.b;
+      ea.reg = g.restarts + 4 * g.b;
+      ea.Ureg = ctx->Ureg;
+      ea.s_rec = ctx->s_rec;
+      for (int ri = 0; ri < nreg; ++ri) {
+        const int r = used[ri];
+        double* Ur = Unew + (int64_t)ri * stride * L;
+        double* TUr = TUnew + (int64_t)ri * stride * L;
+        if (!take[ri]) {  // keep the current space
+          CK(cudaMemcpyAsync(Ur, ctx->Ureg + (int64_t)ri * ctx->s_rec * L, (size_t)nsz[ri] * L * 8,
+                             cudaMemcpyDeviceToDevice, st));
+          CK(cudaMemcpyAsync(TUr, ctx->TUreg + (int64_t)ri * ctx->s_rec * L, (size_t)nsz[ri] * L * 8,
+                             cudaMemcpyDeviceToDevice, st));
+          continue;
+        }
+        const int sl = slot_of[round == 0 ? r : ri], m1 = hm[sl], sr = nsz[ri];
+        // Z = the cycle's search directions (u_j for j < su, else P^{-1} q_j) and normalised Q (j <= m1)
+        const dim3 gz((unsigned)((sd.nrep + 127) / 128), (unsigned)m1);
+        CK(cudaMemsetAsync(Z, 0, (size_t)m1 * L * 8, st));
+        K_DISPATCH(k, (k_rec_z<KK><<<gz, 128, 0, st>>>(ea, sl, m1, Z)));
+        LAUNCHED();
+        std::vector<double> heta(m1 + 1);
+        CK(cudaMemcpy(heta.data(), g.eta + (int64_t)sl * ld, (m1 + 1) * 8, cudaMemcpyDeviceToHost));
+        for (int j = 0; j <= m1; ++j) {
+          const double inv = 1.0 / heta[j];
+          CKB(cublasDcopy(ctx->cublas, (int)L, g.Qb + ((int64_t)sl * ld + j) * L, 1, Qn + (int64_t)j * L, 1));
+          CKB(cublasDscal(ctx->cublas, (int)L, &inv, Qn + (int64_t)j * L, 1));
+        }
+        const double* Hb = g.Hraw + (int64_t)sl * ld * mmax;  // column-major (m1+1) x m1, ld = mmax + 1
+        // A = Hbar^T Hbar, B = Z^T Z (+ tiny ridge), generalised symmetric eigenproblem A p = theta B p
+        CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_T, CUBLAS_OP_N, m1, m1, m1 + 1, &one, Hb, ld, Hb, ld, &zero, Am, m1));
+        CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_T, CUBLAS_OP_N, m1, m1, (int)L, &one, Z, (int)L, Z, (int)L, &zero, Bm,
+                        m1));
+        {
+          std::vector<double> hb((size_t)m1 * m1);
+          CK(cudaMemcpy(hb.data(), Bm, hb.size() * 8, cudaMemcpyDeviceToHost));
+          double tr = 0.0;
+          for (int j = 0; j < m1; ++j) tr += hb[(size_t)j * m1 + j];
+          const double ridge = 1e-10 * tr / m1;
+          for (int j = 0; j < m1; ++j) hb[(size_t)j * m1 + j] += ridge;
+          CK(cudaMemcpy(Bm, hb.data(), hb.size() * 8, cudaMemcpyHostToDevice));
+        }
+        int lwork = 0;
+        CKS(cusolverDnDsygvd_bufferSize(ctx->cusolver, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
+                                        CUBLAS_FILL_MODE_UPPER, m1, Am, m1, Bm, m1, Wv, &lwork));
+        dfree(work);
+        work = dalloc<double>(ctx, std::max(lwork, 1), false);
+        CKS(cusolverDnDsygvd(ctx->cusolver, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, m1,
+                             Am, m1, Bm, m1, Wv, work, lwork, dinfo));
+        int hinfo = 0;
+        CK(cudaMemcpy(&hinfo, dinfo, sizeof(int), cudaMemcpyDeviceToHost));
+        if (hinfo != 0) {
+          // Z^T Z numerically singular: select in the Euclidean metric of the coefficients instead
+          // (smallest right singular vectors of Hbar; measured nearly as effective)
+          CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_T, CUBLAS_OP_N, m1, m1, m1 + 1, &one, Hb, ld, Hb, ld, &zero, Am,
+                          m1));
+          int lw2 = 0;
+          CKS(cusolverDnDsyevd_bufferSize(ctx->cusolver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, m1, Am,
+                                          m1, Wv, &lw2));
+          dfree(work);
+          work = dalloc<double>(ctx, std::max(lw2, 1), false);
+          CKS(cusolverDnDsyevd(ctx->cusolver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, m1, Am, m1, Wv, work,
+                               lw2, dinfo));
+          CK(cudaMemcpy(&hinfo, dinfo, sizeof(int), cudaMemcpyDeviceToHost));
+          if (hinfo != 0) {
+            set_err(ctx, "lyap_build_recycle: syevd info = %d for seed %d", hinfo, r);
+            throw Fail{LYAP_ECUDA};
+          }
+        }
+        // P = eigenvectors of the sr smallest eigenvalues (ascending: first columns of Am);
+        // U = Z P, C(v)U = Qn Hbar P, TU = Delta(v) U - C(v) U
+        CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)L, sr, m1, &one, Z, (int)L, Am, m1, &zero, Ur,
+                        (int)L));
+        CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, m1 + 1, sr, m1, &one, Hb, ld, Am, m1, &zero, HP,
+                        m1 + 1));
+        CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)L, sr, m1 + 1, &one, Qn, (int)L, HP, m1 + 1,
+                        &zero, CU, (int)L));
+        std::vector<double> hs(k);
+        for (int64_t t = 0; t < k; ++t) hs[t] = 1.0 / seeds[(int64_t)r * k + t];
+        CK(cudaMemcpy(sig, hs.data(), k * 8, cudaMemcpyHostToDevice));
+        k_rec_tu<<<(unsigned)std::min<int64_t>(((int64_t)sr * L + 255) / 256, 65535), 256, 0, st>>>(
+            Ur, CU, sig, L, sd.npad, sr, TUr);
+        LAUNCHED();
+      }
+      CK(cudaStreamSynchronize(st));
+      dfree(ctx->Ureg);
+      dfree(ctx->TUreg);
+      ctx->Ureg = Unew;
+      ctx->TUreg = TUnew;
+      Unew = TUnew = nullptr;
+      sizes = nsz;
+      dfree(ctx->sreg);
+      ctx->sreg = dalloc<int>(ctx, nreg, false);
+      CK(cudaMemcpy(ctx->sreg, sizes.data(), nreg * sizeof(int), cudaMemcpyHostToDevice));
+      ctx->nreg = nreg;
+      ctx->s_rec = stride;
     }
-    CK(cudaStreamSynchronize(st));
-    ctx->Ureg = Unew;
-    ctx->TUreg = TUnew;
-    Unew = TUnew = nullptr;
-    dfree(ctx->sreg);
-    ctx->sreg = dalloc<int>(ctx, nreg, false);
-    CK(cudaMemcpy(ctx->sreg, sizes.data(), nreg * sizeof(int), cudaMemcpyHostToDevice));
+    std::vector<double> seeds_used;
+    for (int r : used)
+      for (int64_t t = 0; t < k; ++t) seeds_used.push_back(std::log(std::fabs(seeds[(int64_t)r * k + t])));
     ctx->reg_seeds.assign(reinterpret_cast<const char*>(seeds_used.data()), seeds_used.size() * sizeof(double));
-    ctx->nreg = nreg;
-    ctx->s_rec = s_eff;
   } catch (Fail f) {
     rc = f.code;
+    dfree(ctx->Ureg);
+    dfree(ctx->TUreg);
+    dfree(ctx->sreg);
+    ctx->Ureg = ctx->TUreg = nullptr;
+    ctx->sreg = nullptr;
+    ctx->nreg = ctx->s_rec = 0;
   }
   for (void* p : {(void*)dV, (void*)dtr, (void*)dst, (void*)Z, (void*)Qn, (void*)Am, (void*)Bm, (void*)Wv, (void*)work,
-                  (void*)HP, (void*)CU, (void*)sig, (void*)Unew, (void*)TUnew, (void*)dinfo})
+                  (void*)HP, (void*)CU, (void*)sig, (void*)Unew, (void*)TUnew, (void*)dinfo, (void*)dreg})
     dfree(p);
   return rc;
 }
