@@ -354,10 +354,37 @@ def test_recycle_any_space_keeps_parity():
     assert rel_err(tau2, tau).max() <= 1e-10
 
 
-@pytest.mark.parametrize("name,s", [("c1", 24), ("c2", 48)])
-def test_recycle_built_spaces_parity_and_savings(name, s):
-    """lyap_build_recycle from the 2^k grid corners: traces still match the oracle samples and the
-    T-applies per v drop."""
+def test_recycle_dependent_directions():
+    """A space with a repeated and a zero column: the recycled candidate C(v)u is dependent on the
+    current basis inside the first s steps (Arnoldi breakdown).  The cycle must still update x with
+    the u_i it used, the space is dropped at the next restart, and every trace matches the oracle."""
+    W = workloads.make("c1")
+    P = _problem(W.A0, W.Bl, W.Br, W.Q, W.E)
+    npad, n = P.info["npad"], W.n
+    rng = np.random.default_rng(52)
+    U = rng.standard_normal((1, 10, W.k, npad))
+    U[..., n:] = 0.0
+    U[0, 3] = U[0, 2]  # dependent: breakdown at step 3
+    U[0, 6] = 0.0      # (never reached in a cycle that broke down at 3)
+    P.set_recycle(U, np.array([[1.0, 1.0]]))
+    tau, st, ap, rs = P.trace_batch(W.V, return_diagnostics=True)
+    g = _golden("c1")
+    idx = np.array(g["indices"])
+    assert np.all(st == 0)
+    assert rel_err(tau[idx], np.array(g["traces"])).max() <= RTOL
+    U2 = U.copy()
+    U2[0, 0] = 0.0  # zero first direction: breakdown at step 0
+    P.set_recycle(U2, np.array([[1.0, 1.0]]))
+    tau2, st2, _, _ = P.trace_batch(W.V, return_diagnostics=True)
+    assert np.all(st2 == 0)
+    assert rel_err(tau2[idx], np.array(g["traces"])).max() <= RTOL
+
+
+@pytest.mark.parametrize("name,s,rounds", [("c1", 24, "1"), ("c1", 24, "2"), ("c2", 48, "2")])
+def test_recycle_built_spaces_parity_and_savings(name, s, rounds, monkeypatch):
+    """lyap_build_recycle from the 2^k grid corners, with (rounds = 2) and without the refinement
+    pass: traces still match the oracle samples and the T-applies per v drop."""
+    monkeypatch.setenv("LYAP_RECYCLE_ROUNDS", rounds)
     W = workloads.make(name)
     P = _problem(W.A0, W.Bl, W.Br, W.Q, W.E)
     P.reset_stats()
