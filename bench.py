@@ -288,7 +288,7 @@ def main():
     tfile = os.path.join(ROOT, "profiles", f"k1_traffic_{args.config}.json")
     if os.path.exists(tfile):
         traffic = json.load(open(tfile)).get("bytes_per_launch")
-    roof = {"bound": "fp64", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+    roof = {"bound": "tensor", "dtype": "f64", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
             "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
             "kernel": "k1_dgemm (Cauchy-fused T-apply GEMM, DMMA)",
             "peak_source": "measured DMMA mma.sync.m8n8k4.f64 microbench (profiles/r01_fp64_peaks.md); "

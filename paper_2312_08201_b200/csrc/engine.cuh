@@ -621,121 +621,66 @@ __global__ void __launch_bounds__(256) k_gout(EngArgs a) {
 }
 
 // ---------------------------------------------------------------- cycle end: R y = e
-// One block per slot that just finished a cycle (phase XUPD): the rotated Hessenberg (upper
-// triangular R, m1 x m1, packed by columns) is staged in shared memory with one coalesced load,
-// then one warp runs the back substitution with y distributed over the lanes (shuffle broadcast).
-__global__ void __launch_bounds__(256) k_backsub(EngArgs a, int smem_doubles) {
-  extern __shared__ double Rs[];  // m1 (m1 + 1) / 2, then m1 reciprocal diagonal entries
+// One block per slot that just finished a cycle (phase XUPD); R = the Givens-rotated Hessenberg
+// (m1 x m1 upper triangular, column j at H[j * ld], ld = mmax + 1).  Blocked by 32 rows from the
+// bottom: warp 0 solves a 32 x 32 diagonal block with the block's columns in registers (lane l holds
+// row l), so the serial chain is one multiply, one shuffle and one FMA per unknown; the whole block
+// then removes the solved unknowns from the rows above with a coalesced GEMV.  R is read once from
+// L2/HBM, nothing is staged; any m1 <= mmax (the earlier per-column version spent ~300 cycles per
+// unknown on predicated register selects and fell back to one global round trip per column).
+constexpr int BS_THREADS = 128;
+__global__ void __launch_bounds__(BS_THREADS) k_backsub(EngArgs a) {
+  __shared__ double es[32 * CTRL_RMAX];  // the right-hand side e, updated in place
+  __shared__ double ys[32];
   const int slot = blockIdx.x;
   if (a.phase[slot] != PH_XUPD) return;
   const int ld = a.mmax + 1;
   const int m1 = a.m[slot];
   const double* H = a.H + (int64_t)slot * ld * a.mmax;
-  if (m1 * (m1 + 1) / 2 + m1 > smem_doubles) {  // long cycle: R from global, one column ahead
-    if (threadIdx.x >= 32) return;
-    const int lane = threadIdx.x;
-    const double* e = a.e + (int64_t)slot * ld;
-    const double* eta = a.eta + (int64_t)slot * ld;
-    double yv[CTRL_RMAX], hv[CTRL_RMAX], hn[CTRL_RMAX];
-#pragma unroll
-    for (int r = 0; r < CTRL_RMAX; ++r) {
-      const int i = lane + 32 * r;
-      yv[r] = (i < m1) ? e[i] : 0.0;
-      hv[r] = (i < m1) ? H[(int64_t)(m1 - 1) * ld + i] : 0.0;
-    }
-    for (int j = m1 - 1; j >= 0; --j) {
-      if (j > 0) {
-#pragma unroll
-        for (int r = 0; r < CTRL_RMAX; ++r) {
-          const int i = lane + 32 * r;
-          hn[r] = (i < j) ? H[(int64_t)(j - 1) * ld + i] : 0.0;
-        }
-      }
-      const int owner = j & 31, rj = j >> 5;
-      double yj = 0.0, dj = 0.0;
-#pragma unroll
-      for (int r = 0; r < CTRL_RMAX; ++r)
-        if (r == rj) {
-          yj = yv[r];
-          dj = hv[r];
-        }
-      yj = __shfl_sync(0xffffffffu, yj, owner);
-      dj = __shfl_sync(0xffffffffu, dj, owner);
-      yj = dj != 0.0 ? yj / dj : 0.0;
-#pragma unroll
-      for (int r = 0; r < CTRL_RMAX; ++r) {
-        const int i = lane + 32 * r;
-        if (i == j) yv[r] = yj;
-        else if (i < j) yv[r] -= hv[r] * yj;
-        hv[r] = hn[r];
-      }
-    }
-    double* y = a.y + (int64_t)slot * a.mmax;
-#pragma unroll
-    for (int r = 0; r < CTRL_RMAX; ++r) {
-      const int i = lane + 32 * r;
-      if (i < m1) y[i] = i < a.su[slot] ? yv[r] : yv[r] / eta[i];
-    }
-    return;
-  }
-  double* dinv = Rs + m1 * (m1 + 1) / 2;
-  // flat loop over the packed triangle, 8 independent loads in flight per thread (latency-bound
-  // otherwise: one dependent L2 round trip per element)
-  const int tot = m1 * (m1 + 1) / 2;
-  constexpr int UNR = 8;
-  for (int base = threadIdx.x; base < tot; base += blockDim.x * UNR) {
-    double v[UNR];
-    int jj[UNR], ii[UNR];
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      const int idx = base + u * blockDim.x;
-      int j = (int)((sqrt(8.0 * idx + 1.0) - 1.0) * 0.5);
-      if ((j + 1) * (j + 2) / 2 <= idx) ++j;  // guard the float rounding of the inversion
-      if (j * (j + 1) / 2 > idx) --j;
-      jj[u] = j;
-      ii[u] = idx - j * (j + 1) / 2;
-      v[u] = idx < tot ? H[(int64_t)j * ld + ii[u]] : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      const int idx = base + u * blockDim.x;
-      if (idx < tot) {
-        Rs[idx] = v[u];
-        if (ii[u] == jj[u]) dinv[jj[u]] = v[u] != 0.0 ? 1.0 / v[u] : 0.0;
-      }
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x >= 32) return;
-  const int lane = threadIdx.x;
   const double* e = a.e + (int64_t)slot * ld;
   const double* eta = a.eta + (int64_t)slot * ld;
-  double yv[CTRL_RMAX];
-#pragma unroll
-  for (int r = 0; r < CTRL_RMAX; ++r) {
-    const int i = lane + 32 * r;
-    yv[r] = (i < m1) ? e[i] : 0.0;
-  }
-  for (int j = m1 - 1; j >= 0; --j) {
-    const double* Rj = Rs + j * (j + 1) / 2;
-    const int owner = j & 31, rj = j >> 5;
-    double yj = 0.0;
-#pragma unroll
-    for (int r = 0; r < CTRL_RMAX; ++r)
-      if (r == rj) yj = yv[r];
-    yj = __shfl_sync(0xffffffffu, yj, owner) * dinv[j];
-#pragma unroll
-    for (int r = 0; r < CTRL_RMAX; ++r) {
-      const int i = lane + 32 * r;
-      if (i == j) yv[r] = yj;
-      else if (i < j) yv[r] -= Rj[i] * yj;
-    }
-  }
   double* y = a.y + (int64_t)slot * a.mmax;
+  const int su = a.su[slot];
+  for (int i = threadIdx.x; i < m1; i += BS_THREADS) es[i] = e[i];
+  __syncthreads();
+  for (int r0 = m1 > 0 ? ((m1 - 1) / 32) * 32 : -1; r0 >= 0; r0 -= 32) {
+    const int nb = min(32, m1 - r0);
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x, i = r0 + lane;
+      double Rr[32];
 #pragma unroll
-  for (int r = 0; r < CTRL_RMAX; ++r) {
-    const int i = lane + 32 * r;
-    if (i < m1) y[i] = i < a.su[slot] ? yv[r] : yv[r] / eta[i];  // u_i raw; P^{-1} q^_i / eta_i
+      for (int c = 0; c < 32; ++c) Rr[c] = (c < nb && lane <= c) ? H[(int64_t)(r0 + c) * ld + i] : 0.0;
+      double d = 0.0;
+#pragma unroll
+      for (int c = 0; c < 32; ++c) d = (c == lane) ? Rr[c] : d;
+      const double dinv = d != 0.0 ? 1.0 / d : 0.0;  // a zero pivot (breakdown column) gives y = 0
+      double ev = lane < nb ? es[i] : 0.0, yl = 0.0;
+#pragma unroll
+      for (int c = 31; c >= 0; --c) {
+        if (c < nb) {  // warp-uniform
+          const double yc = __shfl_sync(0xffffffffu, ev * dinv, c);
+          yl = (lane == c) ? yc : yl;
+          ev = (lane < c) ? fma(-Rr[c], yc, ev) : ev;
+        }
+      }
+      if (lane < nb) {
+        ys[lane] = yl;
+        y[i] = i < su ? yl : yl / eta[i];  // u_i raw; P^{-1} q^_i / eta_i
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < r0; i += BS_THREADS) {
+      double acc0 = 0.0, acc1 = 0.0;
+      int c = 0;
+#pragma unroll 4
+      for (; c + 1 < nb; c += 2) {
+        acc0 = fma(H[(int64_t)(r0 + c) * ld + i], ys[c], acc0);
+        acc1 = fma(H[(int64_t)(r0 + c + 1) * ld + i], ys[c + 1], acc1);
+      }
+      if (c < nb) acc0 = fma(H[(int64_t)(r0 + c) * ld + i], ys[c], acc0);
+      es[i] -= acc0 + acc1;
+    }
+    __syncthreads();
   }
 }
 

@@ -358,9 +358,6 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   const size_t upd_smem = sizeof(double) * (mmax + 1);
   const size_t ctrl_smem = sizeof(double) * 16 * (size_t)(mmax + 2);
   const size_t gram_smem = sizeof(double) * (size_t)(mmax + 1);
-  const size_t bs_smem = std::min<size_t>(sizeof(double) * ((size_t)mmax * (mmax + 1) / 2 + mmax), 220 * 1024);
-  const int bs_doubles = (int)(bs_smem / sizeof(double));
-  if (bs_smem > 48 * 1024) CK(cudaFuncSetAttribute(k_backsub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bs_smem));
   if (gram_smem > 48 * 1024) CK(cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_smem));
   if (ctrl_smem > 48 * 1024) CK(cudaFuncSetAttribute(k_ctrl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctrl_smem));
   if (upd_smem > 48 * 1024) CK(cudaFuncSetAttribute(k_upd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem));
@@ -407,7 +404,7 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
       k_gout<<<dim3((unsigned)std::min<int64_t>((g.L + 255) / 256, 64), (unsigned)bg), 256, 0, sg>>>(x);
       LAUNCHED();
     }
-    k_backsub<<<bg, 256, bs_smem, sg>>>(x, bs_doubles);
+    k_backsub<<<bg, BS_THREADS, 0, sg>>>(x);
     LAUNCHED();
     k_xcomb<<<gxc, 256, 0, sg>>>(x);
     LAUNCHED();
