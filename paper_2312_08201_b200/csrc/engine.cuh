@@ -333,6 +333,7 @@ __global__ void __launch_bounds__(256) k_uapply(EngArgs a) {
 // k_dots, ITER: part[slot][i][chunk] = q^_i . w  (i <= m) and part2[slot][i][chunk] = q^_i . q^_m
 // (i < m), w = the candidate q^_{m+1} written by K1's epilogue.
 // VERIFY: part3[slot][chunk] = (||R||^2, ||rhs||^2, <hf, X>) with R in q^_0.
+constexpr int DOT_IG = 64;  // basis vectors per k_dots block (grid.z splits long cycles)
 __global__ void __launch_bounds__(256) k_dots(EngArgs a) {
   __shared__ double ws[RED_CE];
   __shared__ double qm[RED_CE];
@@ -342,6 +343,7 @@ __global__ void __launch_bounds__(256) k_dots(EngArgs a) {
   const int64_t e0 = (int64_t)chunk * RED_CE;
   const int64_t qs = (int64_t)(a.mmax + 1) * a.L;
   if (ph == PH_VERIFY || ph == PH_START) {
+    if (blockIdx.z != 0) return;
     double* R = a.Qb + slot * qs;
     const double* X = a.X + (int64_t)slot * a.L;
     const bool start = ph == PH_START;  // g = 0: R = rhs, written here as q^_0
@@ -376,6 +378,9 @@ __global__ void __launch_bounds__(256) k_dots(EngArgs a) {
   }
   if (ph != PH_ITER) return;
   const int m = a.m[slot];
+  const int i0 = blockIdx.z * DOT_IG;  // this block's basis vectors: [i0, min(m, i0 + DOT_IG - 1)]
+  if (i0 > m) return;
+  const int i1 = min(m, i0 + DOT_IG - 1);
   const double* w = a.Qb + slot * qs + (int64_t)(m + 1) * a.L;
   const double* qlast = a.Qb + slot * qs + (int64_t)m * a.L;
   for (int i = threadIdx.x; i < RED_CE; i += blockDim.x) {
@@ -386,16 +391,21 @@ __global__ void __launch_bounds__(256) k_dots(EngArgs a) {
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int lim = (int)((a.L - e0) < RED_CE ? (a.L - e0) : RED_CE);
-  for (int i = warp; i <= m; i += 8) {
+  for (int i = i0 + warp; i <= i1; i += 8) {
     const double* q = a.Qb + slot * qs + (int64_t)i * a.L + e0;
     double d0 = 0.0, d1 = 0.0, g0 = 0.0, g1 = 0.0;
     int e = lane;
-    for (; e + 96 < lim; e += 128) {
-      const double x0 = q[e], x1 = q[e + 32], x2 = q[e + 64], x3 = q[e + 96];
-      d0 += x0 * ws[e] + x2 * ws[e + 64];
-      d1 += x1 * ws[e + 32] + x3 * ws[e + 96];
-      g0 += x0 * qm[e] + x2 * qm[e + 64];
-      g1 += x1 * qm[e + 32] + x3 * qm[e + 96];
+    for (; e + 224 < lim; e += 256) {  // 8 independent loads per lane per round
+      double x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = q[e + 32 * u];
+#pragma unroll
+      for (int u = 0; u < 8; u += 2) {
+        d0 = fma(x[u], ws[e + 32 * u], d0);
+        d1 = fma(x[u + 1], ws[e + 32 * u + 32], d1);
+        g0 = fma(x[u], qm[e + 32 * u], g0);
+        g1 = fma(x[u + 1], qm[e + 32 * u + 32], g1);
+      }
     }
     for (; e < lim; e += 32) {
       d0 += q[e] * ws[e];
@@ -482,12 +492,30 @@ __global__ void __launch_bounds__(256) k_upd(EngArgs a) {
     ok[r] = eo[r] < a.L;
     acc[r] = 0.0;
   }
-  for (int i = 0; i <= m; ++i) {
+  // 8 basis vectors per round: 8 * EPT independent loads in flight per thread (the chain over the
+  // basis, not bandwidth, bounds the slot with the longest cycle otherwise)
+  int i = 0;
+  for (; i + 8 <= m + 1; i += 8) {
+    double v[8][EPT];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double* q = Q + (int64_t)(i + u) * a.L;
+#pragma unroll
+      for (int r = 0; r < EPT; ++r) v[u][r] = ok[r] ? q[eo[r]] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double c = cfs[i + u];
+#pragma unroll
+      for (int r = 0; r < EPT; ++r) acc[r] = fma(c, v[u][r], acc[r]);
+    }
+  }
+  for (; i <= m; ++i) {
     const double c = cfs[i];
     const double* q = Q + (int64_t)i * a.L;
 #pragma unroll
     for (int r = 0; r < EPT; ++r)
-      if (ok[r]) acc[r] += c * q[eo[r]];
+      if (ok[r]) acc[r] = fma(c, q[eo[r]], acc[r]);
   }
   double nrm = 0.0;
 #pragma unroll

@@ -392,7 +392,7 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
       LAUNCHED();
     }
     launch_k1(ctx, gk[gi], sg, evb, eve, evflags, gi);
-    k_dots<<<gred, 256, 0, sg>>>(x);
+    k_dots<<<dim3((unsigned)g.nchunk, (unsigned)bg, (unsigned)((mmax + DOT_IG) / DOT_IG)), 256, 0, sg>>>(x);
     LAUNCHED();
     k_gram<<<bg, 256, gram_smem, sg>>>(x);
     LAUNCHED();
