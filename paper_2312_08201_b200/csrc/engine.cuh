@@ -454,16 +454,26 @@ __global__ void __launch_bounds__(256) k_gram(EngArgs a) {
   double* Hc = a.H + (int64_t)slot * ld * a.mmax + (int64_t)m * ld;
   double* cf = a.cf + (int64_t)slot * ld;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int i = warp; i <= m; i += nw) {
+  // four rows per warp at a time: 4 independent loads per lane per step of the row sweep
+  for (int i = warp * 4; i <= m; i += nw * 4) {
     const double* Gi = G + (int64_t)i * ld;
-    double acc = 0.0;
-    for (int j = lane; j <= m; j += 32) acc += Gi[j] * ds[j];
-    acc = warp_sum(acc);
-    if (lane == 0) {
-      const double c = 2.0 * ds[i] - acc;
-      Hc[i] = c;
-      cf[i] = c / eta[i];
-      if (a.record) a.Hraw[(int64_t)slot * ld * a.mmax + (int64_t)m * ld + i] = c;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 2
+    for (int j = lane; j <= m; j += 32) {
+      const double dj = ds[j];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (i + u <= m) acc[u] = fma(Gi[(int64_t)u * ld + j], dj, acc[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double sum = warp_sum(acc[u]);
+      if (lane == 0 && i + u <= m) {
+        const double c = 2.0 * ds[i + u] - sum;
+        Hc[i + u] = c;
+        cf[i + u] = c / eta[i + u];
+        if (a.record) a.Hraw[(int64_t)slot * ld * a.mmax + (int64_t)m * ld + i + u] = c;
+      }
     }
   }
 }
@@ -743,11 +753,16 @@ __global__ void __launch_bounds__(256) k_xcomb(EngArgs a) {
     double s0 = 0.0, s1 = 0.0;
     if (e < a.L) {
       int i = sl;
-      for (; i + 4 < m1; i += 8) {
-        s0 += ys[i] * Q[(int64_t)i * a.L + e];
-        s1 += ys[i + 4] * Q[(int64_t)(i + 4) * a.L + e];
+      double s2 = 0.0, s3 = 0.0;
+      for (; i + 12 < m1; i += 16) {  // 4 independent basis loads per step
+        s0 = fma(ys[i], Q[(int64_t)i * a.L + e], s0);
+        s1 = fma(ys[i + 4], Q[(int64_t)(i + 4) * a.L + e], s1);
+        s2 = fma(ys[i + 8], Q[(int64_t)(i + 8) * a.L + e], s2);
+        s3 = fma(ys[i + 12], Q[(int64_t)(i + 12) * a.L + e], s3);
       }
-      for (; i < m1; i += 4) s0 += ys[i] * Q[(int64_t)i * a.L + e];
+      for (; i < m1; i += 4) s0 = fma(ys[i], Q[(int64_t)i * a.L + e], s0);
+      s0 += s2;
+      s1 += s3;
     }
     red[sl][el] = s0 + s1;
     __syncthreads();
