@@ -101,5 +101,6 @@ struct lyap_ctx {
   std::vector<double> auto_box;  // bounding box (lo, hi per parameter) the automatic spaces were built for
   bool recycle_manual = false;   // spaces given by lyap_set_recycle / lyap_build_recycle: no automatic rebuild
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evfork = nullptr, evjoin = nullptr;
-  cudaStream_t stream2 = nullptr;  // second slot group
+  cudaStream_t xstream[4] = {};  // streams of slot groups 1..3 (group 0 runs on `stream`)
+  cudaEvent_t xjoin[4] = {};
 };

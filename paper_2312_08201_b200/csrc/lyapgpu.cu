@@ -166,7 +166,8 @@ void ensure_engine(lyap_ctx* ctx, int b, int mmax) {
   g.mmax = mmax;
   g.L = s.k * s.npad;
   g.groups = b >= 64 ? 2 : 1;
-  if (const char* ev = std::getenv("LYAP_GROUPS")) g.groups = std::max(1, std::min(2, std::atoi(ev)));  // experiments
+  if (const char* ev = std::getenv("LYAP_GROUPS")) g.groups = std::max(1, std::min(4, std::atoi(ev)));  // experiments
+  g.groups = std::max(1, std::min(g.groups, b / 32));  // every group keeps >= 32 slots
   g.ncol = roundup((int64_t)((b + g.groups - 1) / g.groups) * s.k * s.k, tile_n(s));
   g.nchunk = (int)((g.L + RED_CE - 1) / RED_CE);
   g.Bop = dalloc<double>(ctx, (size_t)g.groups * s.npad * g.ncol);
@@ -368,10 +369,12 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   sts[0] = st;
   CK(cudaEventRecord(ctx->ev0, st));
   if (G > 1) {
-    if (!ctx->stream2) CK(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
-    sts[1] = ctx->stream2;
     CK(cudaEventRecord(ctx->evfork, st));
-    CK(cudaStreamWaitEvent(ctx->stream2, ctx->evfork, 0));
+    for (int gi = 1; gi < G; ++gi) {
+      if (!ctx->xstream[gi]) CK(cudaStreamCreateWithFlags(&ctx->xstream[gi], cudaStreamNonBlocking));
+      sts[gi] = ctx->xstream[gi];
+      CK(cudaStreamWaitEvent(sts[gi], ctx->evfork, 0));
+    }
   }
   // one engine iteration of slot group gi on stream sg (optionally with events around the GEMM)
   auto issue = [&](int gi, cudaStream_t sg, cudaEvent_t evb, cudaEvent_t eve, unsigned evflags) -> int64_t {
@@ -464,9 +467,10 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   for (auto& ge : gexec)
     if (ge) cudaGraphExecDestroy(ge);
   for (auto& e : evs) cudaEventDestroy(e);
-  if (G > 1) {
-    CK(cudaEventRecord(ctx->evjoin, ctx->stream2));
-    CK(cudaStreamWaitEvent(st, ctx->evjoin, 0));
+  for (int gi = 1; gi < G; ++gi) {
+    if (!ctx->xjoin[gi]) CK(cudaEventCreateWithFlags(&ctx->xjoin[gi], cudaEventDisableTiming));
+    CK(cudaEventRecord(ctx->xjoin[gi], sts[gi]));
+    CK(cudaStreamWaitEvent(st, ctx->xjoin[gi], 0));
   }
   CK(cudaMemcpyAsync(g.h_ctrl, g.ctrl, 8 * (G + 1) * sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaEventRecord(ctx->ev1, st));
@@ -586,7 +590,10 @@ static void destroy_impl(lyap_ctx* c) {
   dfree(c->sreg);
   c->basis.reset();
   if (c->stream) cudaStreamDestroy(c->stream);
-  if (c->stream2) cudaStreamDestroy(c->stream2);
+  for (int gi = 1; gi < 4; ++gi) {
+    if (c->xstream[gi]) cudaStreamDestroy(c->xstream[gi]);
+    if (c->xjoin[gi]) cudaEventDestroy(c->xjoin[gi]);
+  }
   if (c->evfork) cudaEventDestroy(c->evfork);
   if (c->evjoin) cudaEventDestroy(c->evjoin);
   delete c;
