@@ -539,6 +539,59 @@ __global__ void __launch_bounds__(256) k_upd(EngArgs a) {
   if (threadIdx.x == 0) a.part3[((int64_t)slot * a.nchunk + chunk) * 3] = nrm;
 }
 
+// ---------------------------------------------------------------- cycle end: R y = e
+// Run by the k_ctrl warp that ends a slot's cycle (no separate launch on the iteration's chain).
+// R = the Givens-rotated Hessenberg (m1 x m1 upper triangular, column j at H[j * ld]).  Blocked by
+// 32 rows from the bottom: the warp solves a 32 x 32 diagonal block with the block's columns in
+// registers (lane l holds row l), so the serial chain is one multiply, one shuffle and one FMA per
+// unknown; it then removes the solved unknowns from the rows above (lane l owns rows l + 32 j, a
+// coalesced sweep of the block's columns).  e is reduced in place (it is rebuilt at the next cycle).
+// (An earlier per-column version spent ~300 cycles per unknown on predicated register selects;
+// profiles/r01_backsub_ncu.md.)
+__device__ __forceinline__ void warp_backsub(const EngArgs& a, int slot, int lane) {
+  const int ld = a.mmax + 1;
+  const int m1 = a.m[slot];
+  const double* H = a.H + (int64_t)slot * ld * a.mmax;
+  double* e = a.e + (int64_t)slot * ld;
+  const double* eta = a.eta + (int64_t)slot * ld;
+  double* y = a.y + (int64_t)slot * a.mmax;
+  const int su = a.su[slot];
+  for (int r0 = m1 > 0 ? ((m1 - 1) / 32) * 32 : -1; r0 >= 0; r0 -= 32) {
+    const int nb = min(32, m1 - r0);
+    const int i = r0 + lane;
+    double Rr[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) Rr[c] = (c < nb && lane <= c) ? H[(int64_t)(r0 + c) * ld + i] : 0.0;
+    double d = 0.0;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) d = (c == lane) ? Rr[c] : d;
+    const double dinv = d != 0.0 ? 1.0 / d : 0.0;  // a zero pivot (breakdown column) gives y = 0
+    double ev = lane < nb ? e[i] : 0.0, yl = 0.0;
+#pragma unroll
+    for (int c = 31; c >= 0; --c) {
+      if (c < nb) {  // warp-uniform
+        const double yc = __shfl_sync(0xffffffffu, ev * dinv, c);
+        yl = (lane == c) ? yc : yl;
+        ev = (lane < c) ? fma(-Rr[c], yc, ev) : ev;
+      }
+    }
+    if (lane < nb) y[i] = i < su ? yl : yl / eta[i];  // u_i raw; P^{-1} q^_i / eta_i
+    double yb[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) yb[c] = __shfl_sync(0xffffffffu, yl, c);
+    for (int r = lane; r < r0; r += 32) {  // r0 is a multiple of 32: uniform trip count
+      double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+      for (int c = 0; c < 32; c += 2) {
+        if (c < nb) acc0 = fma(H[(int64_t)(r0 + c) * ld + r], yb[c], acc0);
+        if (c + 1 < nb) acc1 = fma(H[(int64_t)(r0 + c + 1) * ld + r], yb[c + 1], acc1);
+      }
+      e[r] -= acc0 + acc1;
+    }
+    __syncwarp();
+  }
+}
+
 // ---------------------------------------------------------------- per-slot control (K4)
 // one warp per slot: VERIFY -> done / restart;  ITER -> Hessenberg column, Givens, cycle end.
 __global__ void __launch_bounds__(128) k_ctrl(EngArgs a) {
@@ -646,6 +699,10 @@ __global__ void __launch_bounds__(128) k_ctrl(EngArgs a) {
       a.phase[slot] = PH_XUPD;
     }
   }
+  if (!a.record) {
+    __syncwarp();  // the rotated column (Hc) and e[m], e[m + 1] are visible to the whole warp
+    warp_backsub(a, slot, lane);
+  }
 }
 
 // k_gout (lyap_solution only): a slot that finished its v in this iteration's k_ctrl is FREE until
@@ -658,69 +715,6 @@ __global__ void __launch_bounds__(256) k_gout(EngArgs a) {
     a.gout[idx * a.L + e] = a.X[(int64_t)slot * a.L + e];
 }
 
-// ---------------------------------------------------------------- cycle end: R y = e
-// One block per slot that just finished a cycle (phase XUPD); R = the Givens-rotated Hessenberg
-// (m1 x m1 upper triangular, column j at H[j * ld], ld = mmax + 1).  Blocked by 32 rows from the
-// bottom: warp 0 solves a 32 x 32 diagonal block with the block's columns in registers (lane l holds
-// row l), so the serial chain is one multiply, one shuffle and one FMA per unknown; the whole block
-// then removes the solved unknowns from the rows above with a coalesced GEMV.  R is read once from
-// L2/HBM, nothing is staged; any m1 <= mmax (the earlier per-column version spent ~300 cycles per
-// unknown on predicated register selects and fell back to one global round trip per column).
-constexpr int BS_THREADS = 128;
-__global__ void __launch_bounds__(BS_THREADS) k_backsub(EngArgs a) {
-  __shared__ double es[32 * CTRL_RMAX];  // the right-hand side e, updated in place
-  __shared__ double ys[32];
-  const int slot = blockIdx.x;
-  if (a.phase[slot] != PH_XUPD) return;
-  const int ld = a.mmax + 1;
-  const int m1 = a.m[slot];
-  const double* H = a.H + (int64_t)slot * ld * a.mmax;
-  const double* e = a.e + (int64_t)slot * ld;
-  const double* eta = a.eta + (int64_t)slot * ld;
-  double* y = a.y + (int64_t)slot * a.mmax;
-  const int su = a.su[slot];
-  for (int i = threadIdx.x; i < m1; i += BS_THREADS) es[i] = e[i];
-  __syncthreads();
-  for (int r0 = m1 > 0 ? ((m1 - 1) / 32) * 32 : -1; r0 >= 0; r0 -= 32) {
-    const int nb = min(32, m1 - r0);
-    if (threadIdx.x < 32) {
-      const int lane = threadIdx.x, i = r0 + lane;
-      double Rr[32];
-#pragma unroll
-      for (int c = 0; c < 32; ++c) Rr[c] = (c < nb && lane <= c) ? H[(int64_t)(r0 + c) * ld + i] : 0.0;
-      double d = 0.0;
-#pragma unroll
-      for (int c = 0; c < 32; ++c) d = (c == lane) ? Rr[c] : d;
-      const double dinv = d != 0.0 ? 1.0 / d : 0.0;  // a zero pivot (breakdown column) gives y = 0
-      double ev = lane < nb ? es[i] : 0.0, yl = 0.0;
-#pragma unroll
-      for (int c = 31; c >= 0; --c) {
-        if (c < nb) {  // warp-uniform
-          const double yc = __shfl_sync(0xffffffffu, ev * dinv, c);
-          yl = (lane == c) ? yc : yl;
-          ev = (lane < c) ? fma(-Rr[c], yc, ev) : ev;
-        }
-      }
-      if (lane < nb) {
-        ys[lane] = yl;
-        y[i] = i < su ? yl : yl / eta[i];  // u_i raw; P^{-1} q^_i / eta_i
-      }
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < r0; i += BS_THREADS) {
-      double acc0 = 0.0, acc1 = 0.0;
-      int c = 0;
-#pragma unroll 4
-      for (; c + 1 < nb; c += 2) {
-        acc0 = fma(H[(int64_t)(r0 + c) * ld + i], ys[c], acc0);
-        acc1 = fma(H[(int64_t)(r0 + c + 1) * ld + i], ys[c + 1], acc1);
-      }
-      if (c < nb) acc0 = fma(H[(int64_t)(r0 + c) * ld + i], ys[c], acc0);
-      es[i] -= acc0 + acc1;
-    }
-    __syncthreads();
-  }
-}
 
 // ---------------------------------------------------------------- solution update
 // XUPD: X += P(v)^{-1} (sum_{i<m} y_i q^_i)   (y already carries the 1/eta_i).  Two kernels: the

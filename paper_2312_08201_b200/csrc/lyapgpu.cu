@@ -407,8 +407,6 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
       k_gout<<<dim3((unsigned)std::min<int64_t>((g.L + 255) / 256, 64), (unsigned)bg), 256, 0, sg>>>(x);
       LAUNCHED();
     }
-    k_backsub<<<bg, BS_THREADS, 0, sg>>>(x);
-    LAUNCHED();
     k_xcomb<<<gxc, 256, 0, sg>>>(x);
     LAUNCHED();
     K_DISPATCH(s.k, (k_xupd<KK><<<grep, 128, 0, sg>>>(x)));
