@@ -144,12 +144,9 @@ __global__ void k_assign(EngArgs a) {
 // ---------------------------------------------------------------- preconditioner factor (K2)
 // Minv[slot][rep] = (diag(sigma) - F_rep)^{-1}, k x k complex, Gauss-Jordan with partial pivoting;
 // rows with v_t = 0 are identity rows (column t absent).  Cold start zeroes X for new v's.
+// (Run by k_prec's thread for the same (slot, rep) before it applies the block: one launch fewer.)
 template <int K>
-__global__ void __launch_bounds__(128) k_pfactor(EngArgs a) {
-  const int slot = blockIdx.y;
-  if (!a.newv[slot]) return;
-  const int64_t rep = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (rep >= a.nrep) return;
+__device__ __forceinline__ void pfactor_rep(const EngArgs& a, int slot, int64_t rep) {
   cplx M[K][K], R[K][K];
 #pragma unroll
   for (int s = 0; s < K; ++s) {
@@ -229,15 +226,17 @@ __device__ __forceinline__ void apply_minv(const double* mi, const cplx (&r)[K],
 }
 
 // ---------------------------------------------------------------- apply input (K2 apply)
-// ITER: Xin = P(v)^{-1} (q^_m / eta_m);  VERIFY: Xin = X.
+// ITER: Xin = P(v)^{-1} (q^_m / eta_m);  VERIFY: Xin = X.  A slot with a new v first factors its
+// blocks (pfactor_rep).
 template <int K>
 __global__ void __launch_bounds__(128) k_prec(EngArgs a) {
   const int slot = blockIdx.y;
+  const int64_t rep = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (rep >= a.nrep) return;
+  if (a.newv[slot]) pfactor_rep<K>(a, slot, rep);  // a v assigned in this iteration's k_assign
   const int ph = a.phase[slot];
   if (ph != PH_ITER && ph != PH_VERIFY) return;
   if (ph == PH_ITER && a.m[slot] < a.su[slot]) return;  // recycled direction: no K1 input
-  const int64_t rep = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (rep >= a.nrep) return;
   const int64_t c = rep_coord(rep, a.npairs);
   const bool pair = rep < a.npairs;
   double* xin = a.Xin + (int64_t)slot * a.L;

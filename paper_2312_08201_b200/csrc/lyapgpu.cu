@@ -386,8 +386,6 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
     const dim3 gxc((unsigned)std::min<int64_t>((g.L + 63) / 64, 128), (unsigned)bg);
     k_assign<<<1, (int)roundup(bg, 32), 0, sg>>>(x);
     LAUNCHED();
-    K_DISPATCH(s.k, (k_pfactor<KK><<<grep, 128, 0, sg>>>(x)));
-    LAUNCHED();
     K_DISPATCH(s.k, (k_prec<KK><<<grep, 128, 0, sg>>>(x)));
     LAUNCHED();
     if (x.s_rec > 0) {
