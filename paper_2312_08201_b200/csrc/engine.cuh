@@ -716,73 +716,78 @@ __global__ void __launch_bounds__(256) k_gout(EngArgs a) {
 
 
 // ---------------------------------------------------------------- solution update
-// XUPD: X += P(v)^{-1} (sum_{i<m} y_i q^_i)   (y already carries the 1/eta_i).  Two kernels: the
-// basis combination is elementwise (coalesced over the vector, many blocks per slot); the k x k
-// P^{-1} blocks then act per representative.  Xin (consumed by K1 earlier in the iteration) holds
-// the combination in between.
+// XUPD: X += U y_U + P(v)^{-1} (sum_{i>=su} y_i q^_i)   (y already carries the 1/eta_i).  One kernel:
+// a block owns a window of 64 coordinates for all k rows (pairs never straddle it: the window starts
+// at an even coordinate), forms the basis combination there (64 elements x 4 slices of the basis
+// index, reduced in shared memory), then applies the k x k P^{-1} block of every representative in
+// the window.
+template <int K>
 __global__ void __launch_bounds__(256) k_xcomb(EngArgs a) {
-  // 64 elements x 4 slices of the basis index per block; slices reduced in shared memory
   __shared__ double ys[1024];
   __shared__ double red[4][64];
+  __shared__ double xs[K][64];
   const int slot = blockIdx.y;
   if (a.phase[slot] != PH_XUPD) return;
   const int m1 = a.m[slot];
   const int su = min(a.su[slot], m1);
-  for (int i = threadIdx.x; i < m1; i += blockDim.x) ys[i] = i < su ? 0.0 : a.y[(int64_t)slot * a.mmax + i];
+  const double* ysl = a.y + (int64_t)slot * a.mmax;
+  for (int i = threadIdx.x; i < m1; i += blockDim.x) ys[i] = i < su ? 0.0 : ysl[i];
   __syncthreads();
-  if (su > 0) {  // recycled directions enter x directly (not through P^{-1})
-    const double* U = a.Ureg + (int64_t)a.reg[slot] * a.s_rec * a.L;
-    const double* ysl = a.y + (int64_t)slot * a.mmax;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < a.L; e += (int64_t)gridDim.x * blockDim.x) {
-      double acc = 0.0;
-      for (int i = 0; i < su; ++i) acc += ysl[i] * U[(int64_t)i * a.L + e];
-      a.X[(int64_t)slot * a.L + e] += acc;
-    }
-  }
   const double* Q = a.Qb + (int64_t)slot * (a.mmax + 1) * a.L;
+  double* X = a.X + (int64_t)slot * a.L;
   const int el = threadIdx.x & 63, sl = threadIdx.x >> 6;
-  for (int64_t e0 = (int64_t)blockIdx.x * 64; e0 < a.L; e0 += (int64_t)gridDim.x * 64) {
-    const int64_t e = e0 + el;
-    double s0 = 0.0, s1 = 0.0;
-    if (e < a.L) {
-      int i = sl;
-      double s2 = 0.0, s3 = 0.0;
-      for (; i + 12 < m1; i += 16) {  // 4 independent basis loads per step
-        s0 = fma(ys[i], Q[(int64_t)i * a.L + e], s0);
-        s1 = fma(ys[i + 4], Q[(int64_t)(i + 4) * a.L + e], s1);
-        s2 = fma(ys[i + 8], Q[(int64_t)(i + 8) * a.L + e], s2);
-        s3 = fma(ys[i + 12], Q[(int64_t)(i + 12) * a.L + e], s3);
+  for (int64_t c0 = (int64_t)blockIdx.x * 64; c0 < a.npad; c0 += (int64_t)gridDim.x * 64) {
+    const int64_t c = c0 + el;
+#pragma unroll 1
+    for (int t = 0; t < K; ++t) {
+      const int64_t e = (int64_t)t * a.npad + c;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      if (c < a.npad) {
+        int i = sl;
+        for (; i + 12 < m1; i += 16) {  // 4 independent basis loads per step
+          s0 = fma(ys[i], Q[(int64_t)i * a.L + e], s0);
+          s1 = fma(ys[i + 4], Q[(int64_t)(i + 4) * a.L + e], s1);
+          s2 = fma(ys[i + 8], Q[(int64_t)(i + 8) * a.L + e], s2);
+          s3 = fma(ys[i + 12], Q[(int64_t)(i + 12) * a.L + e], s3);
+        }
+        for (; i < m1; i += 4) s0 = fma(ys[i], Q[(int64_t)i * a.L + e], s0);
       }
-      for (; i < m1; i += 4) s0 = fma(ys[i], Q[(int64_t)i * a.L + e], s0);
-      s0 += s2;
-      s1 += s3;
+      red[sl][el] = (s0 + s2) + (s1 + s3);
+      __syncthreads();
+      if (sl == 0) xs[t][el] = (red[0][el] + red[1][el]) + (red[2][el] + red[3][el]);
+      __syncthreads();
     }
-    red[sl][el] = s0 + s1;
-    __syncthreads();
-    if (sl == 0 && e < a.L) a.Xin[(int64_t)slot * a.L + e] = (red[0][el] + red[1][el]) + (red[2][el] + red[3][el]);
-    __syncthreads();
-  }
-}
-
-template <int K>
-__global__ void __launch_bounds__(128) k_xupd(EngArgs a) {
-  const int slot = blockIdx.y;
-  if (a.phase[slot] != PH_XUPD) return;
-  const int64_t rep = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (rep >= a.nrep) return;
-  const int64_t c = rep_coord(rep, a.npairs);
-  const bool pair = rep < a.npairs;
-  const double* sv = a.Xin + (int64_t)slot * a.L + c;
-  cplx r[K], z[K];
+    if (su > 0) {  // recycled directions enter x directly (not through P^{-1})
+      const double* U = a.Ureg + (int64_t)a.reg[slot] * a.s_rec * a.L;
+      for (int idx = threadIdx.x; idx < K * 64; idx += blockDim.x) {
+        const int64_t cc = c0 + (idx & 63);
+        if (cc >= a.npad) continue;
+        const int64_t e = (int64_t)(idx >> 6) * a.npad + cc;
+        double acc = 0.0;
+        for (int i = 0; i < su; ++i) acc = fma(ysl[i], U[(int64_t)i * a.L + e], acc);
+        X[e] += acc;
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x < 64) {
+      const int64_t cc = c0 + threadIdx.x;
+      const bool pair = cc < 2 * a.npairs;
+      const int64_t rep = pair ? cc / 2 : cc - a.npairs;
+      if (!(pair && (cc & 1)) && rep < a.nrep) {
+        cplx r[K], z[K];
 #pragma unroll
-  for (int t = 0; t < K; ++t) r[t] = mk(sv[t * a.npad], pair ? sv[t * a.npad + 1] : 0.0);
-  apply_minv<K>(a.Minv + (((int64_t)slot * a.nrep + rep) * K * K) * 2, r, z);
-  double* X = a.X + (int64_t)slot * a.L + c;
+        for (int t = 0; t < K; ++t) r[t] = mk(xs[t][threadIdx.x], pair ? xs[t][threadIdx.x + 1] : 0.0);
+        apply_minv<K>(a.Minv + (((int64_t)slot * a.nrep + rep) * K * K) * 2, r, z);
 #pragma unroll
-  for (int t = 0; t < K; ++t) {
-    X[t * a.npad] += z[t].re;
-    if (pair) X[t * a.npad + 1] += z[t].im;
+        for (int t = 0; t < K; ++t) {
+          X[(int64_t)t * a.npad + cc] += z[t].re;
+          if (pair) X[(int64_t)t * a.npad + cc + 1] += z[t].im;
+        }
+      }
+    }
+    __syncthreads();
   }
 }
 
 }  // namespace lyap
+

@@ -383,7 +383,7 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
     const int bg = gb[gi];
     const dim3 grep((unsigned)((s.nrep + 127) / 128), (unsigned)bg);
     const dim3 gred((unsigned)g.nchunk, (unsigned)bg);
-    const dim3 gxc((unsigned)std::min<int64_t>((g.L + 63) / 64, 128), (unsigned)bg);
+    const dim3 gxc((unsigned)std::min<int64_t>((s.npad + 63) / 64, 128), (unsigned)bg);
     k_assign<<<1, (int)roundup(bg, 32), 0, sg>>>(x);
     LAUNCHED();
     K_DISPATCH(s.k, (k_prec<KK><<<grep, 128, 0, sg>>>(x)));
@@ -405,9 +405,7 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
       k_gout<<<dim3((unsigned)std::min<int64_t>((g.L + 255) / 256, 64), (unsigned)bg), 256, 0, sg>>>(x);
       LAUNCHED();
     }
-    k_xcomb<<<gxc, 256, 0, sg>>>(x);
-    LAUNCHED();
-    K_DISPATCH(s.k, (k_xupd<KK><<<grep, 128, 0, sg>>>(x)));
+    K_DISPATCH(s.k, (k_xcomb<KK><<<gxc, 256, 0, sg>>>(x)));
     LAUNCHED();
     return ctx->stats.kernel_launches - l0;
   };
