@@ -332,7 +332,10 @@ __global__ void __launch_bounds__(256) k_uapply(EngArgs a) {
 // k_dots, ITER: part[slot][i][chunk] = q^_i . w  (i <= m) and part2[slot][i][chunk] = q^_i . q^_m
 // (i < m), w = the candidate q^_{m+1} written by K1's epilogue.
 // VERIFY: part3[slot][chunk] = (||R||^2, ||rhs||^2, <hf, X>) with R in q^_0.
-constexpr int DOT_IG = 64;  // basis vectors per k_dots block (grid.z splits long cycles)
+#ifndef LYAP_DOT_IG
+#define LYAP_DOT_IG 64
+#endif
+constexpr int DOT_IG = LYAP_DOT_IG;  // basis vectors per k_dots block (grid.z splits long cycles)
 __global__ void __launch_bounds__(256) k_dots(EngArgs a) {
   __shared__ double ws[RED_CE];
   __shared__ double qm[RED_CE];
@@ -478,6 +481,9 @@ __global__ void __launch_bounds__(256) k_gram(EngArgs a) {
 }
 
 // k_upd: w' = w - sum_i cf_i q^_i (one read of the basis); part3[slot][chunk][0] = ||w'||^2.
+#ifndef LYAP_UPD_UNROLL
+#define LYAP_UPD_UNROLL 8
+#endif
 __global__ void __launch_bounds__(256) k_upd(EngArgs a) {
   extern __shared__ double cfs[];  // mmax + 1
   __shared__ double red[8];
@@ -503,17 +509,18 @@ __global__ void __launch_bounds__(256) k_upd(EngArgs a) {
   }
   // 8 basis vectors per round: 8 * EPT independent loads in flight per thread (the chain over the
   // basis, not bandwidth, bounds the slot with the longest cycle otherwise)
+  constexpr int UU = LYAP_UPD_UNROLL;
   int i = 0;
-  for (; i + 8 <= m + 1; i += 8) {
-    double v[8][EPT];
+  for (; i + UU <= m + 1; i += UU) {
+    double v[UU][EPT];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < UU; ++u) {
       const double* q = Q + (int64_t)(i + u) * a.L;
 #pragma unroll
       for (int r = 0; r < EPT; ++r) v[u][r] = ok[r] ? q[eo[r]] : 0.0;
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < UU; ++u) {
       const double c = cfs[i + u];
 #pragma unroll
       for (int r = 0; r < EPT; ++r) acc[r] = fma(c, v[u][r], acc[r]);

@@ -15,6 +15,8 @@
 namespace lyap {
 
 constexpr int K1_TILE_C = 32;  // coordinates per prologue / epilogue tile
+constexpr int K1_THREADS = 256;  // prologue / epilogue block size: compile-time strides let the
+                                 // staging loops unroll, so each thread's loads are in flight together
 
 template <int K>
 struct K1Tile {
@@ -56,13 +58,16 @@ __global__ void __launch_bounds__(256) k1_gen(K1Args a, const double* __restrict
   if (s0 >= nact) return;
   __shared__ double xs[TS][K][TC];
   __shared__ double bs[TC][K];
-  for (int idx = threadIdx.x; idx < TS * K * TC; idx += blockDim.x) {
+#pragma unroll
+  for (int idx = threadIdx.x; idx < TS * K * TC; idx += K1_THREADS) {
     int sl = idx / (K * TC), t = (idx / TC) % K, c = idx % TC;
     xs[sl][t][c] = (s0 + sl < nact) ? a.Xin[(int64_t)k1_slot(a, s0 + sl) * a.L + (int64_t)t * npad + i0 + c] : 0.0;
   }
-  for (int idx = threadIdx.x; idx < TC * K; idx += blockDim.x) bs[idx / K][idx % K] = bhr[(int64_t)i0 * K + idx];
+#pragma unroll
+  for (int idx = threadIdx.x; idx < TC * K; idx += K1_THREADS) bs[idx / K][idx % K] = bhr[(int64_t)i0 * K + idx];
   __syncthreads();
-  for (int idx = threadIdx.x; idx < TC * NC; idx += blockDim.x) {
+#pragma unroll
+  for (int idx = threadIdx.x; idx < TC * NC; idx += K1_THREADS) {
     int r = idx / NC, col = idx % NC;
     int sl = col / (K * K), s = (col / K) % K, t = col % K;
     if (s0 + sl >= nact) continue;
@@ -200,16 +205,18 @@ __global__ void __launch_bounds__(256) k1_epi(K1Args a, const double* __restrict
   if (s0 >= nact) return;
   __shared__ double us[TC][NC + 1];
   __shared__ double xs[TS][K][TC];
-  for (int idx = threadIdx.x; idx < TC * NC; idx += blockDim.x) {
+#pragma unroll
+  for (int idx = threadIdx.x; idx < TC * NC; idx += K1_THREADS) {
     int r = idx / NC, col = idx % NC;
     us[r][col] = (s0 + col / (K * K) < nact) ? U[(int64_t)(i0 + r) * ncol + (int64_t)s0 * K * K + col] : 0.0;
   }
-  for (int idx = threadIdx.x; idx < TS * K * TC; idx += blockDim.x) {
+#pragma unroll
+  for (int idx = threadIdx.x; idx < TS * K * TC; idx += K1_THREADS) {
     int sl = idx / (K * TC), t = (idx / TC) % K, c = idx % TC;
     xs[sl][t][c] = (s0 + sl < nact) ? a.Xin[(int64_t)k1_slot(a, s0 + sl) * a.L + (int64_t)t * npad + i0 + c] : 0.0;
   }
   __syncthreads();
-  for (int idx = threadIdx.x; idx < TS * K * TC; idx += blockDim.x) {
+  for (int idx = threadIdx.x; idx < TS * K * TC; idx += K1_THREADS) {
     int sl = idx / (K * TC), s = (idx / TC) % K, r = idx % TC;
     if (s0 + sl >= nact) continue;
     const int slot = k1_slot(a, s0 + sl);

@@ -211,7 +211,7 @@ void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, cudaEvent_t evb 
   const int two_np = (int)(2 * s.npairs);
   K_DISPATCH(s.k, {
     dim3 grid((unsigned)(s.npad / K1_TILE_C), (unsigned)((a.nslot + K1Tile<KK>::TS - 1) / K1Tile<KK>::TS));
-    k1_gen<KK><<<grid, 256, 0, st>>>(a, s.bhr, (int)s.npad, two_np, g.Bop, g.ncol);
+    k1_gen<KK><<<grid, K1_THREADS, 0, st>>>(a, s.bhr, (int)s.npad, two_np, g.Bop, g.ncol);
   });
   LAUNCHED();
   {
@@ -231,7 +231,7 @@ void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, cudaEvent_t evb 
   }
   K_DISPATCH(s.k, {
     dim3 grid((unsigned)(s.npad / K1_TILE_C), (unsigned)((a.nslot + K1Tile<KK>::TS - 1) / K1Tile<KK>::TS));
-    k1_epi<KK><<<grid, 256, 0, st>>>(a, g.U, g.ncol, s.btl, s.F, s.g0, (int)s.npad, two_np, (int)s.npairs,
+    k1_epi<KK><<<grid, K1_THREADS, 0, st>>>(a, g.U, g.ncol, s.btl, s.F, s.g0, (int)s.npad, two_np, (int)s.npairs,
                                      (int)s.n);
   });
   LAUNCHED();
