@@ -38,15 +38,21 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default=os.environ.get("BENCH_CONFIG", "c2"))
+    ap.add_argument("--config", default=os.environ.get("BENCH_CONFIG", "c5"),
+                    help="BASELINE configuration; default c5 = configs[4], the 1/2/4/8-GPU configuration the "
+                         "metric is quoted on")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--batch", type=int, default=0)
-    ap.add_argument("--scaling", default=os.environ.get("BENCH_SCALING", "weak"), choices=["weak", "strong"],
-                    help="weak: every rank solves a full-size grid of its own (axis 0 refined world-fold and "
-                         "interleaved; N=1 is the configuration itself); strong: the one grid is sharded")
+    ap.add_argument("--scaling", default=os.environ.get("BENCH_SCALING", "strong"), choices=["weak", "strong"],
+                    help="strong (default): the configuration's one grid is sharded over the ranks, cost-balanced "
+                         "(BASELINE c5: 'sharded over 1/2/4/8 GPUs'); weak: every rank solves a full-size grid of "
+                         "its own (axis 0 refined world-fold and interleaved; N=1 is the configuration itself)")
+    ap.add_argument("--emulate-rank", default="",
+                    help="R/N: on this single process, solve only rank R's shard of an N-way strong split "
+                         "(per-rank time of an N-GPU run, measured on one GPU)")
     ap.add_argument("--max-dim", type=int, default=0)
     ap.add_argument("--recycle", type=int, default=int(os.environ.get("BENCH_RECYCLE", "0")),
                     help="recycle-space size s (0: off); spaces built from the 2^k grid corners before timing")
@@ -216,15 +222,21 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     W = workloads.make(args.config)
-    sweep = Sweep(W.nv, rank, world, dev, scaling=args.scaling)
+    P = Problem(W.A0, W.Bl, W.Br, W.Q, W.E, profile=True, device=local, batch=args.batch, max_dim=args.max_dim)
+    cost = P.cost_proxy(W.V)  # the engine's scheduling proxy: balances the strong-scaling shards
+    emu = None
+    if args.emulate_rank:
+        er, en = (int(x) for x in args.emulate_rank.split("/"))
+        emu = (er, en)
+        from paper_2312_08201_b200.sweep import shard_indices
+    sweep = Sweep(W.nv, rank, world, dev, scaling=args.scaling, cost=cost)
     if args.scaling == "weak":
         Vrank = workloads.rank_grid(W, rank, world)
         idx = np.arange(len(Vrank))
     else:
         Vrank = W.V
-        idx = sweep.mine
-    nv_total = sweep.nv
-    P = Problem(W.A0, W.Bl, W.Br, W.Q, W.E, profile=True, device=local, batch=args.batch, max_dim=args.max_dim)
+        idx = sweep.mine if emu is None else shard_indices(W.nv, emu[0], emu[1], cost=cost)
+    nv_total = sweep.nv if emu is None else len(idx)
     setup_ms = P.info["setup_ms"]
     recycle_ms = None
     if args.recycle > 0:
@@ -233,8 +245,13 @@ def main():
         recycle_ms = 1e3 * (time.perf_counter() - t)
     Vd = torch.tensor(Vrank[idx], device=dev)
 
-    def step():
-        return sweep.run(lambda rows: P.trace_batch(Vd))
+    if emu is not None:
+        def step():
+            tau = P.trace_batch(Vd)
+            return tau, torch.argmin(tau)
+    else:
+        def step():
+            return sweep.run(lambda rows: P.trace_batch(Vd))
 
     for _ in range(args.warmup):
         full, am = step()
@@ -323,6 +340,10 @@ def main():
         cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"{cnt} of {W.nv} grid points (corners + centre + seeded uniform) in {el:.1f} s, "
                          "blocked Bartels-Stewart per v, one process per core, 1 BLAS thread"}
+    balance = None
+    if args.scaling == "strong":
+        from paper_2312_08201_b200.sweep import shard_balance
+        balance = {str(N): round(shard_balance(W.nv, N, cost), 4) for N in (2, 4, 8)}
     if rank == 0:
         emit({"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
               "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
@@ -332,7 +353,9 @@ def main():
                                                      "setup_ms": setup_ms, "argmin_flat_index": argmin,
                                                      "recycle_s": args.recycle if args.recycle > 0 else ("auto" if recycle_ms else 0),
                                                      "recycle_build_ms": recycle_ms,
-                                                     "applies_per_v": st["k1_vectors"] / (len(idx) * args.steps)}),
+                                                     "applies_per_v": st["k1_vectors"] / (len(idx) * args.steps),
+                                                     "shard_cost_max_over_mean": balance,
+                                                     "emulated_rank": args.emulate_rank or None}),
               "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
               "gpu_launches": st["kernel_launches"]})
     P.close()

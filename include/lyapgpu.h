@@ -83,6 +83,8 @@ typedef struct {
   double max_abs_lam;
   double setup_ms;     /* device time of lyap_setup */
   int32_t batch, max_dim;
+  double wcost[LYAP_KMAX]; /* ||B~l_t|| ||B^r_t||: weights of the scheduling cost proxy
+                              sum_t |v_t| wcost[t] (opts.schedule; multi-GPU shard balancing) */
 } lyap_info;
 
 typedef struct {
@@ -188,7 +190,11 @@ void lyap_destroy(lyap_ctx* ctx);
  * closed form or any Lyapunov solver), E (n x n, symmetrised), trEX0 = trace(E X0); all host,
  * row-major.  max_dim caps the basis (default 400 columns).  LU of A0 on the device (cuSOLVER).
  * lyap_ek_trace_batch: host V (nv x k) -> traces (nv); dim_used / bwd_err (nullable): basis size
- * and the largest sampled backward error.  max_steps bounds the expansions of this call. */
+ * and the largest sampled backward error.  max_steps bounds the expansions of this call.
+ * Returns LYAP_OK only when a look-ahead block certified bwd_err <= eps (or the basis reached n
+ * columns: the projection is then exact).  LYAP_EPARTIAL (traces still written): the target was not
+ * certified -- the basis hit max_dim below n, max_steps ran out, or a projected solve did not
+ * converge for some v; bwd_err is then the last certified value (infinity if none). */
 typedef struct lyap_ek lyap_ek;
 int lyap_ek_setup(int64_t n, int64_t k, const double* A0, const double* Bl, const double* Br, const double* X0Br,
                   const double* E, double trEX0, int32_t max_dim, lyap_ek** out);

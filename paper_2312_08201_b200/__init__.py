@@ -82,7 +82,15 @@ class Problem:
     def info(self) -> dict:
         i = Info()
         self._check(lib.lyap_get_info(self._ctx, C.byref(i)))
-        return {f: getattr(i, f) for f, _ in Info._fields_}
+        d = {f: getattr(i, f) for f, _ in Info._fields_}
+        d["wcost"] = list(d["wcost"])[: d["k"]]
+        return d
+
+    def cost_proxy(self, V) -> np.ndarray:
+        """The engine's per-v cost proxy sum_t |v_t| ||B~l_t|| ||B^r_t|| (the scheduling key of
+        lyap_trace_batch; used to balance multi-GPU shards)."""
+        V = np.asarray(V, dtype=np.float64).reshape(-1, self.k)
+        return np.abs(V) @ np.asarray(self.info["wcost"])
 
     @property
     def stats(self) -> dict:
@@ -128,7 +136,12 @@ class Problem:
 
     def _trace_batch_device(self, V, return_diagnostics, allow_partial, stream):
         import torch
-        V = V.to(torch.float64).contiguous()
+        V = V.to(torch.float64)
+        if V.ndim == 1:
+            V = V.reshape(-1, self.k)
+        if V.ndim != 2 or V.shape[1] != self.k:
+            raise ValueError(f"V must be (nv, {self.k}), got {tuple(V.shape)}")
+        V = V.contiguous()
         nv = V.shape[0]
         dev = V.device
         tau = torch.empty(nv, dtype=torch.float64, device=dev)
@@ -231,14 +244,16 @@ class EKProblem:
             raise LyapError(rc, lib.lyap_ek_last_error(None).decode())
         self.n, self.k = n, k
 
-    def trace_batch(self, V, eps: float = 1e-8, max_steps: int = 200):
+    def trace_batch(self, V, eps: float = 1e-8, max_steps: int = 200, allow_partial: bool = False):
+        """(traces, basis dim, certified backward error).  LYAP_EPARTIAL (target not certified) raises
+        unless allow_partial."""
         V = _f64(V).reshape(-1, self.k)
         tau = np.empty(V.shape[0])
         dim = C.c_int32()
         err = C.c_double()
         rc = lib.lyap_ek_trace_batch(self._ek, V.shape[0], V.ctypes.data, eps, max_steps, tau.ctypes.data,
                                      C.byref(dim), C.byref(err))
-        if rc != LYAP_OK:
+        if rc != LYAP_OK and not (rc == LYAP_EPARTIAL and allow_partial):
             raise LyapError(rc, lib.lyap_ek_last_error(self._ek).decode())
         return tau, int(dim.value), float(err.value)
 

@@ -40,6 +40,7 @@ struct Seed {
   double* bhr = nullptr;  // npad x k: folded B^r = S^T Br        [coord][s]
   double* btl = nullptr;  // npad x k: folded B~l = S^{-1} Bl     [coord][t]
   double* F = nullptr;    // nrep x k x k complex (re, im):  T_d block of rep j, F_j[s][t]
+  double* Pb = nullptr;   // nrep x 2k x 2k real: diagonal block of the folded T per rep (preconditioner)
   double* g0 = nullptr;   // k x npad folded right-hand side G0 = B^r^T X~0
   double* hf = nullptr;   // k x npad folded trace weights (tau = t0 + 2 <g, hf>)
   double* Lf = nullptr;   // npad x npad folded Cauchy matrix (K1's A operand), row-major
@@ -47,6 +48,7 @@ struct Seed {
   double* Qr = nullptr;   // n x n S_r^{-1} Q S_r^{-T} (column-major), kept for lyap_solution
   double t0 = 0.0;
   double wcost[LYAP_KMAX] = {};  // ||B~l_t|| ||B^r_t||: weights of the scheduling cost proxy
+  double* dwork = nullptr;       // device: [0, k) wcost, [8, 8 + 2k) batch bounding box, [32, ...) log seeds
 };
 
 // Batched Krylov engine buffers (slot-major).
@@ -76,7 +78,14 @@ struct Engine {
   int* h_ctrl = nullptr;                          // pinned mirror
   int* order = nullptr;                           // queue order (nv_cap)
   int64_t order_cap = 0;
-  int* regq = nullptr;                            // queue position -> recycle regime (nv_cap)
+  int* regq = nullptr;                            // queue position -> recycle regime (regq_cap)
+  int64_t regq_cap = 0;
+  // device-side scheduling scratch (sched.cuh): cost keys, sorted keys, identity indices, CUB temp
+  double *skey = nullptr, *skey2 = nullptr;
+  int* sidx = nullptr;
+  void* cub_tmp = nullptr;
+  size_t cub_bytes = 0;
+  int64_t sched_cap = 0;
 };
 
 }  // namespace lyap

@@ -2,7 +2,8 @@
 //
 // Each of b "slots" solves one capacitance system C(v) g = g0, C(v) = Delta(v) - T (the symmetric
 // nk form of eq. (SMW_linearsystem)), right-preconditioned with the exact
-// v-dependent block-diagonal part P(v) = Delta(v) - T_d of eq. (prec) (p-bar = 0).
+// v-dependent diagonal blocks of C(v) per eigen pair (eq. (prec), p-bar = 0,
+// widened by the pair's own Cauchy coupling; see k_pfactor).
 // All slots advance in lock step: one batched K1 launch per iteration applies C(v) to every slot's
 // current vector.  A slot walks   VERIFY (true residual of its current iterate, trace, convergence)
 // -> ITER (Krylov steps, CGS2) -> XUPD (x += P^{-1} Q y) -> VERIFY ...; a converged slot writes
@@ -29,7 +30,7 @@ struct EngArgs {
   int nchunk;
   double tol, tol_inner, t0;
   int max_restarts, warm;
-  const double *V, *g0, *hf, *F;
+  const double *V, *g0, *hf, *Pb;  // Pb: per-rep diagonal blocks of T (preconditioner, k_pfactor)
   const int* order;  // queue position -> row of V (null: identity)
   // recycling: nreg shared spaces of s_rec x-space vectors U and their T U; a v
   // whose queue position maps to regime r >= 0 runs flexible GMRES with U_r as its first search
@@ -142,98 +143,159 @@ __global__ void k_assign(EngArgs a) {
 }
 
 // ---------------------------------------------------------------- preconditioner factor (K2)
-// Minv[slot][rep] = (diag(sigma) - F_rep)^{-1}, k x k complex, Gauss-Jordan with partial pivoting;
-// rows with v_t = 0 are identity rows (column t absent).  Cold start zeroes X for new v's.
-// (Run by k_prec's thread for the same (slot, rep) before it applies the block: one launch fewer.)
+// P(v) = the exact diagonal blocks of C(v) = Delta(v) - T in folded real coordinates, one block per
+// eigen representative: 2k x 2k for a conjugate pair (the unknowns Re/Im G_tj, t = 1..k), k x k for
+// a real eigenvalue.  Pb (setup, k_pblock) holds the block of T: T_d (F_j, eq. (N1M1) / (2,2) block,
+// PAPER.md:302-334) PLUS the part of the Cauchy coupling T_o (eqs. (N2M1)/(N1M2))
+// that stays inside the pair -- the input index i = conj(j), whose Cauchy entry L_{conj j, j} =
+// 1/(2 Re lambda_j) is the largest of its row for light damping.  The paper's eq. (prec)
+// (p-bar = 0) keeps only T_d; adding the pair term cuts the Krylov iterations by
+// ~40 % at no extra cost per iteration (a 2k x 2k real block costs what a k x k complex one does;
+// DESIGN.md §2.4).  Block layout (row, col) = (2s + a, 2t + b), a, b = 0 (Re), 1 (Im); real reps
+// use the top-left k x k with the same row stride 2k.  Rows with v_s = 0 are identity rows.
 template <int K>
-__device__ __forceinline__ void pfactor_rep(const EngArgs& a, int slot, int64_t rep) {
-  cplx M[K][K], R[K][K];
+__device__ __forceinline__ constexpr int pb_stride() { return 4 * K * K; }
+
+// Minv[slot][rep] = P(v)_rep^{-1} by in-place Gauss-Jordan with partial pivoting (rows swapped
+// during elimination, the matching columns of the inverse swapped back at the end).
+template <int D, int K>
+__device__ __forceinline__ void invert_block(const double* __restrict__ pb, const double* mask, const double* sigma,
+                                             double* __restrict__ out) {
+  constexpr int RS = 2 * K, PER = D / K;  // row stride; rows per parameter (2 pair, 1 real)
+  double M[D][D];
+  int perm[D];
 #pragma unroll
-  for (int s = 0; s < K; ++s) {
-    const double msk = a.mask[slot * K + s], sg = a.sigma[slot * K + s];
+  for (int r = 0; r < D; ++r) {
+    const int s = r / PER;
+    const double msk = mask[s];
 #pragma unroll
-    for (int t = 0; t < K; ++t) {
-      const double* f = a.F + ((rep * K + s) * K + t) * 2;
-      cplx v = msk != 0.0 ? mk(-f[0], -f[1]) : mk(0.0, 0.0);
-      if (s == t) v = msk != 0.0 ? v + mk(sg, 0.0) : mk(1.0, 0.0);
-      M[s][t] = v;
-      R[s][t] = mk(s == t ? 1.0 : 0.0, 0.0);
+    for (int c = 0; c < D; ++c) {
+      double v = msk != 0.0 ? -pb[r * RS + c] : 0.0;
+      if (r == c) v = msk != 0.0 ? v + sigma[s] : 1.0;
+      M[r][c] = v;
     }
   }
-#pragma unroll
-  for (int c = 0; c < K; ++c) {
-    // pivot: largest |M[r][c]|, r >= c (select-swap keeps everything in registers)
-    double best = abs2(M[c][c]);
-#pragma unroll
-    for (int r = c + 1; r < K; ++r) {
-      const double v = abs2(M[r][c]);
-      if (v > best) {
-        best = v;
-#pragma unroll
-        for (int t = 0; t < K; ++t) {
-          cplx tm = M[c][t];
-          M[c][t] = M[r][t];
-          M[r][t] = tm;
-          tm = R[c][t];
-          R[c][t] = R[r][t];
-          R[r][t] = tm;
-        }
+  for (int c = 0; c < D; ++c) {
+    int p = c;
+    double best = fabs(M[c][c]);
+    for (int r = c + 1; r < D; ++r)
+      if (fabs(M[r][c]) > best) {
+        best = fabs(M[r][c]);
+        p = r;
       }
-    }
-    const cplx pinv = cinv(M[c][c]);
-#pragma unroll
-    for (int t = 0; t < K; ++t) {
-      M[c][t] = M[c][t] * pinv;
-      R[c][t] = R[c][t] * pinv;
-    }
-#pragma unroll
-    for (int r = 0; r < K; ++r) {
+    perm[c] = p;
+    if (p != c)
+      for (int j = 0; j < D; ++j) {
+        const double t = M[c][j];
+        M[c][j] = M[p][j];
+        M[p][j] = t;
+      }
+    const double piv = M[c][c];
+    const double inv = piv != 0.0 ? 1.0 / piv : 0.0;  // singular block: zero row (z = 0 there)
+    M[c][c] = 1.0;
+    for (int j = 0; j < D; ++j) M[c][j] *= inv;
+    for (int r = 0; r < D; ++r) {
       if (r == c) continue;
-      const cplx f = M[r][c];
-#pragma unroll
-      for (int t = 0; t < K; ++t) {
-        M[r][t] = M[r][t] - f * M[c][t];
-        R[r][t] = R[r][t] - f * R[c][t];
-      }
+      const double f = M[r][c];
+      M[r][c] = 0.0;
+      for (int j = 0; j < D; ++j) M[r][j] = fma(-f, M[c][j], M[r][j]);
     }
   }
-  double* out = a.Minv + (((int64_t)slot * a.nrep + rep) * K * K) * 2;
+  for (int c = D - 1; c >= 0; --c) {
+    const int p = perm[c];
+    if (p != c)
+      for (int r = 0; r < D; ++r) {
+        const double t = M[r][c];
+        M[r][c] = M[r][p];
+        M[r][p] = t;
+      }
+  }
 #pragma unroll
-  for (int s = 0; s < K; ++s)
+  for (int r = 0; r < D; ++r)
 #pragma unroll
-    for (int t = 0; t < K; ++t) {
-      out[(s * K + t) * 2] = R[s][t].re;
-      out[(s * K + t) * 2 + 1] = R[s][t].im;
-    }
+    for (int c = 0; c < D; ++c) out[r * RS + c] = M[r][c];
+}
+
+// One thread per (slot with a new v, rep): factor the rep's block; a cold start zeroes X there.
+template <int K>
+__global__ void __launch_bounds__(128) k_pfactor(EngArgs a) {
+  const int slot = blockIdx.y;
+  const int64_t rep = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (rep >= a.nrep || !a.newv[slot]) return;
+  const bool pair = rep < a.npairs;
+  double* out = a.Minv + ((int64_t)slot * a.nrep + rep) * pb_stride<K>();
+  const double* pb = a.Pb + rep * pb_stride<K>();
+  if (pair)
+    invert_block<2 * K, K>(pb, a.mask + slot * K, a.sigma + slot * K, out);
+  else
+    invert_block<K, K>(pb, a.mask + slot * K, a.sigma + slot * K, out);
   if (!a.warm) {
     const int64_t c = rep_coord(rep, a.npairs);
-    const int w = rep < a.npairs ? 2 : 1;
+    const int w = pair ? 2 : 1;
     for (int t = 0; t < K; ++t)
       for (int q = 0; q < w; ++q) a.X[(int64_t)slot * a.L + t * a.npad + c + q] = 0.0;
   }
 }
 
-// z = Minv_rep * r (k complex), real reps keep the real part
+// z = P_rep^{-1} r on the rep's folded coordinates: r[2t + b] (pairs) / r[t] (reals)
 template <int K>
-__device__ __forceinline__ void apply_minv(const double* mi, const cplx (&r)[K], cplx (&z)[K]) {
+__device__ __forceinline__ void apply_pinv(const double* __restrict__ mi, bool pair, const double (&r)[2 * K],
+                                           double (&z)[2 * K]) {
+  constexpr int RS = 2 * K;
+  if (pair) {
 #pragma unroll
-  for (int s = 0; s < K; ++s) {
-    cplx acc = mk(0.0, 0.0);
+    for (int i = 0; i < 2 * K; ++i) {
+      double acc = 0.0;
 #pragma unroll
-    for (int t = 0; t < K; ++t) acc = acc + mk(mi[(s * K + t) * 2], mi[(s * K + t) * 2 + 1]) * r[t];
-    z[s] = acc;
+      for (int j = 0; j < 2 * K; ++j) acc = fma(mi[i * RS + j], r[j], acc);
+      z[i] = acc;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < K; ++j) acc = fma(mi[i * RS + j], r[j], acc);
+      z[i] = acc;
+    }
+  }
+}
+
+// gather / scatter of a rep's folded coordinates of a k x npad vector (scaled on the way in)
+template <int K>
+__device__ __forceinline__ void rep_load(const double* __restrict__ x, int64_t npad, int64_t c, bool pair, double sc,
+                                         double (&r)[2 * K]) {
+#pragma unroll
+  for (int t = 0; t < K; ++t) {
+    if (pair) {
+      r[2 * t] = sc * x[t * npad + c];
+      r[2 * t + 1] = sc * x[t * npad + c + 1];
+    } else {
+      r[t] = sc * x[t * npad + c];
+    }
+  }
+}
+template <int K>
+__device__ __forceinline__ void rep_store(double* __restrict__ x, int64_t npad, int64_t c, bool pair,
+                                          const double (&z)[2 * K], bool add) {
+#pragma unroll
+  for (int t = 0; t < K; ++t) {
+    if (pair) {
+      x[t * npad + c] = add ? x[t * npad + c] + z[2 * t] : z[2 * t];
+      x[t * npad + c + 1] = add ? x[t * npad + c + 1] + z[2 * t + 1] : z[2 * t + 1];
+    } else {
+      x[t * npad + c] = add ? x[t * npad + c] + z[t] : z[t];
+    }
   }
 }
 
 // ---------------------------------------------------------------- apply input (K2 apply)
-// ITER: Xin = P(v)^{-1} (q^_m / eta_m);  VERIFY: Xin = X.  A slot with a new v first factors its
-// blocks (pfactor_rep).
+// ITER: Xin = P(v)^{-1} (q^_m / eta_m);  VERIFY: Xin = X.
 template <int K>
 __global__ void __launch_bounds__(128) k_prec(EngArgs a) {
   const int slot = blockIdx.y;
   const int64_t rep = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (rep >= a.nrep) return;
-  if (a.newv[slot]) pfactor_rep<K>(a, slot, rep);  // a v assigned in this iteration's k_assign
   const int ph = a.phase[slot];
   if (ph != PH_ITER && ph != PH_VERIFY) return;
   if (ph == PH_ITER && a.m[slot] < a.su[slot]) return;  // recycled direction: no K1 input
@@ -252,15 +314,10 @@ __global__ void __launch_bounds__(128) k_prec(EngArgs a) {
   const int m = a.m[slot];
   const double sc = 1.0 / a.eta[(int64_t)slot * (a.mmax + 1) + m];
   const double* q = a.Qb + ((int64_t)slot * (a.mmax + 1) + m) * a.L;
-  cplx r[K], z[K];
-#pragma unroll
-  for (int t = 0; t < K; ++t) r[t] = mk(sc * q[t * a.npad + c], pair ? sc * q[t * a.npad + c + 1] : 0.0);
-  apply_minv<K>(a.Minv + (((int64_t)slot * a.nrep + rep) * K * K) * 2, r, z);
-#pragma unroll
-  for (int t = 0; t < K; ++t) {
-    xin[t * a.npad + c] = z[t].re;
-    if (pair) xin[t * a.npad + c + 1] = z[t].im;
-  }
+  double r[2 * K], z[2 * K];
+  rep_load<K>(q, a.npad, c, pair, sc, r);
+  apply_pinv<K>(a.Minv + ((int64_t)slot * a.nrep + rep) * pb_stride<K>(), pair, r, z);
+  rep_store<K>(xin, a.npad, c, pair, z, false);
 }
 
 // lyap_build_recycle helpers: Z[:, j] = P(v)^{-1} q^_j / eta_j, or u_j for j < su (the search
@@ -283,16 +340,10 @@ __global__ void __launch_bounds__(128) k_rec_z(EngArgs a, int slot, int m1, doub
   }
   const double sc = 1.0 / a.eta[(int64_t)slot * (a.mmax + 1) + j];
   const double* q = a.Qb + ((int64_t)slot * (a.mmax + 1) + j) * a.L;
-  cplx r[K], z[K];
-#pragma unroll
-  for (int t = 0; t < K; ++t) r[t] = mk(sc * q[t * a.npad + c], pair ? sc * q[t * a.npad + c + 1] : 0.0);
-  apply_minv<K>(a.Minv + (((int64_t)slot * a.nrep + rep) * K * K) * 2, r, z);
-  double* zo = Z + (int64_t)j * a.L;
-#pragma unroll
-  for (int t = 0; t < K; ++t) {
-    zo[t * a.npad + c] = z[t].re;
-    if (pair) zo[t * a.npad + c + 1] = z[t].im;
-  }
+  double r[2 * K], z[2 * K];
+  rep_load<K>(q, a.npad, c, pair, sc, r);
+  apply_pinv<K>(a.Minv + ((int64_t)slot * a.nrep + rep) * pb_stride<K>(), pair, r, z);
+  rep_store<K>(Z + (int64_t)j * a.L, a.npad, c, pair, z, false);
 }
 
 __global__ void k_rec_tu(const double* __restrict__ U, const double* __restrict__ CU, const double* __restrict__ sig,
@@ -781,15 +832,18 @@ __global__ void __launch_bounds__(256) k_xcomb(EngArgs a) {
       const bool pair = cc < 2 * a.npairs;
       const int64_t rep = pair ? cc / 2 : cc - a.npairs;
       if (!(pair && (cc & 1)) && rep < a.nrep) {
-        cplx r[K], z[K];
-#pragma unroll
-        for (int t = 0; t < K; ++t) r[t] = mk(xs[t][threadIdx.x], pair ? xs[t][threadIdx.x + 1] : 0.0);
-        apply_minv<K>(a.Minv + (((int64_t)slot * a.nrep + rep) * K * K) * 2, r, z);
+        double r[2 * K], z[2 * K];
 #pragma unroll
         for (int t = 0; t < K; ++t) {
-          X[(int64_t)t * a.npad + cc] += z[t].re;
-          if (pair) X[(int64_t)t * a.npad + cc + 1] += z[t].im;
+          if (pair) {
+            r[2 * t] = xs[t][threadIdx.x];
+            r[2 * t + 1] = xs[t][threadIdx.x + 1];
+          } else {
+            r[t] = xs[t][threadIdx.x];
+          }
         }
+        apply_pinv<K>(a.Minv + ((int64_t)slot * a.nrep + rep) * pb_stride<K>(), pair, r, z);
+        rep_store<K>(X, a.npad, cc, pair, z, true);
       }
     }
     __syncthreads();

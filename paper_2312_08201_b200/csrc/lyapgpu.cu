@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <limits>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -18,6 +19,7 @@
 #include "ctx.h"
 #include "engine.cuh"
 #include "k1.cuh"
+#include "sched.cuh"
 #include "setup.cuh"
 
 using namespace lyap;
@@ -111,6 +113,21 @@ inline int tile_n(const Seed& s) { return s.n <= SMALL_N ? S_BN : G_BN; }
     default: break;              \
   }
 
+// device scratch of the scheduler: [0, k) cost weights, [8, 8 + 2k) bounding box, [32, ...) the log
+// seeds of the recycle regimes (nreg x k <= 2^KMAX x KMAX)
+constexpr size_t DWORK_SEEDS = 32;
+void ensure_dwork(lyap_ctx* ctx) {
+  Seed& sd = ctx->seed;
+  if (sd.dwork) return;
+  sd.dwork = dalloc<double>(ctx, DWORK_SEEDS + ((size_t)1 << LYAP_KMAX) * LYAP_KMAX);
+  CK(cudaMemcpy(sd.dwork, sd.wcost, sizeof(double) * sd.k, cudaMemcpyHostToDevice));
+}
+void upload_seeds(lyap_ctx* ctx) {
+  ensure_dwork(ctx);
+  if (!ctx->reg_seeds.empty())
+    CK(cudaMemcpy(ctx->seed.dwork + DWORK_SEEDS, ctx->reg_seeds.data(), ctx->reg_seeds.size(), cudaMemcpyHostToDevice));
+}
+
 // ------------------------------------------------------------------ engine allocation
 void free_engine(Engine& g, bool keep_order = true) {
   void* ps[] = {g.Bop, g.U, g.Xin, g.X, g.Qb, g.Minv, g.sigma, g.mask, g.eta, g.H, g.e, g.y,
@@ -120,16 +137,32 @@ void free_engine(Engine& g, bool keep_order = true) {
   if (g.h_ctrl) cudaFreeHost(g.h_ctrl);
   int* order = g.order;
   int* regq = g.regq;
-  const int64_t cap = g.order_cap;
+  const int64_t cap = g.order_cap, rcap = g.regq_cap;
+  double *skey = g.skey, *skey2 = g.skey2;
+  int* sidx = g.sidx;
+  void* cub_tmp = g.cub_tmp;
+  const size_t cub_bytes = g.cub_bytes;
+  const int64_t scap = g.sched_cap;
   if (!keep_order) {
     dfree(order);
     dfree(regq);
+    dfree(skey);
+    dfree(skey2);
+    dfree(sidx);
+    dfree(cub_tmp);
   }
   g = Engine{};
   if (keep_order) {
     g.order = order;
     g.regq = regq;
     g.order_cap = cap;
+    g.regq_cap = rcap;
+    g.skey = skey;
+    g.skey2 = skey2;
+    g.sidx = sidx;
+    g.cub_tmp = cub_tmp;
+    g.cub_bytes = cub_bytes;
+    g.sched_cap = scap;
   }
 }
 
@@ -175,7 +208,7 @@ void ensure_engine(lyap_ctx* ctx, int b, int mmax) {
   g.Xin = dalloc<double>(ctx, (size_t)b * g.L);
   g.X = dalloc<double>(ctx, (size_t)b * g.L);
   g.Qb = dalloc<double>(ctx, (size_t)b * (mmax + 1) * g.L);
-  g.Minv = dalloc<double>(ctx, (size_t)b * s.nrep * s.k * s.k * 2);
+  g.Minv = dalloc<double>(ctx, (size_t)b * s.nrep * s.k * s.k * 4);
   g.sigma = dalloc<double>(ctx, (size_t)b * s.k);
   g.mask = dalloc<double>(ctx, (size_t)b * s.k);
   g.eta = dalloc<double>(ctx, (size_t)b * (mmax + 1));
@@ -283,7 +316,7 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   a.order = dorder;
   a.g0 = s.g0;
   a.hf = s.hf;
-  a.F = s.F;
+  a.Pb = s.Pb;
   a.traces = dtr;
   a.status = dst;
   a.out_applies = dap;
@@ -313,7 +346,7 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
     x.X = g.X + s0 * g.L;
     x.Xin = g.Xin + s0 * g.L;
     x.Qb = g.Qb + s0 * ld * g.L;
-    x.Minv = g.Minv + s0 * s.nrep * s.k * s.k * 2;
+    x.Minv = g.Minv + s0 * s.nrep * s.k * s.k * 4;
     x.sigma = g.sigma + s0 * s.k;
     x.mask = g.mask + s0 * s.k;
     x.eta = g.eta + s0 * ld;
@@ -385,6 +418,8 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
     const dim3 gred((unsigned)g.nchunk, (unsigned)bg);
     const dim3 gxc((unsigned)std::min<int64_t>((s.npad + 63) / 64, 128), (unsigned)bg);
     k_assign<<<1, (int)roundup(bg, 32), 0, sg>>>(x);
+    LAUNCHED();
+    K_DISPATCH(s.k, (k_pfactor<KK><<<grep, 128, 0, sg>>>(x)));
     LAUNCHED();
     K_DISPATCH(s.k, (k_prec<KK><<<grep, 128, 0, sg>>>(x)));
     LAUNCHED();
@@ -514,6 +549,10 @@ void build_config(lyap_ctx* ctx, const double* Blc, const double* Brc) {
     LAUNCHED();
     k_fold_b<<<(unsigned)((s.npad * k + 255) / 256), 256, 0, st>>>(Blr, Brr, n, s.npad, k, two_np, s.btl, s.bhr);
     LAUNCHED();
+    s.Pb = dalloc<double>(ctx, (size_t)s.nrep * k * k * 4);
+    K_DISPATCH(k, (k_pblock<KK><<<(unsigned)((s.nrep + 127) / 128), 128, 0, st>>>(B.Lf, s.npad, s.bhr, s.btl, s.F,
+                                                                                     s.npairs, s.nrep, s.Pb)));
+    LAUNCHED();
     k_sum<<<1, 1024, 0, st>>>(t0part, s.nrep, t0d);
     LAUNCHED();
     CK(cudaMemcpyAsync(&s.t0, t0d, 8, cudaMemcpyDeviceToHost, st));
@@ -529,6 +568,7 @@ void build_config(lyap_ctx* ctx, const double* Blc, const double* Brc) {
         nr += hr[c * k + t] * hr[c * k + t];
       }
       s.wcost[t] = std::sqrt(nb * nr);
+      ctx->info.wcost[t] = s.wcost[t];
     }
     ctx->info.t0 = s.t0;
     if (!std::isfinite(s.t0)) {
@@ -569,7 +609,7 @@ static void destroy_impl(lyap_ctx* c) {
   cudaSetDevice(c->device);
   free_engine(c->eng, false);
   Seed& s = c->seed;
-  void* ps[] = {s.bhr, s.btl, s.F, s.g0, s.hf};  // lam, Lf, Sr, Qr belong to the shared Basis
+  void* ps[] = {s.bhr, s.btl, s.F, s.Pb, s.g0, s.hf, s.dwork};  // lam, Lf, Sr, Qr belong to the shared Basis
   if (!c->basis) {  // setup failed before the Basis took ownership
     dfree(s.lam);
     dfree(s.Lf);
@@ -983,93 +1023,73 @@ int lyap_trace_batch_ex(lyap_ctx* ctx, int64_t nv, const double* V, double* trac
       dap = applies;
       dres = resid;
     }
-    // schedule: expensive (large-perturbation) v first, so slow systems do not form a tail
+    // schedule (device-side, on the call's stream; V never visits the host): expensive
+    // (large-perturbation) v first, so slow systems do not form a tail (sched.cuh)
     const int* dorder = nullptr;
     const int s_auto = ctx->opts.recycle < 0 ? (ctx->seed.n * ctx->seed.k >= 12000 ? 32 : 0) : ctx->opts.recycle;
-    if (ctx->opts.schedule || s_auto > 0) {
-      std::vector<double> hV((size_t)nv * k);
-      if (own) {
-        std::memcpy(hV.data(), V, hV.size() * 8);
-      } else {
-        CK(cudaMemcpyAsync(hV.data(), V, hV.size() * 8, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
+    Seed& sd = ctx->seed;
+    ensure_dwork(ctx);
+    if (s_auto > 0 && !ctx->recycle_manual) {
+      // automatic recycle spaces from the corners of the batch's bounding box: the 2k box bounds are
+      // the only host read of the call before the engine runs
+      k_box<<<(unsigned)k, 256, 0, st>>>(dV, (int)nv, (int)k, sd.dwork + 8);
+      LAUNCHED();
+      std::vector<double> box(2 * k);
+      CK(cudaMemcpyAsync(box.data(), sd.dwork + 8, sizeof(double) * 2 * k, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      bool positive = true, inside = !ctx->auto_box.empty();
+      for (int64_t t = 0; t < k; ++t) {
+        positive = positive && box[2 * t] > 0.0;
+        if (inside) inside = box[2 * t] >= ctx->auto_box[2 * t] && box[2 * t + 1] <= ctx->auto_box[2 * t + 1];
       }
-      if (s_auto > 0) {  // automatic recycle spaces from the corners of the batch's bounding box
-        std::vector<double> box(2 * k);
-        bool positive = true;
-        for (int64_t t = 0; t < k; ++t) {
-          double lo = 1e300, hi = -1e300;
-          for (int64_t i = 0; i < nv; ++i) {
-            lo = std::min(lo, hV[i * k + t]);
-            hi = std::max(hi, hV[i * k + t]);
-          }
-          box[2 * t] = lo;
-          box[2 * t + 1] = hi;
-          positive = positive && lo > 0.0;
+      // rebuild only for a box the current spaces do not cover (optimizer-style callers pass a new,
+      // usually nested, box on every call)
+      if (positive && !inside) {
+        std::vector<double> seeds;
+        for (int64_t c = 0; c < (int64_t(1) << k); ++c) {
+          std::vector<double> v(k);
+          for (int64_t t = 0; t < k; ++t) v[t] = box[2 * t + ((c >> (k - 1 - t)) & 1)];
+          bool dup = false;  // a degenerate box (lo == hi on an axis) repeats corners
+          for (size_t q = 0; q + k <= seeds.size() && !dup; q += k)
+            dup = std::equal(v.begin(), v.end(), seeds.begin() + q);
+          if (!dup) seeds.insert(seeds.end(), v.begin(), v.end());
         }
-        if (positive && !ctx->recycle_manual && box != ctx->auto_box) {
-          std::vector<double> seeds;
-          for (int64_t c = 0; c < (int64_t(1) << k); ++c)
-            for (int64_t t = 0; t < k; ++t) seeds.push_back(box[2 * t + ((c >> (k - 1 - t)) & 1)]);
-          const int brc = lyap_build_recycle(ctx, (int32_t)(seeds.size() / k), seeds.data(), s_auto);
-          if (brc != LYAP_OK) throw Fail{brc};
-          ctx->recycle_manual = false;  // automatic: rebuilt when the box changes
-          ctx->auto_box = box;
-        }
+        const int brc = lyap_build_recycle(ctx, (int32_t)(seeds.size() / k), seeds.data(), s_auto);
+        if (brc != LYAP_OK) throw Fail{brc};
+        ctx->recycle_manual = false;  // automatic: rebuilt when a batch leaves the box
+        ctx->auto_box = box;
       }
     }
     if (ctx->opts.schedule) {
-      std::vector<double> hV((size_t)nv * k);
-      if (own) {
-        std::memcpy(hV.data(), V, hV.size() * 8);
-      } else {
-        CK(cudaMemcpyAsync(hV.data(), V, hV.size() * 8, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-      }
-      std::vector<double> cost(nv);
-      for (int64_t i = 0; i < nv; ++i) {
-        double c = 0.0;
-        for (int64_t t = 0; t < k; ++t) c += std::fabs(hV[i * k + t]) * ctx->seed.wcost[t];
-        cost[i] = c;
-      }
-      std::vector<int> ord(nv);
-      for (int64_t i = 0; i < nv; ++i) ord[i] = (int)i;
-      std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return cost[x] > cost[y]; });
       Engine& g = ctx->eng;
-      if (g.order_cap < nv) {
-        dfree(g.order);
+      if (g.sched_cap < nv || !g.order || !g.regq) {
+        for (void* p : {(void*)g.order, (void*)g.regq, (void*)g.skey, (void*)g.skey2, (void*)g.sidx, g.cub_tmp}) dfree(p);
+        g.order = g.regq = g.sidx = nullptr;
+        g.skey = g.skey2 = nullptr;
+        g.cub_tmp = nullptr;
+        g.sched_cap = g.order_cap = g.regq_cap = 0;
         g.order = dalloc<int>(ctx, nv, false);
-        g.order_cap = nv;
+        g.regq = dalloc<int>(ctx, nv, false);
+        g.sidx = dalloc<int>(ctx, nv, false);
+        g.skey = dalloc<double>(ctx, nv, false);
+        g.skey2 = dalloc<double>(ctx, nv, false);
+        g.cub_bytes = 0;
+        CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, g.cub_bytes, g.skey, g.skey2, g.sidx, g.order, (int)nv,
+                                                     0, 64, st));
+        g.cub_tmp = dalloc<char>(ctx, g.cub_bytes, false);
+        g.sched_cap = g.order_cap = g.regq_cap = nv;
       }
-      CK(cudaMemcpyAsync(g.order, ord.data(), nv * sizeof(int), cudaMemcpyHostToDevice, st));
-      CK(cudaStreamSynchronize(st));
+      const unsigned nb = (unsigned)std::min<int64_t>((nv + 255) / 256, 4096);
+      k_cost<<<nb, 256, 0, st>>>(dV, (int)nv, (int)k, sd.dwork, g.skey, g.sidx);
+      LAUNCHED();
+      // stable descending radix sort: equal costs keep row order (the host std::stable_sort order)
+      size_t bytes = g.cub_bytes;
+      CK(cub::DeviceRadixSort::SortPairsDescending(g.cub_tmp, bytes, g.skey, g.skey2, g.sidx, g.order, (int)nv, 0, 64,
+                                                   st));
       dorder = g.order;
-      if (ctx->nreg > 0) {  // nearest regime seed in log|v| (host scheduling logic)
-        std::vector<int> rq(nv);
-        const double* seeds = reinterpret_cast<const double*>(ctx->reg_seeds.data());
-        for (int64_t q = 0; q < nv; ++q) {
-          const double* v = &hV[(size_t)ord[q] * k];
-          double best = 1e300;
-          int arg = -1;
-          for (int r = 0; r < ctx->nreg; ++r) {
-            double d2 = 0.0;
-            for (int64_t t = 0; t < k; ++t) {
-              const double dv = std::log(std::fabs(v[t]) + 1e-300) - seeds[r * k + t];
-              d2 += dv * dv;
-            }
-            if (d2 < best) {
-              best = d2;
-              arg = r;
-            }
-          }
-          rq[q] = arg;
-        }
-        if (!g.regq || g.order_cap < nv) {
-          dfree(g.regq);
-          g.regq = dalloc<int>(ctx, std::max<int64_t>(nv, g.order_cap), false);
-        }
-        CK(cudaMemcpyAsync(g.regq, rq.data(), nv * sizeof(int), cudaMemcpyHostToDevice, st));
-        CK(cudaStreamSynchronize(st));
+      if (ctx->nreg > 0) {  // nearest regime seed in log|v|
+        k_regime<<<nb, 256, 0, st>>>(dV, g.order, (int)nv, (int)k, sd.dwork + 32, ctx->nreg, g.regq);
+        LAUNCHED();
       }
     }
     rc = run_batch(ctx, nv, dV, dorder, dtr, dst, dap, dres, st, nullptr,
@@ -1204,6 +1224,7 @@ int lyap_set_recycle(lyap_ctx* ctx, int32_t nreg, int32_t s, const double* U, co
     std::vector<double> ls((size_t)nreg * sd.k);
     for (size_t i = 0; i < ls.size(); ++i) ls[i] = std::log(std::fabs(seeds[i]) + 1e-300);
     ctx->reg_seeds.assign(reinterpret_cast<const char*>(ls.data()), ls.size() * sizeof(double));
+    upload_seeds(ctx);
     dfree(ctx->sreg);
     ctx->sreg = dalloc<int>(ctx, nreg, false);
     std::vector<int> hsz(nreg, s);
@@ -1454,6 +1475,7 @@ static int build_recycle_impl(lyap_ctx* ctx, int32_t nseeds, const double* seeds
     for (int r : used)
       for (int64_t t = 0; t < k; ++t) seeds_used.push_back(std::log(std::fabs(seeds[(int64_t)r * k + t])));
     ctx->reg_seeds.assign(reinterpret_cast<const char*>(seeds_used.data()), seeds_used.size() * sizeof(double));
+    upload_seeds(ctx);
   } catch (Fail f) {
     rc = f.code;
     dfree(ctx->Ureg);

@@ -341,6 +341,46 @@ __global__ void k_solution_Y(const double* __restrict__ lam, const double* __res
   Y[b * n + a] = acc.re;
 }
 
+// Per-rep diagonal block of the folded T (the preconditioner's v-independent part, engine.cuh
+// k_pfactor): the exact response of K1's operator (k1_gen -> Lf -> k1_epi) at the rep's own
+// coordinates to a unit input there -- T_d (F) plus the Cauchy coupling restricted to the rep's own
+// folded 2 x 2 block of Lf (for a pair: L_jj and L_{conj j, j} = 1/(2 Re lambda_j)).
+// Pb[rep][(2s + a) * 2K + (2t + b)] for pairs (a, b = Re, Im), Pb[rep][s * 2K + t] for reals.
+template <int K>
+__global__ void k_pblock(const double* __restrict__ Lf, int64_t npad, const double* __restrict__ bhr,
+                         const double* __restrict__ btl, const double* __restrict__ F, int64_t npairs, int64_t nrep,
+                         double* __restrict__ Pb) {
+  const int64_t rep = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (rep >= nrep) return;
+  constexpr int RS = 2 * K;
+  double* out = Pb + rep * 4 * K * K;
+  const bool pair = rep < npairs;
+  const int64_t c = pair ? 2 * rep : rep + npairs;
+  if (pair) {
+    const double l00 = Lf[c * npad + c], l01 = Lf[c * npad + c + 1];
+    const double l10 = Lf[(c + 1) * npad + c], l11 = Lf[(c + 1) * npad + c + 1];
+    for (int t = 0; t < K; ++t)
+      for (int b = 0; b < 2; ++b) {
+        const double x = b == 0 ? 1.0 : 0.0, y = b == 0 ? 0.0 : 1.0;  // unit input X_t = e_b
+        for (int s = 0; s < K; ++s) {
+          const double br = bhr[c * K + s], bi = bhr[(c + 1) * K + s];
+          const double p0 = br * x - bi * y, p1 = br * y + bi * x;  // k1_gen: (B^r_s)(x + iy)
+          const cplx u = mk(l00 * p0 + l01 * p1, l10 * p0 + l11 * p1);  // Lf block
+          const cplx bl = mk(btl[c * K + t], btl[(c + 1) * K + t]);
+          const double* f = F + ((rep * K + s) * K + t) * 2;
+          const cplx yv = bl * u + mk(f[0], f[1]) * mk(x, y);  // k1_epi
+          out[(2 * s) * RS + 2 * t + b] = yv.re;
+          out[(2 * s + 1) * RS + 2 * t + b] = yv.im;
+        }
+      }
+  } else {
+    const double l = Lf[c * npad + c];
+    for (int s = 0; s < K; ++s)
+      for (int t = 0; t < K; ++t)
+        out[s * RS + t] = btl[c * K + t] * l * bhr[c * K + s] + F[((rep * K + s) * K + t) * 2];
+  }
+}
+
 // deterministic sum of t0 partials (one block)
 __global__ void k_sum(const double* __restrict__ x, int64_t n, double* out) {
   __shared__ double red[32];

@@ -127,3 +127,52 @@ def test_gloo_weak_sweep():
     for _, full, am in res:
         np.testing.assert_array_equal(full, ref)
         assert am == int(np.argmin(ref))
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_cost_balanced_shards(world):
+    """Cost-balanced strong sharding (snake deal of the cost-sorted rows): on c5's 8^4 grid with a
+    proxy sum_t |v_t| w_t, every rank's summed cost is within 5 % of the mean (the chunked
+    round-robin deal it replaces is far off), and the shards partition the grid with equal sizes."""
+    from paper_2312_08201_b200.sweep import shard_balance
+    import workloads
+    W = workloads.make("c5")
+    cost = np.abs(W.V) @ np.array([1.0, 0.7, 1.3, 0.9])
+    parts = [shard_indices(W.nv, r, world, cost=cost) for r in range(world)]
+    np.testing.assert_array_equal(np.sort(np.concatenate(parts)), np.arange(W.nv))
+    assert max(len(p) for p in parts) - min(len(p) for p in parts) <= 1
+    assert shard_balance(W.nv, world, cost) <= 1.05
+    assert shard_balance(W.nv, world, cost, balanced=False) > 1.05  # the old chunked deal
+
+
+def _worker_cost(rank, world, port, V, cost, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sw = Sweep(len(V), rank, world, torch.device("cpu"), cost=cost)
+        full, am = sw.run(lambda rows: torch.tensor(fake_tau(V[rows]), dtype=torch.float64))
+        out_q.put((rank, full.numpy().copy(), int(am)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_cost_balanced_sweep_matches_serial():
+    world = 3
+    V = np.random.default_rng(3).uniform(0.05, 5.0, (301, 2))
+    V = np.concatenate([V, V[:4]])  # ties: the first occurrence must win
+    cost = V.sum(1)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_cost, args=(r, world, port, V, cost, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ref = fake_tau(V)
+    for _, full, am in res:
+        np.testing.assert_array_equal(full, ref)
+        assert am == int(np.argmin(ref))

@@ -20,7 +20,7 @@ import multiprocessing as mp  # noqa: E402
 import oracle  # noqa: E402
 import workloads  # noqa: E402
 
-SAMPLES = {"c1": 256, "c2": 64, "c3": 64, "c4": 32, "c5": 24}
+SAMPLES = {"c1": 256, "c2": 256, "c3": 256, "c4": 64, "c5": 32}
 _W = {}
 
 
