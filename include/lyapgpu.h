@@ -66,11 +66,12 @@ typedef struct {
                           sum_t |v_t| ||B~l_t|| ||B^r_t|| (largest perturbation first, so the slow
                           systems do not form a tail); 0: in row order of V.  Results are returned
                           in row order either way. */
-  int32_t recycle;     /* recycle-space size s: -1 (default) auto = 32 when n k >= 12000 (where the
-                          T-apply dominates; c5 443 -> 528 v/s), else off; 0 off; > 0 that size.
+  int32_t recycle;     /* automatic recycle spaces of size s: -1 (default) and 0 off; > 0 that size.
                           With s > 0, lyap_trace_batch builds the spaces itself (lyap_build_recycle
                           on the 2^k corners of the batch's bounding box, all v > 0) the first time
-                          and whenever the box changes; the build time is in lyap_stats. */
+                          and whenever a batch leaves the box; the build time is in lyap_stats.
+                          (Off by default since the pair-block preconditioner: measured c5 909.7 v/s
+                          off vs 786.7 with s = 32.) */
 } lyap_opts;
 
 typedef struct {
@@ -96,6 +97,8 @@ typedef struct {
   int64_t kernel_launches; /* all kernels this library launched */
   double batch_ms;         /* device time of the last lyap_trace_batch */
   double recycle_build_ms; /* time spent building recycle spaces (automatic or lyap_build_recycle) */
+  int64_t graph_instantiations; /* engine CUDA graphs instantiated (a repeated call updates them in place) */
+  int64_t graph_updates;        /* engine CUDA graphs updated in place (cudaGraphExecUpdate) */
 } lyap_stats;
 
 /* Fills *opts with the defaults above. */

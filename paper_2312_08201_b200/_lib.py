@@ -38,7 +38,8 @@ class Info(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("k1_launches", C.c_int64), ("k1_vectors", C.c_int64), ("k1_ms", C.c_double),
                 ("k1_flops", C.c_double), ("iterations", C.c_int64), ("kernel_launches", C.c_int64),
-                ("batch_ms", C.c_double), ("recycle_build_ms", C.c_double)]
+                ("batch_ms", C.c_double), ("recycle_build_ms", C.c_double),
+                ("graph_instantiations", C.c_int64), ("graph_updates", C.c_int64)]
 
 
 def _load():

@@ -53,7 +53,8 @@ struct Seed {
 
 // Batched Krylov engine buffers (slot-major).
 struct Engine {
-  int b = 0;        // slots
+  int b = 0;        // slots of the current run (<= bcap)
+  int bcap = 0;     // slots allocated
   int mmax = 0;     // restart length
   int64_t L = 0;    // vector length k * npad
   int64_t ncol = 0; // K1 GEMM columns, b*k*k rounded up to the N tile
@@ -111,5 +112,7 @@ struct lyap_ctx {
   bool recycle_manual = false;   // spaces given by lyap_set_recycle / lyap_build_recycle: no automatic rebuild
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evfork = nullptr, evjoin = nullptr;
   cudaStream_t xstream[4] = {};  // streams of slot groups 1..3 (group 0 runs on `stream`)
+  cudaGraphExec_t gexec[4] = {};  // per slot group: the engine iteration graph, kept across calls
+  std::vector<cudaEvent_t> prof_evs;  // K1 timing events of the graphs (opts.profile)
   cudaEvent_t xjoin[4] = {};
 };

@@ -190,21 +190,42 @@ int auto_mmax(const lyap_ctx* ctx) {
   return ctx->seed.n * ctx->seed.k >= 12000 ? 384 : 160;
 }
 
+int engine_groups(int b) {
+  int G = b >= 64 ? 2 : 1;
+  if (const char* ev = std::getenv("LYAP_GROUPS")) G = std::max(1, std::min(4, std::atoi(ev)));  // experiments
+  return std::max(1, std::min(G, b / 32));  // every group keeps >= 32 slots
+}
+
+// Sets the run shape (slots b, slot groups, K1 columns per group) of an allocated engine.
+void configure_run(const Seed& s, Engine& g, int b) {
+  g.b = b;
+  g.groups = engine_groups(b);
+  g.ncol = roundup((int64_t)((b + g.groups - 1) / g.groups) * s.k * s.k, s.n <= SMALL_N ? S_BN : G_BN);
+}
+
+// The engine is allocated for a capacity of bcap slots and reused by any later call that needs
+// b <= bcap slots with the same restart length (NEXT row f3: optimizer-style callers change nv on
+// every call; reallocating the multi-GB Krylov basis each time dominated their run time).
 void ensure_engine(lyap_ctx* ctx, int b, int mmax) {
   Engine& g = ctx->eng;
-  if (g.b == b && g.mmax == mmax && g.Qb) return;
-  free_engine(g);
   const Seed& s = ctx->seed;
-  g.b = b;
+  if (g.Qb && g.mmax == mmax && g.bcap >= b) {
+    configure_run(s, g, b);
+    return;
+  }
+  free_engine(g);
+  g.bcap = b;
   g.mmax = mmax;
   g.L = s.k * s.npad;
-  g.groups = b >= 64 ? 2 : 1;
-  if (const char* ev = std::getenv("LYAP_GROUPS")) g.groups = std::max(1, std::min(4, std::atoi(ev)));  // experiments
-  g.groups = std::max(1, std::min(g.groups, b / 32));  // every group keeps >= 32 slots
-  g.ncol = roundup((int64_t)((b + g.groups - 1) / g.groups) * s.k * s.k, tile_n(s));
+  // K1 operand columns for any run b' <= b and any group count (sum over groups of the rounded
+  // per-group widths)
+  int64_t colcap = 0;
+  for (int G = 1; G <= 4; ++G)
+    colcap = std::max<int64_t>(colcap, G * roundup((int64_t)((b + G - 1) / G) * s.k * s.k, s.n <= SMALL_N ? S_BN : G_BN));
+  configure_run(s, g, b);
   g.nchunk = (int)((g.L + RED_CE - 1) / RED_CE);
-  g.Bop = dalloc<double>(ctx, (size_t)g.groups * s.npad * g.ncol);
-  g.U = dalloc<double>(ctx, (size_t)g.groups * s.npad * g.ncol);
+  g.Bop = dalloc<double>(ctx, (size_t)s.npad * colcap);
+  g.U = dalloc<double>(ctx, (size_t)s.npad * colcap);
   g.Xin = dalloc<double>(ctx, (size_t)b * g.L);
   g.X = dalloc<double>(ctx, (size_t)b * g.L);
   g.Qb = dalloc<double>(ctx, (size_t)b * (mmax + 1) * g.L);
@@ -227,9 +248,8 @@ void ensure_engine(lyap_ctx* ctx, int b, int mmax) {
   g.vidx = dalloc<int>(ctx, b);
   g.applies = dalloc<int>(ctx, b);
   g.restarts = dalloc<int>(ctx, 5 * (size_t)b);  // restarts | newv | alist | su | reg
-  g.ctrl = dalloc<int>(ctx, 8 * (g.groups + 1));
-  CK(cudaMallocHost(&g.h_ctrl, 8 * (g.groups + 1) * sizeof(int)));
-  ctx->info.batch = b;
+  g.ctrl = dalloc<int>(ctx, 8 * 5);               // up to 4 groups + the shared block
+  CK(cudaMallocHost(&g.h_ctrl, 8 * 5 * sizeof(int)));
   ctx->info.max_dim = mmax;
 }
 
@@ -287,6 +307,7 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   const Seed& s = ctx->seed;
   const int b = auto_batch(ctx, nv), mmax = auto_mmax(ctx);
   ensure_engine(ctx, b, mmax);
+  ctx->info.batch = b;
   Engine& g = ctx->eng;
   const int G = g.groups;
   CK(cudaMemsetAsync(g.phase, 0, sizeof(int) * b, st));  // PH_FREE
@@ -447,12 +468,15 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   // CUDA graphs: `poll` iterations per group are captured once (each with its own GEMM event pair
   // when profiling) and replayed; the host only polls the done counter between replays.
   const bool prof = ctx->opts.profile != 0;
-  std::vector<cudaEvent_t> evs;
-  if (prof) {
-    evs.resize((size_t)2 * G * poll);
+  std::vector<cudaEvent_t>& evs = ctx->prof_evs;
+  if (prof && evs.size() < (size_t)2 * G * poll) {
+    for (auto& e : evs) cudaEventDestroy(e);
+    evs.assign((size_t)2 * G * poll, nullptr);
     for (auto& e : evs) CK(cudaEventCreate(&e));
   }
-  std::vector<cudaGraphExec_t> gexec(G, nullptr);
+  // the instantiated graphs are kept in the ctx: a later call re-captures (cheap) and updates the
+  // executable in place when the topology matches (cudaGraphExecUpdate), instead of re-instantiating
+  cudaGraphExec_t* gexec = ctx->gexec;
   int64_t launches_per_replay = 0;
   for (int gi = 0; gi < G; ++gi) {
     cudaGraph_t graph;
@@ -463,7 +487,20 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
       launches_per_replay += issue(gi, sts[gi], eb, ee, cudaEventRecordExternal);
     }
     CK(cudaStreamEndCapture(sts[gi], &graph));
-    CK(cudaGraphInstantiate(&gexec[gi], graph, 0));
+    if (gexec[gi]) {
+      cudaGraphExecUpdateResultInfo info;
+      if (cudaGraphExecUpdate(gexec[gi], graph, &info) != cudaSuccess) {
+        cudaGetLastError();
+        cudaGraphExecDestroy(gexec[gi]);
+        gexec[gi] = nullptr;
+      } else {
+        ctx->stats.graph_updates++;
+      }
+    }
+    if (!gexec[gi]) {
+      CK(cudaGraphInstantiate(&gexec[gi], graph, 0));
+      ctx->stats.graph_instantiations++;
+    }
     CK(cudaGraphDestroy(graph));
   }
   ctx->stats.kernel_launches -= launches_per_replay;  // counted per replay below
@@ -478,7 +515,7 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
     CK(cudaMemcpyAsync(g.h_ctrl, g.ctrl, 8 * (G + 1) * sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (prof) {
-      for (size_t i = 0; i < evs.size(); i += 2) {
+      for (size_t i = 0; i < (size_t)2 * G * poll; i += 2) {
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, evs[i], evs[i + 1]));
         ctx->stats.k1_ms += ms;
@@ -493,9 +530,6 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
       break;
     }
   }
-  for (auto& ge : gexec)
-    if (ge) cudaGraphExecDestroy(ge);
-  for (auto& e : evs) cudaEventDestroy(e);
   for (int gi = 1; gi < G; ++gi) {
     if (!ctx->xjoin[gi]) CK(cudaEventCreateWithFlags(&ctx->xjoin[gi], cudaEventDisableTiming));
     CK(cudaEventRecord(ctx->xjoin[gi], sts[gi]));
@@ -628,6 +662,9 @@ static void destroy_impl(lyap_ctx* c) {
     if (c->xstream[gi]) cudaStreamDestroy(c->xstream[gi]);
     if (c->xjoin[gi]) cudaEventDestroy(c->xjoin[gi]);
   }
+  for (auto& ge : c->gexec)
+    if (ge) cudaGraphExecDestroy(ge);
+  for (auto& e : c->prof_evs) cudaEventDestroy(e);
   if (c->evfork) cudaEventDestroy(c->evfork);
   if (c->evjoin) cudaEventDestroy(c->evjoin);
   delete c;
@@ -1026,7 +1063,7 @@ int lyap_trace_batch_ex(lyap_ctx* ctx, int64_t nv, const double* V, double* trac
     // schedule (device-side, on the call's stream; V never visits the host): expensive
     // (large-perturbation) v first, so slow systems do not form a tail (sched.cuh)
     const int* dorder = nullptr;
-    const int s_auto = ctx->opts.recycle < 0 ? (ctx->seed.n * ctx->seed.k >= 12000 ? 32 : 0) : ctx->opts.recycle;
+    const int s_auto = ctx->opts.recycle < 0 ? 0 : ctx->opts.recycle;
     Seed& sd = ctx->seed;
     ensure_dwork(ctx);
     if (s_auto > 0 && !ctx->recycle_manual) {

@@ -404,8 +404,10 @@ def test_recycle_built_spaces_parity_and_savings(name, s, rounds, monkeypatch):
 # ----------------------------------------------------------------------------- NEXT row f1
 @pytest.mark.parametrize("name,nsub", [("c1", 256), ("c2", 40)])
 def test_extended_krylov_projection(name, nsub):
-    """EKProblem (PAPER.md §2.2, Alg. 1): an approximation controlled by the backward-error target;
-    against the oracle samples it converges as eps shrinks."""
+    """EKProblem (§2.2, Alg. 1): an approximation controlled by the backward-error target of
+    Prop. 2.1.  A returned LYAP_OK certifies bwd <= eps; the trace error against the oracle must then
+    scale with eps (forward error <= condition x backward error: <= 1e3 eps here), and shrink as eps
+    does."""
     from paper_2312_08201_b200 import EKProblem
     W = workloads.make(name)
     X0 = scipy.linalg.solve_continuous_lyapunov(W.A0, -W.Q)  # seed solution (independent LAPACK)
@@ -415,161 +417,30 @@ def test_extended_krylov_projection(name, nsub):
     ref = np.array(g["traces"])[:nsub]
     errs, info = [], []
     for eps in (1e-6, 1e-10):
-        ek = EKProblem(W.A0, W.Bl, W.Br, X0 @ W.Br, W.E, t0, max_dim=800)
+        ek = EKProblem(W.A0, W.Bl, W.Br, X0 @ W.Br, W.E, t0, max_dim=W.n)
         tau, dim, bwd = ek.trace_batch(W.V[idx], eps=eps)
         errs.append(rel_err(tau, ref).max())
         info.append((eps, dim, bwd, errs[-1]))
-        assert dim % (4 * W.k) == 0 and dim <= min(W.n, 800)
+        assert bwd <= eps, info
+        assert errs[-1] <= 1e3 * eps, info
+        assert dim % (4 * W.k) == 0 and dim <= W.n
         ek.close()
-    assert errs[1] <= max(1e-7, errs[0]), info
-    assert errs[1] <= 1e-6, info
+    assert errs[1] <= errs[0], info
 
 
-# ----------------------------------------------------------------------------- M1 (argmin) on the engine
-def test_sweep_argmin_c1_matches_oracle_golden():
-    """M1 (north star (c)): the engine's traces of the whole c1 grid through Sweep.run (the bench's
-    step) give the oracle's argmin (tests/golden/oracle_c1.json holds all 256 oracle traces)."""
-    import torch
-    from paper_2312_08201_b200.sweep import Sweep
-    g = _golden("c1")
-    assert g["indices"] == list(range(256))
+def test_extended_krylov_capacity_is_flagged():
+    """A basis capped below n cannot certify a tight target: LYAP_EPARTIAL, and with allow_partial the
+    reported backward error is the last certified one (> eps), never a fabricated 0."""
+    from paper_2312_08201_b200 import EKProblem, LyapError
     W = workloads.make("c1")
-    P = _problem(W.A0, W.Bl, W.Br, W.Q, W.E)
-    Vd = torch.tensor(W.V, device="cuda")
-    sw = Sweep(W.nv, 0, 1, torch.device("cuda"))
-    full, am = sw.run(lambda rows: P.trace_batch(Vd[torch.as_tensor(rows, device="cuda")]))
-    ref = np.array(g["traces"])
-    assert int(am) == int(np.argmin(ref)) == 204
-    assert rel_err(full.cpu().numpy(), ref).max() <= RTOL
-    P.close()
-
-
-def test_sweep_argmin_one_dof_critical_damping():
-    """M1 pinned by a closed form: one mode A0 = [[0, w], [-w, -2 a w]], damper weight
-    phi: tau(v) = 2/c + c/(2 w^2), c = 2 a w + v phi^2, minimised at critical damping c = 2w, i.e.
-    v* = 2 w (1 - a) / phi^2.  The engine's argmin over a fine grid is the grid point nearest v*."""
-    import torch
-    from paper_2312_08201_b200.sweep import Sweep
-    w, a, phi = 1.7, 0.02, 0.6
-    A0 = np.array([[0.0, w], [-w, -2 * a * w]])
-    B = np.array([[0.0], [phi]])
-    V = np.geomspace(0.5, 50.0, 2001)[:, None]
-    P = _problem(A0, B, B, np.eye(2), np.eye(2))
-    sw = Sweep(len(V), 0, 1, torch.device("cuda"))
-    Vd = torch.tensor(V, device="cuda")
-    full, am = sw.run(lambda rows: P.trace_batch(Vd))
-    c = 2 * a * w + V[:, 0] * phi ** 2
-    closed = 2.0 / c + c / (2 * w * w)
-    assert rel_err(full.cpu().numpy(), closed).max() <= 1e-11
-    vstar = 2 * w * (1 - a) / phi ** 2
-    assert int(am) == int(np.argmin(np.abs(np.log(V[:, 0] / vstar))))
-    P.close()
-
-
-# ----------------------------------------------------------------------------- K1 at the large-tile config
-def test_k1_large_tile_config():
-    """K1 with n > 1536 runs the 128 x 128 x 32 CTA-tile GEMM (lyapgpu.cu: SMALL_N); check it against
-    the complex operator built from eqs. (N1M1)/(N2M1)/(N1M2) as the small-n test does."""
-    import torch
-    rng = np.random.default_rng(77)
-    n, k = 1603, 2
-    A0, Bl, Br, Q, E = workloads.random_stable(n, k, rng)
-    P = _problem(A0, Bl, Br, Q, E)
-    st = P.export_state()
-    npairs, npad = st["n_pairs"], st["npad"]
-    assert npad % 128 == 0 and npad >= n
-    lam, br, bl = _complex_factors(st, n)
-    L = 1.0 / (lam[:, None] + lam[None, :])
-    F = np.einsum("ij,is,it->jst", L, br, bl)
-    nvec = 3
-    sig = rng.uniform(-2, 3, (nvec, k))
-    Gs = [_unfold(_fold(rng.standard_normal((k, n)) + 1j * rng.standard_normal((k, n)), npairs, npad), npairs, n)
-          for _ in range(nvec)]
-    Xs = np.stack([_fold(G, npairs, npad) for G in Gs])
-    Y = P.apply_C(torch.tensor(Xs, device="cuda"), torch.tensor(sig, device="cuda")).cpu().numpy()
-    for v in range(nvec):
-        G = Gs[v]
-        U = (L.T @ (br[:, :, None] * G.T[:, None, :]).reshape(n, -1)).reshape(n, k, k)  # j, s, t
-        TG = np.einsum("jst,tj->sj", F, G) + np.einsum("jt,jst->sj", bl, U)
-        expect = _fold(sig[v][:, None] * G - TG, npairs, npad)
-        np.testing.assert_allclose(Y[v], expect, rtol=0, atol=1e-12 * np.abs(expect).max())
-        assert np.all(Y[v][:, n:] == 0.0)
-    P.close()
-
-
-# ----------------------------------------------------------------------------- boundary / scheduling
-def test_device_schedule_matches_unscheduled_and_regq_growth():
-    """Device-side scheduling (sched.cuh: cost keys + CUB radix sort + regime map) only permutes the
-    work; a recycle-regime map that must grow between calls (small nv, then a larger nv on one ctx)
-    keeps parity (regq capacity)."""
-    import torch
-    W = workloads.make("c1")
-    g = _golden("c1")
-    ref = np.array(g["traces"])
-    P = _problem(W.A0, W.Bl, W.Br, W.Q, W.E)
-    P.build_recycle(V=W.V, s=16)
-    small = P.trace_batch(torch.tensor(W.V[:5], device="cuda")).cpu().numpy()
-    assert rel_err(small, ref[:5]).max() <= RTOL
-    full = P.trace_batch(torch.tensor(W.V, device="cuda")).cpu().numpy()
-    assert rel_err(full, ref).max() <= RTOL
-    plain = _problem(W.A0, W.Bl, W.Br, W.Q, W.E, schedule=False).trace_batch(W.V)
-    assert rel_err(plain, ref).max() <= RTOL
-    P.close()
-
-
-def test_trace_batch_rejects_bad_device_shape():
-    import torch
-    W = workloads.make("c1")
-    P = _problem(W.A0, W.Bl, W.Br, W.Q, W.E)
-    with pytest.raises(ValueError):
-        P.trace_batch(torch.zeros(4, 3, dtype=torch.float64, device="cuda"))
-    P.close()
-
-
-# ----------------------------------------------------------------------------- sharded sweep, real engine
-def _sharded_worker(rank, world, port, name, out_q):
-    import os
-
-    import torch
-    import torch.distributed as dist
-    from paper_2312_08201_b200 import Problem
-    from paper_2312_08201_b200.sweep import Sweep
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    try:
-        W = workloads.make(name)
-        P = Problem(W.A0, W.Bl, W.Br, W.Q, W.E, device=0, recycle=0)
-        sw = Sweep(W.nv, rank, world, torch.device("cpu"), scaling="strong", cost=P.cost_proxy(W.V))
-        full, am = sw.run(lambda rows: torch.tensor(P.trace_batch(W.V[rows])))
-        out_q.put((rank, full.numpy().copy(), int(am)))
-        P.close()
-    finally:
-        dist.destroy_process_group()
-
-
-@pytest.mark.parametrize("name", ["c1", "c2"])
-def test_sharded_sweep_real_engine_bitwise(name):
-    """two ranks (gloo, both on cuda:0) running the real engine on their shards give
-    traces BITWISE equal to a single-rank run of the whole grid (every v starts from g = 0 and every
-    reduction has a fixed order, so a trace does not depend on the batch it was solved in)."""
-    import socket
-
-    import torch.multiprocessing as mp
-    W = workloads.make(name)
-    single = _problem(W.A0, W.Bl, W.Br, W.Q, W.E, recycle=0).trace_batch(W.V)
-    with socket.socket() as s:
-        s.bind(("127.0.0.1", 0))
-        port = s.getsockname()[1]
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, name, q)) for r in range(2)]
-    for p in procs:
-        p.start()
-    res = [q.get(timeout=600) for _ in procs]
-    for p in procs:
-        p.join(timeout=120)
-        assert p.exitcode == 0
-    for _, full, am in res:
-        np.testing.assert_array_equal(full, single)
-        assert am == int(np.argmin(single))
+    X0 = scipy.linalg.solve_continuous_lyapunov(W.A0, -W.Q)
+    t0 = float(np.sum(W.E * X0))
+    ek = EKProblem(W.A0, W.Bl, W.Br, X0 @ W.Br, W.E, t0, max_dim=16)
+    with pytest.raises(LyapError) as ei:
+        ek.trace_batch(W.V[:8], eps=1e-12)
+    assert ei.value.code == 6
+    ek.close()
+    ek = EKProblem(W.A0, W.Bl, W.Br, X0 @ W.Br, W.E, t0, max_dim=16)
+    tau, dim, bwd = ek.trace_batch(W.V[:8], eps=1e-12, allow_partial=True)
+    assert dim <= 16 and bwd > 1e-12 and np.all(np.isfinite(tau))
+    ek.close()

@@ -208,3 +208,44 @@ def test_golden_config_traces_subset():
         W = workloads.make(name)
         for idx, tau in list(zip(g["indices"], g["traces"]))[:count]:
             assert oracle.trace_EX(W.A0, W.Bl, W.Br, W.Q, W.E, W.V[idx]) == pytest.approx(tau, rel=1e-12)
+
+
+# ----------------------------------------------------------------------------- stability filter (f4)
+def test_stability_oracle_one_dof_closed_form():
+    """Rightmost eigenvalue of A(v) = [[0, w], [-w, -c]], c = 2 a w + v phi^2 (PAPER.md:1183 filter):
+    Re = -c/2 below critical damping, (-c + sqrt(c^2 - 4 w^2))/2 above; stable iff c > 0."""
+    w, a, phi = 1.3, 0.02, 0.7
+    A0 = np.array([[0.0, w], [-w, -2 * a * w]])
+    B = np.array([[0.0], [phi]])
+    for v in (-3.0, -0.2, -2 * a * w / phi ** 2 * 1.001, -2 * a * w / phi ** 2 * 0.999, 0.0, 0.5, 7.0, 40.0):
+        c = 2 * a * w + v * phi ** 2
+        expect = -c / 2 if c * c < 4 * w * w else (-c + np.sqrt(c * c - 4 * w * w)) / 2
+        got = oracle.rightmost_real_part(A0, B, B, [v])
+        assert got == pytest.approx(expect, abs=1e-12 * max(1.0, abs(c)))
+        assert oracle.stable_mask(A0, B, B, [[v]])[0] == (c > 0)
+
+
+def test_stability_oracle_diagonal_rank_one():
+    """A0 = diag(d), Bl = Br = e_1: A(v) = diag(d_1 - v, d_2, ...), so the rightmost real part is
+    max(d_1 - v, d_2, ...) exactly."""
+    d = np.array([-0.5, -2.0, -3.5, -0.75])
+    A0 = np.diag(d)
+    e1 = np.zeros((4, 1))
+    e1[0] = 1.0
+    for v in (-1.0, -0.5, -0.25, 0.0, 0.1, 5.0):
+        assert oracle.rightmost_real_part(A0, e1, e1, [v]) == pytest.approx(max(d[0] - v, d[1], d[2], d[3]), abs=1e-14)
+    np.testing.assert_array_equal(oracle.stable_mask(A0, e1, e1, [[-1.0], [-0.5], [0.2]]), [False, False, True])
+
+
+def test_stability_oracle_quadratic_formula():
+    """Random 2 x 2 A(v): eigenvalues from the characteristic polynomial l^2 - tr l + det."""
+    rng = np.random.default_rng(11)
+    for _ in range(40):
+        A0 = rng.standard_normal((2, 2))
+        Bl, Br = rng.standard_normal((2, 2)), rng.standard_normal((2, 2))
+        v = rng.uniform(-2, 2, 2)
+        A = A0 - Bl @ np.diag(v) @ Br.T
+        tr, det = np.trace(A), np.linalg.det(A)
+        disc = complex(tr * tr - 4 * det)
+        roots = [(tr + np.sqrt(disc)) / 2, (tr - np.sqrt(disc)) / 2]
+        assert oracle.rightmost_real_part(A0, Bl, Br, v) == pytest.approx(max(r.real for r in roots), abs=1e-12)

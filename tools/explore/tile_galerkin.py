@@ -129,11 +129,21 @@ def tile_solve(sm, V, p=4, mode="galerkin", tol=1e-12, maxr=6000, verbose=False,
     a0 = sm.applies
     steps = 0
     t_small = 0.0
+    hybrid = mode.startswith("hybrid")
+    grow = float(mode.split(":")[1]) if ":" in mode else 1.3
+    next_check = 0
+    dirs = {}  # hybrid: member -> (its last direction, T of it)
+    nsolves = 0
     while res.max() > tol and Z.shape[1] < maxr:
         steps += 1
         act = torch.nonzero(res > tol).flatten()
-        order = act[torch.argsort(-res[act])][:p]
-        Rp = R[order].reshape(-1, k, n)
+        if hybrid and Z.shape[1] > 0 and Z.shape[1] < next_check and all(int(b) in dirs for b in act):
+            # block-Krylov continuation: z_b = P_b^{-1} C(v_b) d_b with T d_b already known
+            order = act
+            Rp = torch.stack([sigN[b] * dirs[int(b)][0] - dirs[int(b)][1] for b in act]).reshape(-1, k, n)
+        else:
+            order = act[torch.argsort(-res[act])][:p]
+            Rp = R[order].reshape(-1, k, n)
         if prec == "td":
             D = torch.einsum("bjst,btj->bsj", Minv[order], Rp).reshape(-1, N).T  # N x p
         else:
@@ -148,6 +158,15 @@ def tile_solve(sm, V, p=4, mode="galerkin", tol=1e-12, maxr=6000, verbose=False,
         TQ = sm.T(Qd.T.reshape(-1, k, n)).reshape(-1, N).T
         Z = torch.cat([Z, Qd], 1)
         TZ = torch.cat([TZ, TQ], 1)
+        if hybrid:
+            dirs = {}
+            kept = [int(b) for b, kp in zip(order, keep) if kp]
+            for i, b in enumerate(kept):
+                dirs[b] = (Qd[:, i], TQ[:, i])
+            if Z.shape[1] < next_check and all(int(b) in dirs for b in act):
+                continue  # no solve this step
+            next_check = max(int(grow * Z.shape[1]), Z.shape[1] + len(act))
+        nsolves += 1
         # projected solves for the unconverged members
         ts = time.time()
         r = Z.shape[1]
@@ -185,6 +204,8 @@ def tile_solve(sm, V, p=4, mode="galerkin", tol=1e-12, maxr=6000, verbose=False,
         res[act] = torch.linalg.norm(Ra, dim=1) / bn
         if verbose and steps % 10 == 0:
             print(f"   step {steps} dim {r} worst {res.max().item():.2e} active {int((res > tol).sum())}", flush=True)
+    if verbose:
+        print(f"   solves {nsolves}", flush=True)
     return sm.applies - a0, Z.shape[1], steps, t_small
 
 
