@@ -139,6 +139,16 @@ int lyap_trace_batch_ex(lyap_ctx* ctx, int64_t nv, const double* V, double* trac
                         int32_t* status, int32_t* applies, double* resid, int v_on_device,
                         void* cuda_stream);
 
+/* NEXT row f3 (solution recycling between consecutive iterates, PAPER.md:375-377 / 670-671): as
+ * lyap_trace_batch_ex with DEVICE pointers only (ordered on cuda_stream), plus
+ *   X0   (nullable): nv x (k x npad) folded initial guesses g(v) -- e.g. the solutions of nearby,
+ *        previously evaluated v (an optimizer's previous iterates); each v starts from its guess and
+ *        is certified by the same true-residual test, so the result does not depend on the guess
+ *        beyond the tolerance;
+ *   Xout (nullable): nv x (k x npad) the solved folded g(v) of every v (to be passed back as X0). */
+int lyap_trace_batch_x(lyap_ctx* ctx, int64_t nv, const double* V, const double* X0, double* Xout, double* traces,
+                       int32_t* status, int32_t* applies, double* resid, void* cuda_stream);
+
 int lyap_get_info(const lyap_ctx* ctx, lyap_info* info);
 int lyap_get_stats(const lyap_ctx* ctx, lyap_stats* stats);
 int lyap_reset_stats(lyap_ctx* ctx);

@@ -155,6 +155,38 @@ class Problem:
             self._check(rc)
         return (tau, st, ap, rs) if return_diagnostics else tau
 
+    def trace_batch_x(self, V, x0=None, *, return_diagnostics: bool = False, allow_partial: bool = False,
+                      stream=None):
+        """Device path with solution recycling (lyap_trace_batch_x, NEXT row f3): V (nv, k) CUDA tensor,
+        x0 (nv, k, npad) CUDA tensor of initial guesses or None.  Returns (tau, G) with G (nv, k, npad)
+        the folded solutions (pass them back as x0 for nearby v); with return_diagnostics also
+        (status, applies, resid)."""
+        import torch
+        V = V.to(torch.float64)
+        if V.ndim == 1:
+            V = V.reshape(-1, self.k)
+        if V.ndim != 2 or V.shape[1] != self.k:
+            raise ValueError(f"V must be (nv, {self.k}), got {tuple(V.shape)}")
+        V = V.contiguous()
+        nv, dev = V.shape[0], V.device
+        npad = self.info["npad"]
+        if x0 is not None:
+            x0 = x0.to(torch.float64).contiguous()
+            if tuple(x0.shape) != (nv, self.k, npad):
+                raise ValueError(f"x0 must be ({nv}, {self.k}, {npad})")
+        tau = torch.empty(nv, dtype=torch.float64, device=dev)
+        G = torch.zeros(nv, self.k, npad, dtype=torch.float64, device=dev)
+        st = torch.empty(nv, dtype=torch.int32, device=dev)
+        ap = torch.empty(nv, dtype=torch.int32, device=dev)
+        rs = torch.empty(nv, dtype=torch.float64, device=dev)
+        s = stream if stream is not None else torch.cuda.current_stream(dev)
+        rc = lib.lyap_trace_batch_x(self._ctx, nv, V.data_ptr(), x0.data_ptr() if x0 is not None else None,
+                                    G.data_ptr(), tau.data_ptr(), st.data_ptr(), ap.data_ptr(), rs.data_ptr(),
+                                    C.c_void_p(s.cuda_stream))
+        if rc != LYAP_OK and not (rc == LYAP_EPARTIAL and allow_partial):
+            self._check(rc)
+        return (tau, G, st, ap, rs) if return_diagnostics else (tau, G)
+
     def solution(self, V, return_traces: bool = False):
         """Full X(v) (n x n) for each row of V (NEXT row f2; O(n^3) per v).  Returns (nv, n, n)."""
         V = _f64(V)

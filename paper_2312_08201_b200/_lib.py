@@ -16,7 +16,8 @@ STATUS_NAMES = {0: "LYAP_OK", 1: "LYAP_EINVAL", 2: "LYAP_ENOMEM", 3: "LYAP_ECUDA
 LYAP_KMAX = 8
 
 # every symbol include/lyapgpu.h declares (checked by tests/test_abi.py)
-EXPORTED = ("lyap_default_opts", "lyap_setup", "lyap_trace_batch", "lyap_trace_batch_ex", "lyap_get_info",
+EXPORTED = ("lyap_default_opts", "lyap_setup", "lyap_trace_batch", "lyap_trace_batch_ex", "lyap_trace_batch_x",
+            "lyap_get_info",
             "lyap_get_stats", "lyap_reset_stats", "lyap_apply_C", "lyap_export_state", "lyap_destroy",
             "lyap_last_error", "lyap_solution", "lyap_setup_like", "lyap_set_recycle",
             "lyap_build_recycle", "lyap_ek_setup", "lyap_ek_trace_batch", "lyap_ek_destroy", "lyap_ek_last_error")
@@ -57,6 +58,8 @@ def _load():
     lib.lyap_trace_batch.restype = C.c_int
     lib.lyap_trace_batch_ex.argtypes = [P, C.c_int64, P, P, P, P, P, C.c_int, P]
     lib.lyap_trace_batch_ex.restype = C.c_int
+    lib.lyap_trace_batch_x.argtypes = [P, C.c_int64, P, P, P, P, P, P, P, P]
+    lib.lyap_trace_batch_x.restype = C.c_int
     lib.lyap_get_info.argtypes = [P, C.POINTER(Info)]
     lib.lyap_get_info.restype = C.c_int
     lib.lyap_get_stats.argtypes = [P, C.POINTER(Stats)]

@@ -49,7 +49,8 @@ struct EngArgs {
   int* qctr;      // shared by all slot groups: [0] next queue position, [1] finished v's
   double *cs, *sn;  // Givens rotations (b x mmax each)
   double* traces;
-  double* gout;  // optional (lyap_solution): nv x L, the solved folded g of every v
+  double* gout;  // optional (lyap_solution, lyap_trace_batch_x): nv x L, the solved folded g of every v
+  const double* x0;  // optional (lyap_trace_batch_x): nv x L initial guesses (solution recycling, f3)
   int32_t* status;
   int32_t* out_applies;
   double* out_resid;
@@ -104,7 +105,7 @@ __global__ void k_assign(EngArgs a) {
       a.newv[tid] = 1;
       // cold start (g = 0): the first residual is the right-hand side itself -- START forms it
       // without a T-apply; a warm start must verify its initial iterate through K1
-      a.phase[tid] = a.warm ? PH_VERIFY : PH_START;
+      a.phase[tid] = (a.warm || a.x0) ? PH_VERIFY : PH_START;
       int r = a.regq ? a.regq[qpos] : -1;
       bool nomask = true;
       for (int t = 0; t < a.K; ++t) nomask = nomask && (a.V[(int64_t)idx * a.K + t] != 0.0);
@@ -229,7 +230,14 @@ __global__ void __launch_bounds__(128) k_pfactor(EngArgs a) {
     invert_block<2 * K, K>(pb, a.mask + slot * K, a.sigma + slot * K, out);
   else
     invert_block<K, K>(pb, a.mask + slot * K, a.sigma + slot * K, out);
-  if (!a.warm) {
+  if (a.x0) {  // caller's initial guess for this v (masked rows: column t absent -> 0)
+    const int64_t c = rep_coord(rep, a.npairs);
+    const int w = pair ? 2 : 1;
+    const double* g = a.x0 + (int64_t)a.vidx[slot] * a.L;
+    for (int t = 0; t < K; ++t)
+      for (int q = 0; q < w; ++q)
+        a.X[(int64_t)slot * a.L + t * a.npad + c + q] = a.mask[slot * K + t] != 0.0 ? g[t * a.npad + c + q] : 0.0;
+  } else if (!a.warm) {
     const int64_t c = rep_coord(rep, a.npairs);
     const int w = pair ? 2 : 1;
     for (int t = 0; t < K; ++t)

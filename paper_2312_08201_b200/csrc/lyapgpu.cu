@@ -294,7 +294,7 @@ void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, cudaEvent_t evb 
 // ------------------------------------------------------------------ the batched engine
 int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, double* dtr, int32_t* dst,
               int32_t* dap, double* dres, cudaStream_t user_st, double* gout = nullptr, const int* dregq = nullptr,
-              int record = 0) {
+              int record = 0, const double* x0 = nullptr) {
   // the engine runs on the library's own streams (graph capture is illegal on the legacy default
   // stream a caller may pass); it is ordered after, and the caller's stream after it, by events
   cudaStream_t st = ctx->stream;
@@ -343,6 +343,7 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   a.out_applies = dap;
   a.out_resid = dres;
   a.gout = gout;
+  a.x0 = x0;
   a.record = record;
   a.s_rec = ctx->nreg > 0 ? ctx->s_rec : 0;
   a.Ureg = ctx->Ureg;
@@ -1027,8 +1028,9 @@ int lyap_setup_like(const lyap_ctx* base, int64_t k, const double* Bl, const dou
   return LYAP_OK;
 }
 
-int lyap_trace_batch_ex(lyap_ctx* ctx, int64_t nv, const double* V, double* traces, int32_t* status,
-                        int32_t* applies, double* resid, int v_on_device, void* cuda_stream) {
+static int trace_batch_impl(lyap_ctx* ctx, int64_t nv, const double* V, double* traces, int32_t* status,
+                            int32_t* applies, double* resid, int v_on_device, void* cuda_stream, const double* x0,
+                            double* xout) {
   if (!ctx) {
     set_err(nullptr, "lyap_trace_batch: ctx is NULL");
     return LYAP_EINVAL;
@@ -1129,8 +1131,8 @@ int lyap_trace_batch_ex(lyap_ctx* ctx, int64_t nv, const double* V, double* trac
         LAUNCHED();
       }
     }
-    rc = run_batch(ctx, nv, dV, dorder, dtr, dst, dap, dres, st, nullptr,
-                   (ctx->nreg > 0 && dorder) ? ctx->eng.regq : nullptr);
+    rc = run_batch(ctx, nv, dV, dorder, dtr, dst, dap, dres, st, xout,
+                   (ctx->nreg > 0 && dorder) ? ctx->eng.regq : nullptr, 0, x0);
     if (rc == LYAP_OK) {
       // any per-v failure -> LYAP_EPARTIAL
       std::vector<int32_t> hs;
@@ -1169,6 +1171,16 @@ int lyap_trace_batch_ex(lyap_ctx* ctx, int64_t nv, const double* V, double* trac
     dfree(dres);
   }
   return rc;
+}
+
+int lyap_trace_batch_ex(lyap_ctx* ctx, int64_t nv, const double* V, double* traces, int32_t* status,
+                        int32_t* applies, double* resid, int v_on_device, void* cuda_stream) {
+  return trace_batch_impl(ctx, nv, V, traces, status, applies, resid, v_on_device, cuda_stream, nullptr, nullptr);
+}
+
+int lyap_trace_batch_x(lyap_ctx* ctx, int64_t nv, const double* V, const double* X0, double* Xout, double* traces,
+                       int32_t* status, int32_t* applies, double* resid, void* cuda_stream) {
+  return trace_batch_impl(ctx, nv, V, traces, status, applies, resid, 1, cuda_stream, X0, Xout);
 }
 
 int lyap_trace_batch(lyap_ctx* ctx, int64_t nv, const double* V, double* traces, int32_t* status,
