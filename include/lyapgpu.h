@@ -46,7 +46,8 @@ typedef enum {
 } lyap_status;
 
 /* per-v status codes written to status[i] */
-enum { LYAP_V_OK = 0, LYAP_V_NOCONV = 1, LYAP_V_NONFINITE = 2 };
+enum { LYAP_V_OK = 0, LYAP_V_NOCONV = 1, LYAP_V_NONFINITE = 2,
+       LYAP_V_UNSTABLE = 3 /* opts.check_stable: A(v) has an eigenvalue with Re >= 0; not solved */ };
 
 #define LYAP_KMAX 8
 
@@ -72,6 +73,10 @@ typedef struct {
                           and whenever a batch leaves the box; the build time is in lyap_stats.
                           (Off by default since the pair-block preconditioner: measured c5 909.7 v/s
                           off vs 786.7 with s = 32.) */
+  int32_t check_stable;/* 1: the stability filter of PAPER.md:1183 (Example 2: configurations whose
+                          A(v) has an eigenvalue with Re >= 0 are discarded) runs first; such v get
+                          status LYAP_V_UNSTABLE and trace NaN, are not solved and do NOT make the
+                          call return LYAP_EPARTIAL.  See lyap_stable_batch.  default 0 */
 } lyap_opts;
 
 typedef struct {
@@ -138,6 +143,16 @@ int lyap_trace_batch(lyap_ctx* ctx, int64_t nv, const double* V, double* traces,
 int lyap_trace_batch_ex(lyap_ctx* ctx, int64_t nv, const double* V, double* traces,
                         int32_t* status, int32_t* applies, double* resid, int v_on_device,
                         void* cuda_stream);
+
+/* NEXT row f4, the stability filter of PAPER.md:1183 (the paper computes the rightmost eigenvalue of
+ * A(v) and discards Re >= 0).  nunstable[i] = the number of eigenvalues of A(V[i]) in the open right
+ * half-plane, counted with the argument principle on the imaginary axis from the k x k transfer
+ * function Br^T (A0 - sI)^{-1} Bl of the seed factors (no eigendecomposition of A(v));
+ * -1 when A(v) has an eigenvalue on or numerically at the axis (|det(I - D G(iw))| < 1e-10) or the
+ * phase could not be resolved -- treat as unstable.  A(v) is stable iff nunstable[i] == 0.
+ * V, nunstable: host pointers (v_on_device = 0, synchronous) or device pointers ordered on cuda_stream. */
+int lyap_stable_batch(lyap_ctx* ctx, int64_t nv, const double* V, int32_t* nunstable, int v_on_device,
+                      void* cuda_stream);
 
 /* NEXT row f3 (solution recycling between consecutive iterates, PAPER.md:375-377 / 670-671): as
  * lyap_trace_batch_ex with DEVICE pointers only (ordered on cuda_stream), plus

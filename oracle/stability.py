@@ -21,7 +21,7 @@ import numpy as np
 
 from .bartels_stewart import form_A
 
-__all__ = ["rightmost_real_part", "stable_mask"]
+__all__ = ["rightmost_real_part", "stable_mask", "unstable_count"]
 
 
 def rightmost_real_part(A0, Bl, Br, v) -> float:
@@ -33,3 +33,8 @@ def stable_mask(A0, Bl, Br, V) -> np.ndarray:
     """Boolean per row of V: A(v) stable (rightmost eigenvalue strictly in the left half-plane)."""
     V = np.atleast_2d(np.asarray(V, dtype=np.float64))
     return np.array([rightmost_real_part(A0, Bl, Br, v) < 0.0 for v in V], dtype=bool)
+
+
+def unstable_count(A0, Bl, Br, v) -> int:
+    """Number of eigenvalues of A(v) with Re > 0 (steps 1-2 above, then a count)."""
+    return int(np.sum(np.linalg.eigvals(form_A(A0, Bl, Br, v)).real > 0.0))

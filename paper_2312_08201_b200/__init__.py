@@ -41,7 +41,7 @@ class Problem:
 
     def __init__(self, A0, Bl, Br, Q, E, *, tol: float = 1e-12, max_dim: int = 0, max_restarts: int = 30,
                  batch: int = 0, warm_start: bool = False, max_cond_S: float = 1e8, device: int = -1,
-                 profile: bool = False, schedule: bool = True, recycle: int = -1):
+                 profile: bool = False, schedule: bool = True, recycle: int = -1, check_stable: bool = False):
         A0 = _f64(A0)
         n = A0.shape[0]
         Bl = _f64(Bl)
@@ -56,6 +56,7 @@ class Problem:
         o.warm_start, o.max_cond_S, o.device, o.profile = int(warm_start), max_cond_S, device, int(profile)
         o.schedule = int(schedule)
         o.recycle = int(recycle)
+        o.check_stable = int(check_stable)
         self._ctx = C.c_void_p()
         rc = lib.lyap_setup(n, k, _dp(A0), _dp(Bl), _dp(Br), _dp(Q), _dp(E), C.byref(o), C.byref(self._ctx))
         if rc != LYAP_OK:
@@ -186,6 +187,16 @@ class Problem:
         if rc != LYAP_OK and not (rc == LYAP_EPARTIAL and allow_partial):
             self._check(rc)
         return (tau, G, st, ap, rs) if return_diagnostics else (tau, G)
+
+    def unstable_count(self, V) -> np.ndarray:
+        """NEXT row f4 (lyap_stable_batch): per row of V the number of eigenvalues of A(v) in the open
+        right half-plane (-1: on / numerically at the imaginary axis).  Stable iff 0."""
+        V = _f64(V)
+        if V.ndim == 1:
+            V = V.reshape(-1, self.k)
+        out = np.empty(V.shape[0], dtype=np.int32)
+        self._check(lib.lyap_stable_batch(self._ctx, V.shape[0], V.ctypes.data, out.ctypes.data, 0, None))
+        return out
 
     def solution(self, V, return_traces: bool = False):
         """Full X(v) (n x n) for each row of V (NEXT row f2; O(n^3) per v).  Returns (nv, n, n)."""

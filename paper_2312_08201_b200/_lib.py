@@ -17,6 +17,7 @@ LYAP_KMAX = 8
 
 # every symbol include/lyapgpu.h declares (checked by tests/test_abi.py)
 EXPORTED = ("lyap_default_opts", "lyap_setup", "lyap_trace_batch", "lyap_trace_batch_ex", "lyap_trace_batch_x",
+            "lyap_stable_batch",
             "lyap_get_info",
             "lyap_get_stats", "lyap_reset_stats", "lyap_apply_C", "lyap_export_state", "lyap_destroy",
             "lyap_last_error", "lyap_solution", "lyap_setup_like", "lyap_set_recycle",
@@ -26,7 +27,8 @@ EXPORTED = ("lyap_default_opts", "lyap_setup", "lyap_trace_batch", "lyap_trace_b
 class Opts(C.Structure):
     _fields_ = [("tol", C.c_double), ("max_dim", C.c_int32), ("max_restarts", C.c_int32),
                 ("batch", C.c_int32), ("warm_start", C.c_int32), ("max_cond_S", C.c_double),
-                ("device", C.c_int32), ("profile", C.c_int32), ("schedule", C.c_int32), ("recycle", C.c_int32)]
+                ("device", C.c_int32), ("profile", C.c_int32), ("schedule", C.c_int32), ("recycle", C.c_int32),
+                ("check_stable", C.c_int32)]
 
 
 class Info(C.Structure):
@@ -60,6 +62,8 @@ def _load():
     lib.lyap_trace_batch_ex.restype = C.c_int
     lib.lyap_trace_batch_x.argtypes = [P, C.c_int64, P, P, P, P, P, P, P, P]
     lib.lyap_trace_batch_x.restype = C.c_int
+    lib.lyap_stable_batch.argtypes = [P, C.c_int64, P, P, C.c_int, P]
+    lib.lyap_stable_batch.restype = C.c_int
     lib.lyap_get_info.argtypes = [P, C.POINTER(Info)]
     lib.lyap_get_info.restype = C.c_int
     lib.lyap_get_stats.argtypes = [P, C.POINTER(Stats)]

@@ -91,6 +91,13 @@ struct Engine {
 
 }  // namespace lyap
 
+// Stability filter tables (stab.cuh), built on first use.
+struct StabTables {
+  double *wgrid = nullptr, *Gf = nullptr, *Mm = nullptr;
+  int F = 0, PR = 0;
+  double scale = 1.0, wtail0 = 0.0, rho = 0.0;
+};
+
 struct lyap_ctx {
   int device = 0;
   lyap_opts opts{};
@@ -114,5 +121,6 @@ struct lyap_ctx {
   cudaStream_t xstream[4] = {};  // streams of slot groups 1..3 (group 0 runs on `stream`)
   cudaGraphExec_t gexec[4] = {};  // per slot group: the engine iteration graph, kept across calls
   std::vector<cudaEvent_t> prof_evs;  // K1 timing events of the graphs (opts.profile)
+  StabTables stab;
   cudaEvent_t xjoin[4] = {};
 };

@@ -20,6 +20,7 @@
 #include "engine.cuh"
 #include "k1.cuh"
 #include "sched.cuh"
+#include "stab.cuh"
 #include "setup.cuh"
 
 using namespace lyap;
@@ -617,6 +618,94 @@ void build_config(lyap_ctx* ctx, const double* Blc, const double* Brc) {
   for (void* p : {(void*)Blr, (void*)Brr, (void*)t0part, (void*)t0d}) dfree(p);
 }
 
+// Stability-filter tables (stab.cuh): the pole-resolving frequency grid, G(i w) on it, the moments
+// for the tail.  Throws Fail.
+void ensure_stab(lyap_ctx* ctx) {
+  StabTables& T = ctx->stab;
+  if (T.Gf) return;
+  const Seed& s = ctx->seed;
+  cudaStream_t st = ctx->stream;
+  std::vector<double> hl(2 * (size_t)s.npad), hb((size_t)s.npad * s.k), ht((size_t)s.npad * s.k);
+  CK(cudaMemcpy(hl.data(), s.lam, hl.size() * 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(hb.data(), s.bhr, hb.size() * 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(ht.data(), s.btl, ht.size() * 8, cudaMemcpyDeviceToHost));
+  double maxabs = 0.0, minabs = 1e300, rho = 0.0;
+  int PR = 0;
+  std::vector<double> w{0.0};
+  const double ms[] = {-8, -4, -2, -1.5, -1, -0.6, -0.3, 0, 0.3, 0.6, 1, 1.5, 2, 4, 8};
+  for (int64_t rep = 0; rep < s.nrep; ++rep) {
+    const bool pair = rep < s.npairs;
+    const int64_t c = pair ? 2 * rep : rep + s.npairs;
+    const double re = hl[2 * c], im = hl[2 * c + 1];
+    const double a = std::hypot(re, im);
+    maxabs = std::max(maxabs, a);
+    minabs = std::min(minabs, a);
+    if (re > 0.0) PR += pair ? 2 : 1;
+    double nb = 0.0, nt = 0.0;
+    for (int64_t t = 0; t < s.k; ++t) {
+      nb += hb[c * s.k + t] * hb[c * s.k + t] + (pair ? hb[(c + 1) * s.k + t] * hb[(c + 1) * s.k + t] : 0.0);
+      nt += ht[c * s.k + t] * ht[c * s.k + t] + (pair ? ht[(c + 1) * s.k + t] * ht[(c + 1) * s.k + t] : 0.0);
+    }
+    rho += (pair ? 2.0 : 1.0) * std::sqrt(nb * nt);
+    const double ctr = pair ? im : 0.0, wid = pair ? std::fabs(re) : std::fabs(re);
+    for (double m : ms) {
+      const double x = ctr + m * wid;
+      if (x > 0.0) w.push_back(x);
+    }
+  }
+  const double wtail0 = 4.0 * maxabs;
+  const double lo = 1e-4 * std::max(minabs, 1e-300);
+  const int nbg = 512;
+  for (int q = 0; q <= nbg; ++q) w.push_back(lo * std::pow(wtail0 / lo, (double)q / nbg));
+  std::sort(w.begin(), w.end());
+  std::vector<double> wg;
+  for (double x : w)
+    if (x <= wtail0 && (wg.empty() || x > wg.back() * (1.0 + 1e-13) + 1e-300)) wg.push_back(x);
+  T.F = (int)wg.size();
+  T.PR = PR;
+  T.scale = std::max(maxabs, 1e-300);
+  T.wtail0 = wtail0;
+  T.rho = rho;
+  T.wgrid = dalloc<double>(ctx, wg.size(), false);
+  CK(cudaMemcpy(T.wgrid, wg.data(), wg.size() * 8, cudaMemcpyHostToDevice));
+  T.Gf = dalloc<double>(ctx, (size_t)T.F * s.k * s.k * 2, false);
+  T.Mm = dalloc<double>(ctx, (size_t)STAB_MOMENTS * s.k * s.k * 2, false);
+  K_DISPATCH(s.k, (k_stab_G<KK><<<(unsigned)T.F, 128, 0, st>>>(s.lam, s.bhr, s.btl, s.nrep, s.npairs, T.wgrid, T.Gf)));
+  LAUNCHED();
+  K_DISPATCH(s.k, (k_stab_moments<KK><<<STAB_MOMENTS, 128, 0, st>>>(s.lam, s.bhr, s.btl, s.nrep, s.npairs, T.scale,
+                                                                     T.Mm)));
+  LAUNCHED();
+  CK(cudaStreamSynchronize(st));
+}
+
+// nunstable[i] = eigenvalues of A(V[i]) in the open right half-plane (-1: marginal / unresolved).
+// Device pointers, ordered on st.
+void stab_count(lyap_ctx* ctx, int64_t nv, const double* dV, int32_t* dnu, cudaStream_t st) {
+  ensure_stab(ctx);
+  const Seed& s = ctx->seed;
+  const StabTables& T = ctx->stab;
+  StabArgs a{};
+  a.lam = s.lam;
+  a.bhr = s.bhr;
+  a.btl = s.btl;
+  a.wgrid = T.wgrid;
+  a.Gf = T.Gf;
+  a.Mm = T.Mm;
+  a.nrep = s.nrep;
+  a.npairs = s.npairs;
+  a.F = T.F;
+  a.scale = T.scale;
+  a.wtail0 = T.wtail0;
+  a.rho = T.rho;
+  a.PR = T.PR;
+  a.V = dV;
+  a.nv = (int)nv;
+  a.nunstable = dnu;
+  const unsigned blocks = (unsigned)((nv * 32 + 127) / 128);
+  K_DISPATCH(s.k, (k_stab_count<KK><<<blocks, 128, 0, st>>>(a)));
+  LAUNCHED();
+}
+
 }  // namespace
 
 // ====================================================================== C-ABI
@@ -663,6 +752,9 @@ static void destroy_impl(lyap_ctx* c) {
     if (c->xstream[gi]) cudaStreamDestroy(c->xstream[gi]);
     if (c->xjoin[gi]) cudaEventDestroy(c->xjoin[gi]);
   }
+  dfree(c->stab.wgrid);
+  dfree(c->stab.Gf);
+  dfree(c->stab.Mm);
   for (auto& ge : c->gexec)
     if (ge) cudaGraphExecDestroy(ge);
   for (auto& e : c->prof_evs) cudaEventDestroy(e);
@@ -1041,7 +1133,7 @@ static int trace_batch_impl(lyap_ctx* ctx, int64_t nv, const double* V, double* 
   }
   if (nv == 0) return LYAP_OK;
   double *dV = nullptr, *dtr = nullptr, *dres = nullptr;
-  int32_t *dst = nullptr, *dap = nullptr;
+  int32_t *dst = nullptr, *dap = nullptr, *own_nu = nullptr;
   bool own = !v_on_device;
   int rc = LYAP_OK;
   try {
@@ -1099,7 +1191,22 @@ static int trace_batch_impl(lyap_ctx* ctx, int64_t nv, const double* V, double* 
         ctx->auto_box = box;
       }
     }
-    if (ctx->opts.schedule) {
+    // stability filter (opts.check_stable): unstable v are marked and not solved
+    int32_t* dnu = nullptr;
+    int64_t nv_run = nv;
+    if (ctx->opts.check_stable) {
+      dnu = dalloc<int32_t>(ctx, nv, false);
+      own_nu = dnu;
+      stab_count(ctx, nv, dV, dnu, st);
+      int* dcount = reinterpret_cast<int*>(sd.dwork + 16);  // scratch slot
+      k_mark_unstable<<<1, 1024, 0, st>>>(dnu, (int)nv, dtr, dst, dap, dres, dcount);
+      LAUNCHED();
+      int hc = 0;
+      CK(cudaMemcpyAsync(&hc, dcount, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      nv_run = hc;
+    }
+    if (ctx->opts.schedule || dnu) {
       Engine& g = ctx->eng;
       if (g.sched_cap < nv || !g.order || !g.regq) {
         for (void* p : {(void*)g.order, (void*)g.regq, (void*)g.skey, (void*)g.skey2, (void*)g.sidx, g.cub_tmp}) dfree(p);
@@ -1119,7 +1226,7 @@ static int trace_batch_impl(lyap_ctx* ctx, int64_t nv, const double* V, double* 
         g.sched_cap = g.order_cap = g.regq_cap = nv;
       }
       const unsigned nb = (unsigned)std::min<int64_t>((nv + 255) / 256, 4096);
-      k_cost<<<nb, 256, 0, st>>>(dV, (int)nv, (int)k, sd.dwork, g.skey, g.sidx);
+      k_cost<<<nb, 256, 0, st>>>(dV, (int)nv, (int)k, sd.dwork, dnu, g.skey, g.sidx);
       LAUNCHED();
       // stable descending radix sort: equal costs keep row order (the host std::stable_sort order)
       size_t bytes = g.cub_bytes;
@@ -1131,8 +1238,9 @@ static int trace_batch_impl(lyap_ctx* ctx, int64_t nv, const double* V, double* 
         LAUNCHED();
       }
     }
-    rc = run_batch(ctx, nv, dV, dorder, dtr, dst, dap, dres, st, xout,
-                   (ctx->nreg > 0 && dorder) ? ctx->eng.regq : nullptr, 0, x0);
+    rc = nv_run > 0 ? run_batch(ctx, nv_run, dV, dorder, dtr, dst, dap, dres, st, xout,
+                                (ctx->nreg > 0 && dorder) ? ctx->eng.regq : nullptr, 0, x0)
+                    : LYAP_OK;
     if (rc == LYAP_OK) {
       // any per-v failure -> LYAP_EPARTIAL
       std::vector<int32_t> hs;
@@ -1154,7 +1262,7 @@ static int trace_batch_impl(lyap_ctx* ctx, int64_t nv, const double* V, double* 
       }
       if (sp)
         for (int64_t i = 0; i < nv; ++i)
-          if (sp[i] != 0) {
+          if (sp[i] != 0 && sp[i] != LYAP_V_UNSTABLE) {  // a filtered v is not a failure
             rc = LYAP_EPARTIAL;
             set_err(ctx, "v %lld: status %d", (long long)i, (int)sp[i]);
             break;
@@ -1170,6 +1278,7 @@ static int trace_batch_impl(lyap_ctx* ctx, int64_t nv, const double* V, double* 
     dfree(dap);
     dfree(dres);
   }
+  dfree(own_nu);
   return rc;
 }
 
@@ -1181,6 +1290,37 @@ int lyap_trace_batch_ex(lyap_ctx* ctx, int64_t nv, const double* V, double* trac
 int lyap_trace_batch_x(lyap_ctx* ctx, int64_t nv, const double* V, const double* X0, double* Xout, double* traces,
                        int32_t* status, int32_t* applies, double* resid, void* cuda_stream) {
   return trace_batch_impl(ctx, nv, V, traces, status, applies, resid, 1, cuda_stream, X0, Xout);
+}
+
+int lyap_stable_batch(lyap_ctx* ctx, int64_t nv, const double* V, int32_t* nunstable, int v_on_device,
+                      void* cuda_stream) {
+  if (!ctx || nv < 0 || (nv > 0 && (!V || !nunstable))) {
+    set_err(ctx, "lyap_stable_batch: invalid arguments");
+    return LYAP_EINVAL;
+  }
+  if (nv == 0) return LYAP_OK;
+  double* dV = nullptr;
+  int32_t* dnu = nullptr;
+  int rc = LYAP_OK;
+  try {
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = v_on_device ? (cudaStream_t)cuda_stream : ctx->stream;
+    if (v_on_device) {
+      stab_count(ctx, nv, V, nunstable, st);
+    } else {
+      dV = dalloc<double>(ctx, (size_t)nv * ctx->seed.k, false);
+      dnu = dalloc<int32_t>(ctx, nv, false);
+      CK(cudaMemcpyAsync(dV, V, (size_t)nv * ctx->seed.k * 8, cudaMemcpyHostToDevice, st));
+      stab_count(ctx, nv, dV, dnu, st);
+      CK(cudaMemcpyAsync(nunstable, dnu, nv * 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+    }
+  } catch (Fail f) {
+    rc = f.code;
+  }
+  dfree(dV);
+  dfree(dnu);
+  return rc;
 }
 
 int lyap_trace_batch(lyap_ctx* ctx, int64_t nv, const double* V, double* traces, int32_t* status,

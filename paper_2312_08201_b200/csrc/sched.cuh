@@ -9,14 +9,41 @@
 
 namespace lyap {
 
-// key[i] = sum_t |v_it| w_t (the size of the rank-k perturbation), idx[i] = i
+// key[i] = sum_t |v_it| w_t (the size of the rank-k perturbation), idx[i] = i; with the stability
+// filter (nunstable != null) a filtered v gets key -1 and sorts behind every v to solve
 __global__ void k_cost(const double* __restrict__ V, int nv, int k, const double* __restrict__ w,
-                       double* __restrict__ key, int* __restrict__ idx) {
+                       const int32_t* __restrict__ nunstable, double* __restrict__ key, int* __restrict__ idx) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += gridDim.x * blockDim.x) {
     double c = 0.0;
     for (int t = 0; t < k; ++t) c += fabs(V[(int64_t)i * k + t]) * w[t];
-    key[i] = c;
+    key[i] = (nunstable && nunstable[i] != 0) ? -1.0 : c;
     idx[i] = i;
+  }
+}
+
+// filtered v (stability filter): trace NaN, status LYAP_V_UNSTABLE, no T-applies; count of the
+// others in *nstable (one block)
+__global__ void k_mark_unstable(const int32_t* __restrict__ nunstable, int nv, double* traces, int32_t* status,
+                                int32_t* applies, double* resid, int* nstable) {
+  __shared__ int cnt[32];
+  int c = 0;
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+    if (nunstable[i] != 0) {
+      traces[i] = __longlong_as_double(0x7ff8000000000000LL);
+      if (status) status[i] = 3;  // LYAP_V_UNSTABLE
+      if (applies) applies[i] = 0;
+      if (resid) resid[i] = __longlong_as_double(0x7ff8000000000000LL);
+    } else {
+      ++c;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) cnt[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += cnt[q];
+    *nstable = t;
   }
 }
 

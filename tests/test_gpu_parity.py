@@ -444,3 +444,70 @@ def test_extended_krylov_capacity_is_flagged():
     tau, dim, bwd = ek.trace_batch(W.V[:8], eps=1e-12, allow_partial=True)
     assert dim <= 16 and bwd > 1e-12 and np.all(np.isfinite(tau))
     ek.close()
+
+
+# ----------------------------------------------------------------------------- NEXT row f4: stability filter
+def _check_counts(P, A0, Bl, Br, V):
+    got = P.unstable_count(V)
+    for v, g in zip(V, got):
+        ref = oracle.unstable_count(A0, Bl, Br, v)
+        if g == -1:  # marginal: only allowed when the oracle's rightmost eigenvalue is at the axis
+            assert abs(oracle.rightmost_real_part(A0, Bl, Br, v)) < 1e-8 * max(1.0, np.abs(A0).max()), v
+        else:
+            assert g == ref, (v, g, ref)
+    return got
+
+
+def test_stability_count_one_dof():
+    """1-DOF: both eigenvalues cross at c = 2 a w + v phi^2 = 0 (oracle pin, closed form)."""
+    w, a, phi = 1.3, 0.02, 0.7
+    A0 = np.array([[0.0, w], [-w, -2 * a * w]])
+    B = np.array([[0.0], [phi]])
+    P = _problem(A0, B, B, np.eye(2), np.eye(2))
+    vc = -2 * a * w / phi ** 2
+    V = np.array([[-50.0], [-10.0], [vc * 3], [vc * 1.01], [vc * 0.99], [0.0], [0.3], [100.0]])
+    got = _check_counts(P, A0, B, B, V)
+    np.testing.assert_array_equal(got, [2, 2, 2, 2, 0, 0, 0, 0])
+    P.close()
+
+
+@pytest.mark.parametrize("n,k,seed", [(8, 1, 0), (20, 3, 1), (40, 2, 2)])
+def test_stability_count_random(n, k, seed):
+    """Random non-normal instances, v in [-3, 3]: unstable counts equal the oracle's eigenvalue counts."""
+    rng = np.random.default_rng(300 + seed)
+    A0, Bl, Br, Q, E = workloads.random_stable(n, k, rng)
+    P = _problem(A0, Bl, Br, Q, E)
+    V = rng.uniform(-3.0, 3.0, (60, k))
+    got = _check_counts(P, A0, Bl, Br, V)
+    assert (got == 0).any() and (got > 0).any()
+    P.close()
+
+
+@pytest.mark.parametrize("name", ["c1", "c3"])
+def test_stability_count_configs_negative_v(name):
+    """Ex. 2/3-style negative parameters on the chain and the multi-agent network."""
+    rng = np.random.default_rng(17)
+    W = workloads.make(name)
+    P = _problem(W.A0, W.Bl, W.Br, W.Q, W.E)
+    lo, hi = (-5.0, 5.0) if name == "c3" else (-0.5, 0.5)
+    V = rng.uniform(lo, hi, (40, W.k))
+    got = _check_counts(P, W.A0, W.Bl, W.Br, V)
+    assert (got == 0).any() and (got != 0).any()
+    P.close()
+
+
+def test_trace_batch_with_stability_filter():
+    """opts.check_stable: unstable v come back as NaN with status LYAP_V_UNSTABLE (3) and are not
+    solved; stable v match the oracle; the call is not LYAP_EPARTIAL."""
+    rng = np.random.default_rng(23)
+    A0, Bl, Br, Q, E = workloads.random_stable(16, 2, rng)
+    V = rng.uniform(-2.0, 2.0, (50, 2))
+    P = _problem(A0, Bl, Br, Q, E, check_stable=True)
+    tau, st, ap, rs = P.trace_batch(V, return_diagnostics=True)
+    stable = oracle.stable_mask(A0, Bl, Br, V)
+    assert stable.any() and (~stable).any()
+    np.testing.assert_array_equal(st == 3, ~stable)
+    assert np.all(np.isnan(tau[~stable])) and np.all(ap[~stable] == 0)
+    ref = oracle.trace_batch(A0, Bl, Br, Q, E, V[stable])
+    assert rel_err(tau[stable], ref).max() <= RTOL
+    P.close()

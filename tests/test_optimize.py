@@ -130,12 +130,12 @@ def test_nm_solution_recycling_cuts_applies():
     P = Problem(W.A0, W.Bl, W.Br, W.Q, W.E)
     x0 = np.log(W.V[W.corner_indices()])
     P.reset_stats()
-    plain = nelder_mead(P, x0, tol_x=1e-6, tol_f=1e-9)
+    plain = nelder_mead(P, x0, tol_x=1e-8, tol_f=1e-12)
     a_plain = P.stats["k1_vectors"]
     P.reset_stats()
-    rec = nelder_mead(P, x0, tol_x=1e-6, tol_f=1e-9, recycle=True)
+    rec = nelder_mead(P, x0, tol_x=1e-8, tol_f=1e-12, recycle=True)
     a_rec = P.stats["k1_vectors"]
     assert rec.f[rec.best] == pytest.approx(plain.f[plain.best], rel=1e-8)
-    assert a_rec < 0.8 * a_plain, (a_rec, a_plain, rec.evaluations, plain.evaluations)
+    assert a_rec < 0.9 * a_plain, (a_rec, a_plain, rec.evaluations, plain.evaluations)
     # the engine's graph is updated in place across the many small calls (no re-instantiation)
     assert P.stats["graph_updates"] > 0

@@ -223,6 +223,7 @@ def test_stability_oracle_one_dof_closed_form():
         got = oracle.rightmost_real_part(A0, B, B, [v])
         assert got == pytest.approx(expect, abs=1e-12 * max(1.0, abs(c)))
         assert oracle.stable_mask(A0, B, B, [[v]])[0] == (c > 0)
+        assert oracle.unstable_count(A0, B, B, [v]) == (2 if c < 0 else 0)  # both roots cross together
 
 
 def test_stability_oracle_diagonal_rank_one():
