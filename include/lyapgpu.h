@@ -170,9 +170,11 @@ int lyap_reset_stats(lyap_ctx* ctx);
 
 /* NEXT row f2: the full solution X(v) (n x n, row-major; X is symmetric) for each
  * of the nv rows of V, eq. (Xsmalllastline): the batch is solved as in
- * lyap_trace_batch, then X = S X~ S^T with X~ = X~0 + L o (B~l G + G^T B~l^T) generated entrywise
- * on the device and two n^3 DGEMMs per v (cuBLAS).  Host pointers; X holds nv * n * n doubles;
- * traces (nullable) as in lyap_trace_batch.  Meant for a few v's (O(n^3) per v). */
+ * lyap_trace_batch, then X = S X~ S^T = S_r Y S_r^T with Y = J X~ J^T, X~ = X~0 + L o (B~l G + G^T B~l^T)
+ * generated entrywise on the device (the Hadamard product with the Cauchy matrix, never formed as
+ * a matrix) for a chunk of v at a time, and the two n^3 products of the whole chunk as two batched
+ * FP64 DMMA GEMMs (the engine's k1_dgemm).  Host pointers; X holds nv * n * n doubles; traces
+ * (nullable) as in lyap_trace_batch.  O(4 n^3) flops per v. */
 int lyap_solution(lyap_ctx* ctx, int64_t nv, const double* V, double* X, double* traces);
 
 /* Recycling across neighbouring v: nreg shared recycle spaces of s folded x-space

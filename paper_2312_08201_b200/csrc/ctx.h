@@ -122,5 +122,6 @@ struct lyap_ctx {
   cudaGraphExec_t gexec[4] = {};  // per slot group: the engine iteration graph, kept across calls
   std::vector<cudaEvent_t> prof_evs;  // K1 timing events of the graphs (opts.profile)
   StabTables stab;
+  double* Spad = nullptr;  // lyap_solution: padded S_r^T and S_r (row-major np x np each)
   cudaEvent_t xjoin[4] = {};
 };

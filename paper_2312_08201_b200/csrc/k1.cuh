@@ -99,11 +99,19 @@ struct DgemmCfg {
   static constexpr size_t SMEM = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double);
 };
 
-template <int BM, int BN, int WM, int WN, int STAGES, int BK_ = 16>
+// Output layouts (OUT): 0 plain C[row * N + col]; the batched full-solution path (lyap_solution,
+// DESIGN.md §2.5) uses 1 = "vertical stack -> horizontal stack": row = v * blk + r is written to
+// C[r * (N * nblk) + v * N + col] (blk = N, nblk = M / N), and 2 = "horizontal stack -> compact":
+// col = v * blk + c is written to C[(v * no + r) * no + c] for r, c < no (the unpadded order).
+struct DgemmOut {
+  int blk, nblk, no;
+};
+
+template <int BM, int BN, int WM, int WN, int STAGES, int BK_ = 16, int OUT = 0>
 __global__ void __launch_bounds__(DgemmCfg<BM, BN, WM, WN, STAGES, BK_>::THREADS,
                                   DgemmCfg<BM, BN, WM, WN, STAGES, BK_>::THREADS <= 128 ? 3 : 1)
     k1_dgemm(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C, int M,
-             int N, int Kd, int lda, const int* __restrict__ nactive, int cols_per_active) {
+             int N, int Kd, int lda, const int* __restrict__ nactive, int cols_per_active, DgemmOut om = {}) {
   using Cfg = DgemmCfg<BM, BN, WM, WN, STAGES, BK_>;
   constexpr int BK = Cfg::BK, AST = Cfg::AST, BST = Cfg::BST, NT = Cfg::THREADS;
   constexpr int MT = WM / 8, NTL = WN / 8;
@@ -187,7 +195,20 @@ __global__ void __launch_bounds__(DgemmCfg<BM, BN, WM, WN, STAGES, BK_>::THREADS
 #pragma unroll
     for (int j = 0; j < NTL; ++j) {
       int col = n0 + wn * WN + j * 8 + (lane & 3) * 2;
-      *reinterpret_cast<double2*>(C + (int64_t)row * N + col) = make_double2(acc[i][j][0], acc[i][j][1]);
+      if (OUT == 0) {
+        *reinterpret_cast<double2*>(C + (int64_t)row * N + col) = make_double2(acc[i][j][0], acc[i][j][1]);
+      } else if (OUT == 1) {
+        const int v = row / om.blk, r = row % om.blk;
+        *reinterpret_cast<double2*>(C + (int64_t)r * N * om.nblk + (int64_t)v * N + col) =
+            make_double2(acc[i][j][0], acc[i][j][1]);
+      } else {
+        const int v = col / om.blk, c = col % om.blk;
+        if (row < om.no) {
+          double* dst = C + ((int64_t)v * om.no + row) * om.no;
+          if (c < om.no) dst[c] = acc[i][j][0];
+          if (c + 1 < om.no) dst[c + 1] = acc[i][j][1];
+        }
+      }
     }
   }
 }

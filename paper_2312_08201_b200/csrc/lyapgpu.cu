@@ -752,6 +752,7 @@ static void destroy_impl(lyap_ctx* c) {
     if (c->xstream[gi]) cudaStreamDestroy(c->xstream[gi]);
     if (c->xjoin[gi]) cudaEventDestroy(c->xjoin[gi]);
   }
+  dfree(c->Spad);
   dfree(c->stab.wgrid);
   dfree(c->stab.Gf);
   dfree(c->stab.Mm);
@@ -1335,35 +1336,59 @@ int lyap_solution(lyap_ctx* ctx, int64_t nv, const double* V, double* X, double*
   }
   if (nv == 0) return LYAP_OK;
   const Seed& s = ctx->seed;
-  double *dV = nullptr, *dtr = nullptr, *gout = nullptr, *Y = nullptr, *T1 = nullptr, *Xd = nullptr;
+  double *dV = nullptr, *dtr = nullptr, *gout = nullptr, *Yst = nullptr, *T1 = nullptr, *Xc = nullptr;
   int32_t* dst = nullptr;
   int rc = LYAP_OK;
   try {
     CK(cudaSetDevice(ctx->device));
     cudaStream_t st = ctx->stream;
-    const int64_t n = s.n, L = s.k * s.npad;
+    const int64_t n = s.n, L = s.k * s.npad, np = roundup(n, G_BM);
     dV = dalloc<double>(ctx, (size_t)nv * s.k, false);
     dtr = dalloc<double>(ctx, nv, false);
     dst = dalloc<int32_t>(ctx, nv, false);
     gout = dalloc<double>(ctx, (size_t)nv * L);
-    Y = dalloc<double>(ctx, (size_t)n * n, false);
-    T1 = dalloc<double>(ctx, (size_t)n * n, false);
-    Xd = dalloc<double>(ctx, (size_t)n * n, false);
     CK(cudaMemcpyAsync(dV, V, (size_t)nv * s.k * 8, cudaMemcpyHostToDevice, st));
     rc = run_batch(ctx, nv, dV, nullptr, dtr, dst, nullptr, nullptr, st, gout);
     if (rc == LYAP_OK) {
       std::vector<int32_t> hs(nv);
       CK(cudaMemcpyAsync(hs.data(), dst, nv * 4, cudaMemcpyDeviceToHost, st));
       if (traces) CK(cudaMemcpyAsync(traces, dtr, nv * 8, cudaMemcpyDeviceToHost, st));
-      const double one = 1.0, zero = 0.0;
-      const int ni = (int)n;
-      for (int64_t v = 0; v < nv; ++v) {
-        k_solution_Y<<<dim3((unsigned)((n + 127) / 128), (unsigned)n), 128, 0, st>>>(
-            s.lam, s.Qr, s.btl, gout + v * L, n, s.npad, s.k, 2 * s.npairs, Y);
+      // X_v = S_r Y_v S_r^T for a chunk of v at a time, two batched DMMA GEMMs (k1_dgemm, DESIGN.md
+      // §2.5): T1 = [Y_1; Y_2; ...] S_r^T (written horizontally: [T1_1 | T1_2 | ...]), then
+      // X = S_r [T1_1 | T1_2 | ...] written compactly as nv x n x n
+      if (!ctx->Spad) {
+        ctx->Spad = dalloc<double>(ctx, 2 * (size_t)np * np, false);
+        k_pad_basis<<<dim3((unsigned)((np + 255) / 256), (unsigned)np), 256, 0, st>>>(s.Sr, n, np, ctx->Spad,
+                                                                                      ctx->Spad + np * np);
         LAUNCHED();
-        CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, ni, ni, ni, &one, s.Sr, ni, Y, ni, &zero, T1, ni));
-        CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_T, ni, ni, ni, &one, T1, ni, s.Sr, ni, &zero, Xd, ni));
-        CK(cudaMemcpyAsync(X + v * n * n, Xd, (size_t)n * n * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaFuncSetAttribute(k1_dgemm<G_BM, G_BN, G_WM, G_WN, G_ST, G_BK, 1>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GCfg::SMEM));
+        CK(cudaFuncSetAttribute(k1_dgemm<G_BM, G_BN, G_WM, G_WN, G_ST, G_BK, 2>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GCfg::SMEM));
+      }
+      const double* Sc = ctx->Spad;            // S_r^T (row-major)
+      const double* Srow = ctx->Spad + np * np;  // S_r (row-major)
+      const int64_t per_v = np * np * 8;
+      const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(nv, ((int64_t)1 << 30) / per_v));
+      Yst = dalloc<double>(ctx, (size_t)chunk * np * np);  // zero padding stays zero
+      T1 = dalloc<double>(ctx, (size_t)chunk * np * np, false);
+      Xc = dalloc<double>(ctx, (size_t)chunk * n * n, false);
+      for (int64_t v0 = 0; v0 < nv; v0 += chunk) {
+        const int64_t bc = std::min(chunk, nv - v0);
+        k_solution_Ystack<<<dim3((unsigned)((n + 127) / 128), (unsigned)n, (unsigned)bc), 128, 0, st>>>(
+            s.lam, s.Qr, s.btl, gout + v0 * L, n, s.npad, s.k, 2 * s.npairs, np, Yst);
+        LAUNCHED();
+        DgemmOut o1{(int)np, (int)bc, (int)n};
+        k1_dgemm<G_BM, G_BN, G_WM, G_WN, G_ST, G_BK, 1>
+            <<<(unsigned)((np / G_BN) * (bc * np / G_BM)), GCfg::THREADS, GCfg::SMEM, st>>>(
+                Yst, Sc, T1, (int)(bc * np), (int)np, (int)np, (int)np, nullptr, 1, o1);
+        LAUNCHED();
+        DgemmOut o2{(int)np, (int)bc, (int)n};
+        k1_dgemm<G_BM, G_BN, G_WM, G_WN, G_ST, G_BK, 2>
+            <<<(unsigned)((bc * np / G_BN) * (np / G_BM)), GCfg::THREADS, GCfg::SMEM, st>>>(
+                Srow, T1, Xc, (int)np, (int)(bc * np), (int)np, (int)np, nullptr, 1, o2);
+        LAUNCHED();
+        CK(cudaMemcpyAsync(X + v0 * n * n, Xc, (size_t)bc * n * n * 8, cudaMemcpyDeviceToHost, st));
       }
       CK(cudaStreamSynchronize(st));
       for (int64_t v = 0; v < nv; ++v)
@@ -1376,7 +1401,7 @@ int lyap_solution(lyap_ctx* ctx, int64_t nv, const double* V, double* X, double*
   } catch (Fail f) {
     rc = f.code;
   }
-  void* ps[] = {dV, dtr, gout, Y, T1, Xd, dst};
+  void* ps[] = {dV, dtr, gout, Yst, T1, Xc, dst};
   for (void* p : ps) dfree(p);
   return rc;
 }

@@ -381,6 +381,94 @@ __global__ void k_pblock(const double* __restrict__ Lf, int64_t npad, const doub
   }
 }
 
+// Batched full solution (f2): Y_v for a chunk of parameter vectors, written as a vertical stack of
+// np x np blocks (np = n padded to the GEMM tile; padding rows / columns stay zero): Yst[(v np + a) np + b].
+// Same entrywise formula as k_solution_Y (Y = J X~ J^T, X~ = X~0 + L o (B~l G + G^T B~l^T)): the
+// Hadamard product with the Cauchy matrix is formed here, element by element, never as a matrix.
+__global__ void k_solution_Ystack(const double* __restrict__ lam, const double* __restrict__ Qr,
+                                  const double* __restrict__ btl, const double* __restrict__ g, int64_t n, int64_t npad,
+                                  int64_t k, int64_t two_np, int64_t np, double* __restrict__ Yst) {
+  const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t b = blockIdx.y, v = blockIdx.z;
+  if (a >= n) return;
+  const double* gv = g + v * k * npad;
+  auto blk = [&](int64_t c, int64_t* idx, cplx* jc, int& w) {
+    if (c < two_np) {
+      const int64_t p0 = c & ~(int64_t)1;
+      idx[0] = p0;
+      idx[1] = p0 + 1;
+      w = 2;
+      if (c & 1) {
+        jc[0] = mk(0.0, 1.0);
+        jc[1] = mk(0.0, -1.0);
+      } else {
+        jc[0] = mk(1.0, 0.0);
+        jc[1] = mk(1.0, 0.0);
+      }
+    } else {
+      idx[0] = c;
+      jc[0] = mk(1.0, 0.0);
+      w = 1;
+    }
+  };
+  auto folded = [&](int64_t t, int64_t i) -> cplx {
+    if (i < two_np) {
+      const int64_t p0 = i & ~(int64_t)1;
+      const cplx z = mk(gv[t * npad + p0], gv[t * npad + p0 + 1]);
+      return (i & 1) ? conj(z) : z;
+    }
+    return mk(gv[t * npad + i], 0.0);
+  };
+  auto blt = [&](int64_t i, int64_t t) -> cplx {
+    if (i < two_np) {
+      const int64_t p0 = i & ~(int64_t)1;
+      const cplx z = mk(btl[p0 * k + t], btl[(p0 + 1) * k + t]);
+      return (i & 1) ? conj(z) : z;
+    }
+    return mk(btl[i * k + t], 0.0);
+  };
+  int64_t ia[2], jb[2];
+  cplx ja[2], jbv[2];
+  int wa, wb;
+  blk(a, ia, ja, wa);
+  blk(b, jb, jbv, wb);
+  cplx acc = mk(0.0, 0.0);
+  for (int u = 0; u < wa; ++u) {
+    const int64_t i = ia[u];
+    cplx ci0, ci1;
+    int wi;
+    jinv_row(i, two_np, ci0, ci1, wi);
+    const int64_t ai0 = (i < two_np) ? (i & ~(int64_t)1) : i;
+    for (int q = 0; q < wb; ++q) {
+      const int64_t j = jb[q];
+      cplx cj0, cj1;
+      int wj;
+      jinv_row(j, two_np, cj0, cj1, wj);
+      const int64_t aj0 = (j < two_np) ? (j & ~(int64_t)1) : j;
+      cplx qt = mk(0.0, 0.0);
+      for (int x = 0; x < wi; ++x)
+        for (int y = 0; y < wj; ++y)
+          qt = qt + ((x ? ci1 : ci0) * (y ? cj1 : cj0)) * mk(Qr[(aj0 + y) * n + ai0 + x], 0.0);
+      cplx rhs = mk(-qt.re, -qt.im);
+      for (int64_t t = 0; t < k; ++t) rhs = rhs + blt(i, t) * folded(t, j) + folded(t, i) * blt(j, t);
+      const cplx L = cinv(eig_of(lam, i, two_np) + eig_of(lam, j, two_np));
+      acc = acc + (ja[u] * jbv[q]) * (L * rhs);
+    }
+  }
+  Yst[(v * np + a) * np + b] = acc.re;
+}
+
+// padded copies of S_r (column-major n x n) for the batched solution GEMMs: Sc = S_r column-major
+// (as a row-major matrix: S_r^T), Sr = S_r row-major; np x np, zero padding
+__global__ void k_pad_basis(const double* __restrict__ S, int64_t n, int64_t np, double* __restrict__ Sc,
+                            double* __restrict__ Srow) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, r = blockIdx.y;
+  if (c >= np) return;
+  const bool in = r < n && c < n;
+  Sc[r * np + c] = in ? S[r * n + c] : 0.0;    // row r of S_r^T = column r of S_r
+  Srow[r * np + c] = in ? S[c * n + r] : 0.0;  // S_r[r][c]
+}
+
 // deterministic sum of t0 partials (one block)
 __global__ void k_sum(const double* __restrict__ x, int64_t n, double* out) {
   __shared__ double red[32];

@@ -276,12 +276,13 @@ def test_error_paths():
 
 
 # ----------------------------------------------------------------------------- NEXT row f2
-@pytest.mark.parametrize("case", ["c1", "random_mixed", "random_real"])
+@pytest.mark.parametrize("case", ["c1", "c2", "random_mixed", "random_real"])
 def test_full_solution_matches_oracle(case):
-    """lyap_solution: X(v) elementwise against the oracle's Bartels-Stewart X."""
+    """lyap_solution: X(v) elementwise against the oracle's Bartels-Stewart X.
+    c2 (n = 800) runs the batched DMMA GEMMs over several 128 x 128 tiles with a ragged padding."""
     rng = np.random.default_rng(31)
-    if case == "c1":
-        W = workloads.make("c1")
+    if case in ("c1", "c2"):
+        W = workloads.make(case)
         A0, Bl, Br, Q, E = W.A0, W.Bl, W.Br, W.Q, W.E
         V = W.V[W.corner_indices()]
     elif case == "random_mixed":
@@ -473,11 +474,11 @@ def test_stability_count_one_dof():
 
 @pytest.mark.parametrize("n,k,seed", [(8, 1, 0), (20, 3, 1), (40, 2, 2)])
 def test_stability_count_random(n, k, seed):
-    """Random non-normal instances, v in [-3, 3]: unstable counts equal the oracle's eigenvalue counts."""
+    """Random non-normal instances, v in [-20, 20]: unstable counts equal the oracle's eigenvalue counts."""
     rng = np.random.default_rng(300 + seed)
     A0, Bl, Br, Q, E = workloads.random_stable(n, k, rng)
     P = _problem(A0, Bl, Br, Q, E)
-    V = rng.uniform(-3.0, 3.0, (60, k))
+    V = rng.uniform(-20.0, 20.0, (60, k))
     got = _check_counts(P, A0, Bl, Br, V)
     assert (got == 0).any() and (got > 0).any()
     P.close()
@@ -489,7 +490,7 @@ def test_stability_count_configs_negative_v(name):
     rng = np.random.default_rng(17)
     W = workloads.make(name)
     P = _problem(W.A0, W.Bl, W.Br, W.Q, W.E)
-    lo, hi = (-5.0, 5.0) if name == "c3" else (-0.5, 0.5)
+    lo, hi = (-5.0, 5.0) if name == "c3" else (-5.0, 5.0)
     V = rng.uniform(lo, hi, (40, W.k))
     got = _check_counts(P, W.A0, W.Bl, W.Br, V)
     assert (got == 0).any() and (got != 0).any()
@@ -501,7 +502,7 @@ def test_trace_batch_with_stability_filter():
     solved; stable v match the oracle; the call is not LYAP_EPARTIAL."""
     rng = np.random.default_rng(23)
     A0, Bl, Br, Q, E = workloads.random_stable(16, 2, rng)
-    V = rng.uniform(-2.0, 2.0, (50, 2))
+    V = rng.uniform(-15.0, 15.0, (50, 2))
     P = _problem(A0, Bl, Br, Q, E, check_stable=True)
     tau, st, ap, rs = P.trace_batch(V, return_diagnostics=True)
     stable = oracle.stable_mask(A0, Bl, Br, V)
