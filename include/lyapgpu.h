@@ -117,6 +117,15 @@ void lyap_default_opts(lyap_opts* opts);
 int lyap_setup(int64_t n, int64_t k, const double* A0, const double* Bl, const double* Br,
                const double* Q, const double* E, const lyap_opts* opts, lyap_ctx** out);
 
+/* A right-hand side linear in v (the projected equation eq. (param_projected) of PAPER.md:581-589
+ * has Q(v) = -G (I_2 (x) D(v)) G^T = sum_i v_i Q_i): Qk holds k symmetric n x n matrices Q_1..Q_k
+ * (k x n x n, row-major) and every v is solved with Q(v) = sum_i v_i Q_i in ONE capacitance system
+ * (its right-hand side G0(v) = sum_i v_i G0_i and seed trace t0(v) = sum_i v_i t0_i are linear in v;
+ * DESIGN.md §2.7).  Everything else as lyap_setup; lyap_trace_batch*, lyap_solution work unchanged
+ * (lyap_setup_like does not take such a base).  Used by the extended-Krylov projection (f1). */
+int lyap_setup_qlin(int64_t n, int64_t k, const double* A0, const double* Bl, const double* Br, const double* Qk,
+                    const double* E, const lyap_opts* opts, lyap_ctx** out);
+
 /* NEXT row f4: a new context for the same A0, Q, E with other damper / edge
  * configurations (Bl, Br: n x k, k may differ from base's).  Reuses base's eigendecomposition,
  * S_r^{-1}, Q_r, E_r and folded Cauchy matrix (shared, reference-counted: base may be destroyed

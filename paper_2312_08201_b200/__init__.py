@@ -37,7 +37,8 @@ def _dp(a: np.ndarray):
 
 
 class Problem:
-    """One seed A0 with its factors (lyap_setup); trace_batch evaluates trace(E X(v))."""
+    """One seed A0 with its factors (lyap_setup); trace_batch evaluates trace(E X(v)).  Q may be (n, n),
+    or (k, n, n) for a right-hand side linear in v, Q(v) = sum_i v_i Q[i] (lyap_setup_qlin)."""
 
     def __init__(self, A0, Bl, Br, Q, E, *, tol: float = 1e-12, max_dim: int = 0, max_restarts: int = 30,
                  batch: int = 0, warm_start: bool = False, max_cond_S: float = 1e8, device: int = -1,
@@ -50,7 +51,13 @@ class Problem:
         k = Bl.shape[1]
         Br = _f64(Br).reshape(n, k)
         Bl = Bl.reshape(n, k)
-        Q, E = _f64(Q, (n, n)), _f64(E, (n, n))
+        E = _f64(E, (n, n))
+        Q = _f64(Q)
+        qlin = Q.ndim == 3  # (k, n, n): Q(v) = sum_i v_i Q[i]  (lyap_setup_qlin)
+        if qlin and Q.shape != (k, n, n):
+            raise ValueError(f"a v-linear Q must be ({k}, {n}, {n})")
+        if not qlin:
+            Q = _f64(Q, (n, n))
         o = default_opts()
         o.tol, o.max_dim, o.max_restarts, o.batch = tol, max_dim, max_restarts, batch
         o.warm_start, o.max_cond_S, o.device, o.profile = int(warm_start), max_cond_S, device, int(profile)
@@ -58,7 +65,8 @@ class Problem:
         o.recycle = int(recycle)
         o.check_stable = int(check_stable)
         self._ctx = C.c_void_p()
-        rc = lib.lyap_setup(n, k, _dp(A0), _dp(Bl), _dp(Br), _dp(Q), _dp(E), C.byref(o), C.byref(self._ctx))
+        setup = lib.lyap_setup_qlin if qlin else lib.lyap_setup
+        rc = setup(n, k, _dp(A0), _dp(Bl), _dp(Br), _dp(Q), _dp(E), C.byref(o), C.byref(self._ctx))
         if rc != LYAP_OK:
             raise LyapError(rc, lib.lyap_last_error(None).decode())
         self.n, self.k = n, k

@@ -20,7 +20,7 @@ struct Basis {
   double* Lf = nullptr;    // npad x npad folded Cauchy matrix
   double* Sr = nullptr;    // n x n real eigenvector basis (column-major)
   double* Sinv = nullptr;  // S_r^{-1}
-  double* Qr = nullptr;    // S_r^{-1} Q S_r^{-T}
+  double* Qr = nullptr;    // S_r^{-1} Q S_r^{-T} (nterms matrices for a v-linear Q)
   double* Er = nullptr;    // S_r^T E S_r
   ~Basis() {
     cudaSetDevice(device);
@@ -47,6 +47,10 @@ struct Seed {
   double* Sr = nullptr;   // n x n real eigenvector basis (column-major), kept for lyap_solution
   double* Qr = nullptr;   // n x n S_r^{-1} Q S_r^{-T} (column-major), kept for lyap_solution
   double t0 = 0.0;
+  int nterms = 1;          // right-hand-side terms: Q(v) = sum_i v_i Q_i when qlin (lyap_setup_qlin)
+  bool qlin = false;
+  double* t0t = nullptr;   // device: t0 of every term
+  std::vector<double> t0h; // host copy
   double wcost[LYAP_KMAX] = {};  // ||B~l_t|| ||B^r_t||: weights of the scheduling cost proxy
   double* dwork = nullptr;       // device: [0, k) wcost, [8, 8 + 2k) batch bounding box, [32, ...) log seeds
 };
@@ -62,6 +66,7 @@ struct Engine {
   int groups = 1;   // slot groups, each on its own stream (K1 of one overlaps the Krylov kernels of the other)
   double *Bop = nullptr, *U = nullptr;            // groups x npad x ncol  (ncol per group)
   double *Xin = nullptr, *X = nullptr;            // b x L
+  double *rhs = nullptr, *t0s = nullptr;          // qlin: per-slot G0(v) (b x L) and t0(v) (b)
   double* Qb = nullptr;                           // b x (mmax+1) x L  (unnormalised basis)
   double* Minv = nullptr;                         // b x nrep x k x k x 2
   double *sigma = nullptr, *mask = nullptr;       // b x k

@@ -51,6 +51,11 @@ struct EngArgs {
   double* traces;
   double* gout;  // optional (lyap_solution, lyap_trace_batch_x): nv x L, the solved folded g of every v
   const double* x0;  // optional (lyap_trace_batch_x): nv x L initial guesses (solution recycling, f3)
+  // v-linear right-hand side (lyap_setup_qlin: Q(v) = sum_i v_i Q_i): g0 holds nterms x L terms, t0t
+  // nterms seed traces; per slot rhs = sum_i v_i g0_i (b x L) and t0s = sum_i v_i t0_i.  nterms = 0: off
+  int nterms;
+  const double* t0t;
+  double *rhs, *t0s;
   int32_t* status;
   int32_t* out_applies;
   double* out_resid;
@@ -103,6 +108,11 @@ __global__ void k_assign(EngArgs a) {
       a.applies[tid] = 0;
       a.restarts[tid] = 0;
       a.newv[tid] = 1;
+      if (a.t0s) {
+        double t0 = 0.0;
+        for (int t = 0; t < a.nterms; ++t) t0 += a.V[(int64_t)idx * a.K + t] * a.t0t[t];
+        a.t0s[tid] = t0;
+      }
       // cold start (g = 0): the first residual is the right-hand side itself -- START forms it
       // without a T-apply; a warm start must verify its initial iterate through K1
       a.phase[tid] = (a.warm || a.x0) ? PH_VERIFY : PH_START;
@@ -230,6 +240,17 @@ __global__ void __launch_bounds__(128) k_pfactor(EngArgs a) {
     invert_block<2 * K, K>(pb, a.mask + slot * K, a.sigma + slot * K, out);
   else
     invert_block<K, K>(pb, a.mask + slot * K, a.sigma + slot * K, out);
+  if (a.rhs) {  // per-slot right-hand side G0(v) = sum_i v_i G0_i at this rep's coordinates
+    const int64_t c = rep_coord(rep, a.npairs);
+    const int w = pair ? 2 : 1;
+    const double* v = a.V + (int64_t)a.vidx[slot] * K;
+    for (int t = 0; t < K; ++t)
+      for (int q = 0; q < w; ++q) {
+        double acc = 0.0;
+        for (int i = 0; i < a.nterms; ++i) acc += v[i] * a.g0[(int64_t)i * a.L + t * a.npad + c + q];
+        a.rhs[(int64_t)slot * a.L + t * a.npad + c + q] = acc;
+      }
+  }
   if (a.x0) {  // caller's initial guess for this v (masked rows: column t absent -> 0)
     const int64_t c = rep_coord(rep, a.npairs);
     const int w = pair ? 2 : 1;
@@ -413,7 +434,7 @@ __global__ void __launch_bounds__(256) k_dots(EngArgs a) {
       const int64_t e = e0 + i;
       if (e < a.L) {
         const int t = (int)(e / a.npad);
-        const double rh = a.mask[slot * a.K + t] * a.g0[e];
+        const double rh = a.mask[slot * a.K + t] * (a.rhs ? a.rhs[(int64_t)slot * a.L + e] : a.g0[e]);
         double r;
         if (start) {
           r = rh;
@@ -679,7 +700,7 @@ __global__ void __launch_bounds__(128) k_ctrl(EngArgs a) {
       s1 += p3[c * 3 + 1];
       s2 += p3[c * 3 + 2];
     }
-    const double rho = sqrt(s0), bn = sqrt(s1), tr = a.t0 + 2.0 * s2;
+    const double rho = sqrt(s0), bn = sqrt(s1), tr = (a.t0s ? a.t0s[slot] : a.t0) + 2.0 * s2;
     const int ap = (ph == PH_VERIFY) ? ++a.applies[slot] : a.applies[slot];  // START needs no T-apply
     const bool bad = !isfinite(rho) || !isfinite(tr);
     const bool conv = rho <= a.tol * bn;

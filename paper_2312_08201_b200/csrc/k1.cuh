@@ -39,6 +39,7 @@ struct K1Args {
   double* Yout;        // apply mode output (nslot x L)
   const int* nactive;  // engine: number of active slots (null: all nslot vectors are active)
   const int* alist;    // engine: active slot ids, compacted (null: identity)
+  const double* rhs;   // engine, v-linear Q: per-slot right-hand side (nslot x L); null: g0
 };
 
 // GEMM column block p (of k^2 columns) belongs to active position p -> slot alist[p]
@@ -241,6 +242,7 @@ __global__ void __launch_bounds__(256) k1_epi(K1Args a, const double* __restrict
     int sl = idx / (K * TC), s = (idx / TC) % K, r = idx % TC;
     if (s0 + sl >= nact) continue;
     const int slot = k1_slot(a, s0 + sl);
+    const double* gsrc = a.rhs ? a.rhs + (int64_t)slot * a.L : g0;
     int c = i0 + r;
     double* dst;
     bool verify = false;
@@ -281,7 +283,7 @@ __global__ void __launch_bounds__(256) k1_epi(K1Args a, const double* __restrict
       cplx xv = mk(xs[sl][s][r], xs[sl][s][r + 1]);
       cplx o = (msk != 0.0) ? (sig * xv - y) : xv;
       if (verify) {
-        o = mk(msk * g0[(int64_t)s * npad + c], msk * g0[(int64_t)s * npad + c + 1]) - o;
+        o = mk(msk * gsrc[(int64_t)s * npad + c], msk * gsrc[(int64_t)s * npad + c + 1]) - o;
       }
       dst[c] = o.re;
       dst[c + 1] = o.im;
@@ -295,7 +297,7 @@ __global__ void __launch_bounds__(256) k1_epi(K1Args a, const double* __restrict
       }
       double xv = xs[sl][s][r];
       double o = (msk != 0.0) ? (sig * xv - y) : xv;
-      if (verify) o = msk * g0[(int64_t)s * npad + c] - o;
+      if (verify) o = msk * gsrc[(int64_t)s * npad + c] - o;
       dst[c] = o;
     }
   }

@@ -133,7 +133,7 @@ void upload_seeds(lyap_ctx* ctx) {
 void free_engine(Engine& g, bool keep_order = true) {
   void* ps[] = {g.Bop, g.U, g.Xin, g.X, g.Qb, g.Minv, g.sigma, g.mask, g.eta, g.H, g.e, g.y,
                 g.bnorm, g.part, g.part3, g.phase, g.m, g.vidx, g.applies, g.restarts, g.ctrl,
-                g.part2, g.Gq, g.cf, g.Hraw};
+                g.part2, g.Gq, g.cf, g.Hraw, g.rhs, g.t0s};
   for (void* p : ps) dfree(p);
   if (g.h_ctrl) cudaFreeHost(g.h_ctrl);
   int* order = g.order;
@@ -244,6 +244,10 @@ void ensure_engine(lyap_ctx* ctx, int b, int mmax) {
   g.Gq = dalloc<double>(ctx, (size_t)b * (mmax + 1) * (mmax + 1));
   g.cf = dalloc<double>(ctx, (size_t)b * (mmax + 1));
   g.Hraw = dalloc<double>(ctx, (size_t)b * (mmax + 1) * mmax);
+  if (s.qlin) {  // per-slot right-hand side G0(v) and t0(v) of a v-linear Q
+    g.rhs = dalloc<double>(ctx, (size_t)b * g.L);
+    g.t0s = dalloc<double>(ctx, b);
+  }
   g.phase = dalloc<int>(ctx, b);
   g.m = dalloc<int>(ctx, b);
   g.vidx = dalloc<int>(ctx, b);
@@ -332,6 +336,10 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   a.tol = ctx->opts.tol;
   a.tol_inner = 0.5 * ctx->opts.tol;
   a.t0 = s.t0;
+  a.nterms = s.qlin ? s.nterms : 0;
+  a.t0t = s.t0t;
+  a.rhs = s.qlin ? g.rhs : nullptr;
+  a.t0s = s.qlin ? g.t0s : nullptr;
   a.max_restarts = ctx->opts.max_restarts;
   a.warm = ctx->opts.warm_start;
   a.V = dV;
@@ -393,6 +401,10 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
     x.alist = g.restarts + 2 * b + s0;
     x.su = g.restarts + 3 * b + s0;
     x.reg = g.restarts + 4 * b + s0;
+    if (x.rhs) {
+      x.rhs = g.rhs + s0 * g.L;
+      x.t0s = g.t0s + s0;
+    }
     x.Hraw = g.Hraw + s0 * ld * mmax;
     x.ctrl = g.ctrl + 8 * gi;
     ga[gi] = x;
@@ -409,6 +421,7 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
     k1.qstride = ld * g.L;
     k1.nactive = x.ctrl + 2;
     k1.alist = x.alist;
+    k1.rhs = x.rhs;
     gk[gi] = k1;
   }
 
@@ -575,24 +588,33 @@ void build_config(lyap_ctx* ctx, const double* Blc, const double* Brc) {
     t0d = dalloc<double>(ctx, 1);
     CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, ni, ki, ni, &one, B.Sinv, ni, Blc, ni, &zero, Blr, ni));
     CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_T, CUBLAS_OP_N, ni, ki, ni, &one, B.Sr, ni, Brc, ni, &zero, Brr, ni));
-    s.g0 = dalloc<double>(ctx, (size_t)k * s.npad);
+    const int nterms = s.nterms;
+    s.g0 = dalloc<double>(ctx, (size_t)nterms * k * s.npad);
     s.hf = dalloc<double>(ctx, (size_t)k * s.npad);
     s.F = dalloc<double>(ctx, (size_t)s.nrep * k * k * 2);
     s.bhr = dalloc<double>(ctx, (size_t)s.npad * k);
     s.btl = dalloc<double>(ctx, (size_t)s.npad * k);
-    K_DISPATCH(k, (k_seed_rep<KK><<<(unsigned)s.nrep, 128, 0, st>>>(B.lam, B.Qr, B.Er, Blr, Brr, n, s.npad, two_np,
-                                                                       s.npairs, s.g0, s.hf, s.F, t0part)));
-    LAUNCHED();
+    s.t0t = dalloc<double>(ctx, nterms);
+    s.t0h.assign(nterms, 0.0);
+    // one right-hand side per Q term (Q(v) = sum_i v_i Q_i: G0(v), t0(v) linear in v)
+    for (int q = nterms - 1; q >= 0; --q) {
+      K_DISPATCH(k, (k_seed_rep<KK><<<(unsigned)s.nrep, 128, 0, st>>>(B.lam, B.Qr + (size_t)q * n * n, B.Er, Blr, Brr, n,
+                                                                         s.npad, two_np, s.npairs,
+                                                                         s.g0 + (size_t)q * k * s.npad, s.hf, s.F,
+                                                                         t0part)));
+      LAUNCHED();
+      k_sum<<<1, 1024, 0, st>>>(t0part, s.nrep, s.t0t + q);
+      LAUNCHED();
+    }
     k_fold_b<<<(unsigned)((s.npad * k + 255) / 256), 256, 0, st>>>(Blr, Brr, n, s.npad, k, two_np, s.btl, s.bhr);
     LAUNCHED();
     s.Pb = dalloc<double>(ctx, (size_t)s.nrep * k * k * 4);
     K_DISPATCH(k, (k_pblock<KK><<<(unsigned)((s.nrep + 127) / 128), 128, 0, st>>>(B.Lf, s.npad, s.bhr, s.btl, s.F,
                                                                                      s.npairs, s.nrep, s.Pb)));
     LAUNCHED();
-    k_sum<<<1, 1024, 0, st>>>(t0part, s.nrep, t0d);
-    LAUNCHED();
-    CK(cudaMemcpyAsync(&s.t0, t0d, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(s.t0h.data(), s.t0t, 8 * nterms, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    s.t0 = s.t0h[0];
     // scheduling weights ||B~l_t|| ||B^r_t|| (folded coordinates)
     std::vector<double> hb((size_t)s.npad * k), hr((size_t)s.npad * k);
     CK(cudaMemcpy(hb.data(), s.btl, hb.size() * 8, cudaMemcpyDeviceToHost));
@@ -607,7 +629,9 @@ void build_config(lyap_ctx* ctx, const double* Blc, const double* Brc) {
       ctx->info.wcost[t] = s.wcost[t];
     }
     ctx->info.t0 = s.t0;
-    if (!std::isfinite(s.t0)) {
+    bool fin = true;
+    for (double t : s.t0h) fin = fin && std::isfinite(t);
+    if (!fin) {
       set_err(ctx, "seed trace t0 is not finite");
       throw Fail{LYAP_EEIG};
     }
@@ -733,7 +757,7 @@ static void destroy_impl(lyap_ctx* c) {
   cudaSetDevice(c->device);
   free_engine(c->eng, false);
   Seed& s = c->seed;
-  void* ps[] = {s.bhr, s.btl, s.F, s.Pb, s.g0, s.hf, s.dwork};  // lam, Lf, Sr, Qr belong to the shared Basis
+  void* ps[] = {s.bhr, s.btl, s.F, s.Pb, s.g0, s.hf, s.dwork, s.t0t};  // lam, Lf, Sr, Qr belong to the shared Basis
   if (!c->basis) {  // setup failed before the Basis took ownership
     dfree(s.lam);
     dfree(s.Lf);
@@ -766,8 +790,9 @@ static void destroy_impl(lyap_ctx* c) {
 
 void lyap_destroy(lyap_ctx* c) { destroy_impl(c); }
 
-int lyap_setup(int64_t n, int64_t k, const double* A0, const double* Bl, const double* Br, const double* Q,
-               const double* E, const lyap_opts* opts, lyap_ctx** out) {
+// nq = 0: one fixed Q (lyap_setup); nq = k: Q(v) = sum_i v_i Q_i (lyap_setup_qlin), Q holds nq matrices
+static int setup_core(int64_t n, int64_t k, const double* A0, const double* Bl, const double* Br, const double* Q,
+                      int nq, const double* E, const lyap_opts* opts, lyap_ctx** out) {
   lyap_ctx* ctx = nullptr;
   if (!out) {
     set_err(nullptr, "lyap_setup: out is NULL");
@@ -779,12 +804,14 @@ int lyap_setup(int64_t n, int64_t k, const double* A0, const double* Bl, const d
             (long long)n, (long long)k, LYAP_KMAX);
     return LYAP_EINVAL;
   }
-  {  // Q symmetric (the nk reduction needs Q = Q^T)
+  const int nterms = nq > 0 ? nq : 1;
+  for (int q = 0; q < nterms; ++q) {  // Q symmetric (the nk reduction needs Q = Q^T)
+    const double* Qq = Q + (size_t)q * n * n;
     double mx = 0.0, asym = 0.0;
     for (int64_t i = 0; i < n; ++i)
       for (int64_t j = 0; j < n; ++j) {
-        mx = std::max(mx, std::fabs(Q[i * n + j]));
-        asym = std::max(asym, std::fabs(Q[i * n + j] - Q[j * n + i]));
+        mx = std::max(mx, std::fabs(Qq[i * n + j]));
+        asym = std::max(asym, std::fabs(Qq[i * n + j] - Qq[j * n + i]));
       }
     if (asym > 1e-13 * mx) {
       set_err(nullptr, "lyap_setup: Q is not symmetric (max |Q - Q^T| = %.3e, max |Q| = %.3e)", asym, mx);
@@ -833,20 +860,22 @@ int lyap_setup(int64_t n, int64_t k, const double* A0, const double* Bl, const d
     Seed& s = ctx->seed;
     s.n = n;
     s.k = k;
+    s.nterms = nterms;
+    s.qlin = nq > 0;
     s.npad = roundup(n, n <= SMALL_N ? S_BM : G_BM);
     const size_t nn = (size_t)n * n;
     dA = dalloc<double>(ctx, nn, false);
-    dQ = dalloc<double>(ctx, nn, false);
+    dQ = dalloc<double>(ctx, nn * nterms, false);
     dE = dalloc<double>(ctx, nn, false);
     dBl = dalloc<double>(ctx, (size_t)n * k, false);
     dBr = dalloc<double>(ctx, (size_t)n * k, false);
     CK(cudaMemcpyAsync(dA, A0, nn * 8, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(dQ, Q, nn * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dQ, Q, nn * nterms * 8, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(dE, E, nn * 8, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(dBl, Bl, (size_t)n * k * 8, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(dBr, Br, (size_t)n * k * 8, cudaMemcpyHostToDevice, st));
     Acm = dalloc<double>(ctx, nn, false);
-    Qs = dalloc<double>(ctx, nn, false);
+    Qs = dalloc<double>(ctx, nn * nterms, false);
     Es = dalloc<double>(ctx, nn, false);
     Blc = dalloc<double>(ctx, (size_t)n * k, false);
     Brc = dalloc<double>(ctx, (size_t)n * k, false);
@@ -857,8 +886,10 @@ int lyap_setup(int64_t n, int64_t k, const double* A0, const double* Bl, const d
     LAUNCHED();
     k_transpose<<<dim3((unsigned)((k + 31) / 32), (unsigned)((n + 31) / 32)), tb, 0, st>>>(dBr, Brc, n, k);
     LAUNCHED();
-    k_symmetrize<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(dQ, Qs, n);
-    LAUNCHED();
+    for (int q = 0; q < nterms; ++q) {
+      k_symmetrize<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(dQ + q * nn, Qs + q * nn, n);
+      LAUNCHED();
+    }
     k_symmetrize<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(dE, Es, n);
     LAUNCHED();
 
@@ -963,14 +994,17 @@ int lyap_setup(int64_t n, int64_t k, const double* A0, const double* Bl, const d
     LAUNCHED();
     // ---- S3-S5: real n^3 products (cuBLAS DGEMM, column-major)
     T1 = dalloc<double>(ctx, nn, false);
-    Qr = dalloc<double>(ctx, nn, false);
+    Qr = dalloc<double>(ctx, nn * nterms, false);
     Er = dalloc<double>(ctx, nn, false);
     Blr = dalloc<double>(ctx, (size_t)n * k, false);
     Brr = dalloc<double>(ctx, (size_t)n * k, false);
     const double one = 1.0, zero = 0.0;
     const int ni = (int)n, ki = (int)k;
-    CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, ni, ni, ni, &one, Sinv, ni, Qs, ni, &zero, T1, ni));
-    CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_T, ni, ni, ni, &one, T1, ni, Sinv, ni, &zero, Qr, ni));
+    for (int q = 0; q < nterms; ++q) {
+      CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, ni, ni, ni, &one, Sinv, ni, Qs + q * nn, ni, &zero, T1, ni));
+      CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_T, ni, ni, ni, &one, T1, ni, Sinv, ni, &zero, Qr + q * nn,
+                      ni));
+    }
     CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_T, CUBLAS_OP_N, ni, ni, ni, &one, Sr, ni, Es, ni, &zero, T1, ni));
     CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, ni, ni, ni, &one, T1, ni, Sr, ni, &zero, Er, ni));
     // ---- eigenvalue extremes
@@ -1050,10 +1084,20 @@ int lyap_setup(int64_t n, int64_t k, const double* A0, const double* Bl, const d
   return LYAP_OK;
 }
 
+int lyap_setup(int64_t n, int64_t k, const double* A0, const double* Bl, const double* Br, const double* Q,
+               const double* E, const lyap_opts* opts, lyap_ctx** out) {
+  return setup_core(n, k, A0, Bl, Br, Q, 0, E, opts, out);
+}
+
+int lyap_setup_qlin(int64_t n, int64_t k, const double* A0, const double* Bl, const double* Br, const double* Qk,
+                    const double* E, const lyap_opts* opts, lyap_ctx** out) {
+  return setup_core(n, k, A0, Bl, Br, Qk, (int)k, E, opts, out);
+}
+
 int lyap_setup_like(const lyap_ctx* base, int64_t k, const double* Bl, const double* Br, const lyap_opts* opts,
                     lyap_ctx** out) {
   lyap_ctx* ctx = nullptr;
-  if (!out || !base || !base->basis || k < 1 || k > LYAP_KMAX || !Bl || !Br) {
+  if (!out || !base || !base->basis || k < 1 || k > LYAP_KMAX || !Bl || !Br || base->seed.qlin) {
     set_err(nullptr, "lyap_setup_like: invalid arguments (base with a basis, k = 1..%d, non-NULL Bl, Br)", LYAP_KMAX);
     return LYAP_EINVAL;
   }
@@ -1376,7 +1420,7 @@ int lyap_solution(lyap_ctx* ctx, int64_t nv, const double* V, double* X, double*
       for (int64_t v0 = 0; v0 < nv; v0 += chunk) {
         const int64_t bc = std::min(chunk, nv - v0);
         k_solution_Ystack<<<dim3((unsigned)((n + 127) / 128), (unsigned)n, (unsigned)bc), 128, 0, st>>>(
-            s.lam, s.Qr, s.btl, gout + v0 * L, n, s.npad, s.k, 2 * s.npairs, np, Yst);
+            s.lam, s.Qr, s.btl, gout + v0 * L, n, s.npad, s.k, 2 * s.npairs, np, Yst, dV, v0, s.qlin ? s.nterms : 0);
         LAUNCHED();
         DgemmOut o1{(int)np, (int)bc, (int)n};
         k1_dgemm<G_BM, G_BN, G_WM, G_WN, G_ST, G_BK, 1>

@@ -264,82 +264,6 @@ __global__ void k_build_Lf(const double* __restrict__ lam, int64_t n, int64_t np
   Lf[jc * npad + ic] = val;
 }
 
-// Full solution (NEXT row f2, eq. (Xsmalllastline)): with the
-// solved G, X~ = X~0 + L o (B~l G + G^T B~l^T), X~0 = -L o Q~, and X = S X~ S^T = S_r Y S_r^T with the
-// REAL matrix Y = J X~ J^T, generated here entrywise (column-major n x n).  g: folded k x npad.
-__global__ void k_solution_Y(const double* __restrict__ lam, const double* __restrict__ Qr,
-                             const double* __restrict__ btl, const double* __restrict__ g, int64_t n, int64_t npad,
-                             int64_t k, int64_t two_np, double* __restrict__ Y) {
-  const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t b = blockIdx.y;
-  if (a >= n) return;
-  auto blk = [&](int64_t c, int64_t* idx, cplx* jc, int& w) {  // eigen indices of coordinate c, J_{c,i}
-    if (c < two_np) {
-      const int64_t p0 = c & ~(int64_t)1;
-      idx[0] = p0;
-      idx[1] = p0 + 1;
-      w = 2;
-      if (c & 1) {
-        jc[0] = mk(0.0, 1.0);
-        jc[1] = mk(0.0, -1.0);
-      } else {
-        jc[0] = mk(1.0, 0.0);
-        jc[1] = mk(1.0, 0.0);
-      }
-    } else {
-      idx[0] = c;
-      jc[0] = mk(1.0, 0.0);
-      w = 1;
-    }
-  };
-  auto folded = [&](const double* v, int64_t stride, int64_t t, int64_t i) -> cplx {  // full-index value
-    if (i < two_np) {
-      const int64_t p0 = i & ~(int64_t)1;
-      const cplx z = mk(v[t * stride + p0], v[t * stride + p0 + 1]);
-      return (i & 1) ? conj(z) : z;
-    }
-    return mk(v[t * stride + i], 0.0);
-  };
-  auto blt = [&](int64_t i, int64_t t) -> cplx {  // B~l_{i,t} from the folded [coord][t] layout
-    if (i < two_np) {
-      const int64_t p0 = i & ~(int64_t)1;
-      const cplx z = mk(btl[p0 * k + t], btl[(p0 + 1) * k + t]);
-      return (i & 1) ? conj(z) : z;
-    }
-    return mk(btl[i * k + t], 0.0);
-  };
-  int64_t ia[2], jb[2];
-  cplx ja[2], jbv[2];
-  int wa, wb;
-  blk(a, ia, ja, wa);
-  blk(b, jb, jbv, wb);
-  cplx acc = mk(0.0, 0.0);
-  for (int u = 0; u < wa; ++u) {
-    const int64_t i = ia[u];
-    cplx ci0, ci1;
-    int wi;
-    jinv_row(i, two_np, ci0, ci1, wi);
-    const int64_t ai0 = (i < two_np) ? (i & ~(int64_t)1) : i;
-    for (int q = 0; q < wb; ++q) {
-      const int64_t j = jb[q];
-      cplx cj0, cj1;
-      int wj;
-      jinv_row(j, two_np, cj0, cj1, wj);
-      const int64_t aj0 = (j < two_np) ? (j & ~(int64_t)1) : j;
-      // Q~_ij = sum Jinv_{i,a'} Qr[a', c'] Jinv_{j,c'}
-      cplx qt = mk(0.0, 0.0);
-      for (int x = 0; x < wi; ++x)
-        for (int y = 0; y < wj; ++y)
-          qt = qt + ((x ? ci1 : ci0) * (y ? cj1 : cj0)) * mk(Qr[(aj0 + y) * n + ai0 + x], 0.0);
-      cplx rhs = mk(-qt.re, -qt.im);
-      for (int64_t t = 0; t < k; ++t)
-        rhs = rhs + blt(i, t) * folded(g, npad, t, j) + folded(g, npad, t, i) * blt(j, t);
-      const cplx L = cinv(eig_of(lam, i, two_np) + eig_of(lam, j, two_np));
-      acc = acc + (ja[u] * jbv[q]) * (L * rhs);
-    }
-  }
-  Y[b * n + a] = acc.re;
-}
 
 // Per-rep diagonal block of the folded T (the preconditioner's v-independent part, engine.cuh
 // k_pfactor): the exact response of K1's operator (k1_gen -> Lf -> k1_epi) at the rep's own
@@ -381,17 +305,27 @@ __global__ void k_pblock(const double* __restrict__ Lf, int64_t npad, const doub
   }
 }
 
-// Batched full solution (f2): Y_v for a chunk of parameter vectors, written as a vertical stack of
-// np x np blocks (np = n padded to the GEMM tile; padding rows / columns stay zero): Yst[(v np + a) np + b].
-// Same entrywise formula as k_solution_Y (Y = J X~ J^T, X~ = X~0 + L o (B~l G + G^T B~l^T)): the
-// Hadamard product with the Cauchy matrix is formed here, element by element, never as a matrix.
+// Full solution (NEXT row f2, eq. (Xsmalllastline)): with the solved
+// G, X~ = X~0 + L o (B~l G + G^T B~l^T), X~0 = -L o Q~, and X = S X~ S^T = S_r Y S_r^T with the REAL
+// matrix Y = J X~ J^T, generated here entrywise for a chunk of parameter vectors, written as a
+// vertical stack of np x np blocks (np = n padded to the GEMM tile; padding stays zero):
+// Yst[(v np + a) np + b].  The Hadamard product with the Cauchy matrix is formed element by element,
+// never as a matrix; g: folded k x npad per v.
+// (v-linear Q, nterms > 0: Q~(v) = sum_i v_i Q~_i with the rows of V (chunk offset v0) as weights)
 __global__ void k_solution_Ystack(const double* __restrict__ lam, const double* __restrict__ Qr,
                                   const double* __restrict__ btl, const double* __restrict__ g, int64_t n, int64_t npad,
-                                  int64_t k, int64_t two_np, int64_t np, double* __restrict__ Yst) {
+                                  int64_t k, int64_t two_np, int64_t np, double* __restrict__ Yst,
+                                  const double* __restrict__ V = nullptr, int64_t v0 = 0, int nterms = 0) {
   const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t b = blockIdx.y, v = blockIdx.z;
   if (a >= n) return;
   const double* gv = g + v * k * npad;
+  auto qr = [&](int64_t idx) -> double {  // Q_r(v) entry
+    if (nterms <= 0) return Qr[idx];
+    double acc = 0.0;
+    for (int i = 0; i < nterms; ++i) acc += V[(v0 + v) * k + i] * Qr[(int64_t)i * n * n + idx];
+    return acc;
+  };
   auto blk = [&](int64_t c, int64_t* idx, cplx* jc, int& w) {
     if (c < two_np) {
       const int64_t p0 = c & ~(int64_t)1;
@@ -448,7 +382,7 @@ __global__ void k_solution_Ystack(const double* __restrict__ lam, const double* 
       cplx qt = mk(0.0, 0.0);
       for (int x = 0; x < wi; ++x)
         for (int y = 0; y < wj; ++y)
-          qt = qt + ((x ? ci1 : ci0) * (y ? cj1 : cj0)) * mk(Qr[(aj0 + y) * n + ai0 + x], 0.0);
+          qt = qt + ((x ? ci1 : ci0) * (y ? cj1 : cj0)) * mk(qr((aj0 + y) * n + ai0 + x), 0.0);
       cplx rhs = mk(-qt.re, -qt.im);
       for (int64_t t = 0; t < k; ++t) rhs = rhs + blt(i, t) * folded(t, j) + folded(t, i) * blt(j, t);
       const cplx L = cinv(eig_of(lam, i, two_np) + eig_of(lam, j, two_np));

@@ -512,3 +512,28 @@ def test_trace_batch_with_stability_filter():
     ref = oracle.trace_batch(A0, Bl, Br, Q, E, V[stable])
     assert rel_err(tau[stable], ref).max() <= RTOL
     P.close()
+
+
+# ----------------------------------------------------------------------------- v-linear right-hand side
+@pytest.mark.parametrize("n,k,seed", [(12, 2, 0), (30, 3, 1)])
+def test_qlin_right_hand_side(n, k, seed):
+    """lyap_setup_qlin: Q(v) = sum_i v_i Q_i (the projected equation of) solved as one
+    capacitance system per v; traces and full X(v) against the oracle run with Q(v) formed explicitly."""
+    rng = np.random.default_rng(70 + seed)
+    A0, Bl, Br, _, E = workloads.random_stable(n, k, rng)
+    Qs = []
+    for _ in range(k):
+        R = rng.standard_normal((n, 2))
+        Qs.append(R @ R.T / n)
+    Qs = np.array(Qs)
+    V = rng.uniform(0.1, 2.0, (9, k))
+    P = _problem(A0, Bl, Br, Qs, E)
+    tau = P.trace_batch(V)
+    X = P.solution(V[:3])
+    for i, v in enumerate(V):
+        Qv = np.tensordot(v, Qs, axes=1)
+        ref, d = oracle.trace_EX(A0, Bl, Br, Qv, E, v, diagnostics=True)
+        assert rel_err(tau[i], ref) <= RTOL, (i, tau[i], ref)
+        if i < 3:
+            assert np.abs(X[i] - d["X"]).max() <= 1e-9 * np.abs(d["X"]).max()
+    P.close()
