@@ -224,7 +224,8 @@ void lyap_destroy(lyap_ctx* ctx);
  * EK_m(A0, P), P = [X0 Br, Bl], for every v; the projected equation eq. (param_projected) is solved by
  * the dense engine above (dimension 4mk; k instances, the right-hand side being linear in v); the
  * space grows by 4k columns per step until the backward error of Prop. 2.1 is
- * <= eps on a sample of the batch.  The result is an APPROXIMATION controlled by eps.
+ * <= eps for every v of the batch (Alg. 1; per-v certification).  The result is an APPROXIMATION
+ * controlled by eps.
  * lyap_ek_setup: A0 (n x n), Bl, Br (n x k), X0Br = X0 Br (n x k; the seed solution's action, from a
  * closed form or any Lyapunov solver), E (n x n, symmetrised), trEX0 = trace(E X0); all host,
  * row-major.  max_dim caps the basis (default 400 columns).  LU of A0 on the device (cuSOLVER).
@@ -239,6 +240,12 @@ int lyap_ek_setup(int64_t n, int64_t k, const double* A0, const double* Bl, cons
                   const double* E, double trEX0, int32_t max_dim, lyap_ek** out);
 int lyap_ek_trace_batch(lyap_ek* ek, int64_t nv, const double* V, double eps, int32_t max_steps, double* traces,
                         int32_t* dim_used, double* bwd_err);
+/* As lyap_ek_trace_batch with per-v certification output (Alg. 1): bwd_v[i] = the
+ * Prop. 2.1 backward error with which V[i]'s trace was certified (host, nullable), dim_v[i] = the basis
+ * size of the space it was taken from (nullable).  Every v is certified separately: its trace comes
+ * from the first checked space whose backward error for that v is <= eps. */
+int lyap_ek_trace_batch_ex(lyap_ek* ek, int64_t nv, const double* V, double eps, int32_t max_steps, double* traces,
+                           double* bwd_v, int32_t* dim_v);
 void lyap_ek_destroy(lyap_ek* ek);
 const char* lyap_ek_last_error(const lyap_ek* ek);
 

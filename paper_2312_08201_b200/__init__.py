@@ -295,10 +295,21 @@ class EKProblem:
             raise LyapError(rc, lib.lyap_ek_last_error(None).decode())
         self.n, self.k = n, k
 
-    def trace_batch(self, V, eps: float = 1e-8, max_steps: int = 200, allow_partial: bool = False):
+    def trace_batch(self, V, eps: float = 1e-8, max_steps: int = 200, allow_partial: bool = False,
+                    per_v: bool = False):
         """(traces, basis dim, certified backward error).  LYAP_EPARTIAL (target not certified) raises
-        unless allow_partial."""
+        unless allow_partial.  per_v: (traces, backward error per v, basis size per v) -- Alg. 1's
+        per-v certification (lyap_ek_trace_batch_ex)."""
         V = _f64(V).reshape(-1, self.k)
+        if per_v:
+            tau = np.empty(V.shape[0])
+            bw = np.empty(V.shape[0])
+            dm = np.empty(V.shape[0], dtype=np.int32)
+            rc = lib.lyap_ek_trace_batch_ex(self._ek, V.shape[0], V.ctypes.data, eps, max_steps, tau.ctypes.data,
+                                            bw.ctypes.data, dm.ctypes.data)
+            if rc != LYAP_OK and not (rc == LYAP_EPARTIAL and allow_partial):
+                raise LyapError(rc, lib.lyap_ek_last_error(self._ek).decode())
+            return tau, bw, dm
         tau = np.empty(V.shape[0])
         dim = C.c_int32()
         err = C.c_double()

@@ -17,7 +17,7 @@ LYAP_KMAX = 8
 
 # every symbol include/lyapgpu.h declares (checked by tests/test_abi.py)
 EXPORTED = ("lyap_default_opts", "lyap_setup", "lyap_trace_batch", "lyap_trace_batch_ex", "lyap_trace_batch_x",
-            "lyap_stable_batch", "lyap_setup_qlin",
+            "lyap_stable_batch", "lyap_setup_qlin", "lyap_ek_trace_batch_ex",
             "lyap_get_info",
             "lyap_get_stats", "lyap_reset_stats", "lyap_apply_C", "lyap_export_state", "lyap_destroy",
             "lyap_last_error", "lyap_solution", "lyap_setup_like", "lyap_set_recycle",
@@ -62,6 +62,8 @@ def _load():
     lib.lyap_trace_batch_ex.restype = C.c_int
     lib.lyap_trace_batch_x.argtypes = [P, C.c_int64, P, P, P, P, P, P, P, P]
     lib.lyap_trace_batch_x.restype = C.c_int
+    lib.lyap_ek_trace_batch_ex.argtypes = [P, C.c_int64, P, C.c_double, C.c_int32, P, P, P]
+    lib.lyap_ek_trace_batch_ex.restype = C.c_int
     lib.lyap_setup_qlin.argtypes = [C.c_int64, C.c_int64, dp, dp, dp, dp, dp, C.POINTER(Opts), C.POINTER(P)]
     lib.lyap_setup_qlin.restype = C.c_int
     lib.lyap_stable_batch.argtypes = [P, C.c_int64, P, P, C.c_int, P]

@@ -1373,33 +1373,31 @@ int lyap_trace_batch(lyap_ctx* ctx, int64_t nv, const double* V, double* traces,
   return lyap_trace_batch_ex(ctx, nv, V, traces, status, nullptr, nullptr, v_on_device, cuda_stream);
 }
 
-int lyap_solution(lyap_ctx* ctx, int64_t nv, const double* V, double* X, double* traces) {
-  if (!ctx || nv < 0 || (nv > 0 && (!V || !X))) {
-    set_err(ctx, "lyap_solution: invalid arguments");
-    return LYAP_EINVAL;
-  }
-  if (nv == 0) return LYAP_OK;
+}  // extern "C"
+
+namespace {
+// Full solutions X(v) (n x n, row-major) of the nv rows of the DEVICE array dV, chunk by chunk
+// (DESIGN.md §2.5): the engine solves every v (gout: the folded g), then per chunk Y_v is generated
+// entrywise and X_v = S_r Y_v S_r^T comes from two batched DMMA GEMMs (k1_dgemm): T1 = [Y_1; ...] S_r^T
+// written horizontally, X = S_r [T1_1 | ...] written compactly.  sink(v0, count, Xc) consumes each
+// chunk (device, count x n x n) on ctx->stream.  Returns the engine status; hs gets the per-v codes,
+// dtr (device, nullable) the traces.  Throws Fail.
+template <class Sink>
+int solution_chunks(lyap_ctx* ctx, int64_t nv, const double* dV, double* dtr, std::vector<int32_t>& hs, Sink sink) {
   const Seed& s = ctx->seed;
-  double *dV = nullptr, *dtr = nullptr, *gout = nullptr, *Yst = nullptr, *T1 = nullptr, *Xc = nullptr;
+  cudaStream_t st = ctx->stream;
+  const int64_t n = s.n, L = s.k * s.npad, np = roundup(n, G_BM);
+  double *gout = nullptr, *Yst = nullptr, *T1 = nullptr, *Xc = nullptr, *dtr_own = nullptr;
   int32_t* dst = nullptr;
   int rc = LYAP_OK;
   try {
-    CK(cudaSetDevice(ctx->device));
-    cudaStream_t st = ctx->stream;
-    const int64_t n = s.n, L = s.k * s.npad, np = roundup(n, G_BM);
-    dV = dalloc<double>(ctx, (size_t)nv * s.k, false);
-    dtr = dalloc<double>(ctx, nv, false);
-    dst = dalloc<int32_t>(ctx, nv, false);
     gout = dalloc<double>(ctx, (size_t)nv * L);
-    CK(cudaMemcpyAsync(dV, V, (size_t)nv * s.k * 8, cudaMemcpyHostToDevice, st));
+    dst = dalloc<int32_t>(ctx, nv, false);
+    if (!dtr) dtr = dtr_own = dalloc<double>(ctx, nv, false);
     rc = run_batch(ctx, nv, dV, nullptr, dtr, dst, nullptr, nullptr, st, gout);
     if (rc == LYAP_OK) {
-      std::vector<int32_t> hs(nv);
+      hs.resize(nv);
       CK(cudaMemcpyAsync(hs.data(), dst, nv * 4, cudaMemcpyDeviceToHost, st));
-      if (traces) CK(cudaMemcpyAsync(traces, dtr, nv * 8, cudaMemcpyDeviceToHost, st));
-      // X_v = S_r Y_v S_r^T for a chunk of v at a time, two batched DMMA GEMMs (k1_dgemm, DESIGN.md
-      // §2.5): T1 = [Y_1; Y_2; ...] S_r^T (written horizontally: [T1_1 | T1_2 | ...]), then
-      // X = S_r [T1_1 | T1_2 | ...] written compactly as nv x n x n
       if (!ctx->Spad) {
         ctx->Spad = dalloc<double>(ctx, 2 * (size_t)np * np, false);
         k_pad_basis<<<dim3((unsigned)((np + 255) / 256), (unsigned)np), 256, 0, st>>>(s.Sr, n, np, ctx->Spad,
@@ -1410,7 +1408,7 @@ int lyap_solution(lyap_ctx* ctx, int64_t nv, const double* V, double* X, double*
         CK(cudaFuncSetAttribute(k1_dgemm<G_BM, G_BN, G_WM, G_WN, G_ST, G_BK, 2>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GCfg::SMEM));
       }
-      const double* Sc = ctx->Spad;            // S_r^T (row-major)
+      const double* Sc = ctx->Spad;              // S_r^T (row-major)
       const double* Srow = ctx->Spad + np * np;  // S_r (row-major)
       const int64_t per_v = np * np * 8;
       const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(nv, ((int64_t)1 << 30) / per_v));
@@ -1432,8 +1430,42 @@ int lyap_solution(lyap_ctx* ctx, int64_t nv, const double* V, double* X, double*
             <<<(unsigned)((bc * np / G_BN) * (np / G_BM)), GCfg::THREADS, GCfg::SMEM, st>>>(
                 Srow, T1, Xc, (int)np, (int)(bc * np), (int)np, (int)np, nullptr, 1, o2);
         LAUNCHED();
-        CK(cudaMemcpyAsync(X + v0 * n * n, Xc, (size_t)bc * n * n * 8, cudaMemcpyDeviceToHost, st));
+        sink(v0, bc, Xc);
       }
+      CK(cudaStreamSynchronize(st));
+    }
+  } catch (Fail f) {
+    rc = f.code;
+  }
+  for (void* p : {(void*)gout, (void*)Yst, (void*)T1, (void*)Xc, (void*)dst, (void*)dtr_own}) dfree(p);
+  return rc;
+}
+}  // namespace
+
+extern "C" {
+
+int lyap_solution(lyap_ctx* ctx, int64_t nv, const double* V, double* X, double* traces) {
+  if (!ctx || nv < 0 || (nv > 0 && (!V || !X))) {
+    set_err(ctx, "lyap_solution: invalid arguments");
+    return LYAP_EINVAL;
+  }
+  if (nv == 0) return LYAP_OK;
+  const Seed& s = ctx->seed;
+  double *dV = nullptr, *dtr = nullptr;
+  int rc = LYAP_OK;
+  try {
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    const int64_t n = s.n;
+    dV = dalloc<double>(ctx, (size_t)nv * s.k, false);
+    dtr = dalloc<double>(ctx, nv, false);
+    CK(cudaMemcpyAsync(dV, V, (size_t)nv * s.k * 8, cudaMemcpyHostToDevice, st));
+    std::vector<int32_t> hs;
+    rc = solution_chunks(ctx, nv, dV, dtr, hs, [&](int64_t v0, int64_t bc, const double* Xc) {
+      CK(cudaMemcpyAsync(X + v0 * n * n, Xc, (size_t)bc * n * n * 8, cudaMemcpyDeviceToHost, st));
+    });
+    if (rc == LYAP_OK) {
+      if (traces) CK(cudaMemcpyAsync(traces, dtr, nv * 8, cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
       for (int64_t v = 0; v < nv; ++v)
         if (hs[v] != 0) {
@@ -1445,8 +1477,8 @@ int lyap_solution(lyap_ctx* ctx, int64_t nv, const double* V, double* X, double*
   } catch (Fail f) {
     rc = f.code;
   }
-  void* ps[] = {dV, dtr, gout, Yst, T1, Xc, dst};
-  for (void* p : ps) dfree(p);
+  dfree(dV);
+  dfree(dtr);
   return rc;
 }
 

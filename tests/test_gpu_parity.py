@@ -429,6 +429,28 @@ def test_extended_krylov_projection(name, nsub):
     assert errs[1] <= errs[0], info
 
 
+@pytest.mark.parametrize("name,nsub,eps", [("c1", 64, 1e-10), ("c3", 48, 1e-10)])
+def test_extended_krylov_per_v_certification(name, nsub, eps):
+    """Alg. 1 per-v certification: every v's trace comes with its own Prop. 2.1
+    backward error <= eps; the traces match the oracle to <= 1e3 eps.  c3 (the multi-agent network,
+    the paper's Ex. 2/3 setting: spaces of 8-56 columns) compresses: every v is
+    certified with a basis far below n."""
+    from paper_2312_08201_b200 import EKProblem
+    W = workloads.make(name)
+    X0 = scipy.linalg.solve_continuous_lyapunov(W.A0, -W.Q)
+    t0 = float(np.sum(0.5 * (W.E + W.E.T) * X0))
+    g = _golden(name)
+    idx = np.array(g["indices"])[:nsub]
+    ref = np.array(g["traces"])[:nsub]
+    ek = EKProblem(W.A0, W.Bl, W.Br, X0 @ W.Br, W.E, t0, max_dim=W.n)
+    tau, bwd, dim = ek.trace_batch(W.V[idx], eps=eps, per_v=True)
+    assert np.all(bwd <= eps), bwd.max()
+    assert rel_err(tau, ref).max() <= 1e3 * eps, rel_err(tau, ref).max()
+    if name == "c3":
+        assert dim.max() <= W.n // 4, dim.max()
+    ek.close()
+
+
 def test_extended_krylov_capacity_is_flagged():
     """A basis capped below n cannot certify a tight target: LYAP_EPARTIAL, and with allow_partial the
     reported backward error is the last certified one (> eps), never a fabricated 0."""
