@@ -42,6 +42,14 @@ struct K1Args {
   const double* rhs;   // engine, v-linear Q: per-slot right-hand side (nslot x L); null: g0
 };
 
+// Fused-epilogue arguments of the K1 GEMM (EPI = k > 0): the k1_epi contraction done from the CTA's
+// accumulator tile in shared memory, so U never goes to global memory and k1_epi is not launched.
+struct K1EpiArgs {
+  K1Args a;
+  const double *btl, *F, *g0;
+  int npad, two_np, npairs, n;
+};
+
 // GEMM column block p (of k^2 columns) belongs to active position p -> slot alist[p]
 __device__ __forceinline__ int k1_nact(const K1Args& a) { return a.nactive ? *a.nactive : a.nslot; }
 __device__ __forceinline__ int k1_slot(const K1Args& a, int pos) { return a.alist ? a.alist[pos] : pos; }
@@ -108,11 +116,17 @@ struct DgemmOut {
   int blk, nblk, no;
 };
 
-template <int BM, int BN, int WM, int WN, int STAGES, int BK_ = 16, int OUT = 0>
+template <int K>
+__device__ __forceinline__ void k1_out_element(const K1EpiArgs& ep, int slot, int s, int c, const double* ur,
+                                               const double* ur1, int ust);
+
+// EPI > 0: fused K1 epilogue for k = EPI (OUT ignored, C unused): see K1EpiArgs.
+template <int BM, int BN, int WM, int WN, int STAGES, int BK_ = 16, int OUT = 0, int EPI = 0>
 __global__ void __launch_bounds__(DgemmCfg<BM, BN, WM, WN, STAGES, BK_>::THREADS,
                                   DgemmCfg<BM, BN, WM, WN, STAGES, BK_>::THREADS <= 128 ? 3 : 1)
     k1_dgemm(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C, int M,
-             int N, int Kd, int lda, const int* __restrict__ nactive, int cols_per_active, DgemmOut om = {}) {
+             int N, int Kd, int lda, const int* __restrict__ nactive, int cols_per_active, DgemmOut om = {},
+             K1EpiArgs ep = {}) {
   using Cfg = DgemmCfg<BM, BN, WM, WN, STAGES, BK_>;
   constexpr int BK = Cfg::BK, AST = Cfg::AST, BST = Cfg::BST, NT = Cfg::THREADS;
   constexpr int MT = WM / 8, NTL = WN / 8;
@@ -189,28 +203,120 @@ __global__ void __launch_bounds__(DgemmCfg<BM, BN, WM, WN, STAGES, BK_>::THREADS
     }
   }
   cp_async_wait<0>();
-  // store: lane holds C[row][2c], C[row][2c+1]
+  if constexpr (EPI > 0) {
+    // fused epilogue: accumulator tile -> shared memory, then the k1_epi contraction per (slot, s, row)
+    constexpr int UST = BN + 1, KK = EPI * EPI, NPOS = BN / KK;
+    static_assert(BN % KK == 0, "a slot's k^2 columns must not straddle tiles");
+    __syncthreads();  // every warp is done with the pipeline buffers
+    double* Us = smem;
 #pragma unroll
-  for (int i = 0; i < MT; ++i) {
-    int row = m0 + wm * WM + i * 8 + (lane >> 2);
+    for (int i = 0; i < MT; ++i) {
+      const int rl = wm * WM + i * 8 + (lane >> 2);
 #pragma unroll
-    for (int j = 0; j < NTL; ++j) {
-      int col = n0 + wn * WN + j * 8 + (lane & 3) * 2;
-      if (OUT == 0) {
-        *reinterpret_cast<double2*>(C + (int64_t)row * N + col) = make_double2(acc[i][j][0], acc[i][j][1]);
-      } else if (OUT == 1) {
-        const int v = row / om.blk, r = row % om.blk;
-        *reinterpret_cast<double2*>(C + (int64_t)r * N * om.nblk + (int64_t)v * N + col) =
-            make_double2(acc[i][j][0], acc[i][j][1]);
-      } else {
-        const int v = col / om.blk, c = col % om.blk;
-        if (row < om.no) {
-          double* dst = C + ((int64_t)v * om.no + row) * om.no;
-          if (c < om.no) dst[c] = acc[i][j][0];
-          if (c + 1 < om.no) dst[c + 1] = acc[i][j][1];
+      for (int j = 0; j < NTL; ++j) {
+        const int cl = wn * WN + j * 8 + (lane & 3) * 2;
+        Us[rl * UST + cl] = acc[i][j][0];
+        Us[rl * UST + cl + 1] = acc[i][j][1];
+      }
+    }
+    __syncthreads();
+    const int nact = k1_nact(ep.a), p0 = n0 / KK;
+    for (int idx = tid; idx < NPOS * EPI * BM; idx += NT) {
+      const int r = idx % BM, s = (idx / BM) % EPI, pp = idx / (BM * EPI);
+      if (p0 + pp >= nact) continue;
+      const int slot = k1_slot(ep.a, p0 + pp);
+      const double* ur = Us + r * UST + pp * KK + s * EPI;  // U[(s, t), row r], t = 0..k-1
+      k1_out_element<EPI>(ep, slot, s, m0 + r, ur, ur + UST, UST);
+    }
+  } else {
+    // store: lane holds C[row][2c], C[row][2c+1]
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      int row = m0 + wm * WM + i * 8 + (lane >> 2);
+#pragma unroll
+      for (int j = 0; j < NTL; ++j) {
+        int col = n0 + wn * WN + j * 8 + (lane & 3) * 2;
+        if (OUT == 0) {
+          *reinterpret_cast<double2*>(C + (int64_t)row * N + col) = make_double2(acc[i][j][0], acc[i][j][1]);
+        } else if (OUT == 1) {
+          const int v = row / om.blk, r = row % om.blk;
+          *reinterpret_cast<double2*>(C + (int64_t)r * N * om.nblk + (int64_t)v * N + col) =
+              make_double2(acc[i][j][0], acc[i][j][1]);
+        } else {
+          const int v = col / om.blk, c = col % om.blk;
+          if (row < om.no) {
+            double* dst = C + ((int64_t)v * om.no + row) * om.no;
+            if (c < om.no) dst[c] = acc[i][j][0];
+            if (c + 1 < om.no) dst[c + 1] = acc[i][j][1];
+          }
         }
       }
     }
+  }
+}
+
+// One output element of K1 (k1_epi's contraction): row c of parameter s of the slot's vector.
+// ur[t] = U[(s, t), c], ur1[t] = U[(s, t), c + 1] (the pair's Im row).  Writes C(v)X (or the VERIFY
+// residual) into the slot's Krylov basis, or Y in apply mode.
+template <int K>
+__device__ __forceinline__ void k1_out_element(const K1EpiArgs& ep, int slot, int s, int c, const double* ur,
+                                               const double* ur1, int) {
+  const K1Args& a = ep.a;
+  const int npad = ep.npad;
+  const double* gsrc = a.rhs ? a.rhs + (int64_t)slot * a.L : ep.g0;
+  const double* x = a.Xin + (int64_t)slot * a.L;
+  double* dst;
+  bool verify = false;
+  double msk = 1.0, sig;
+  if (a.mode == 0) {
+    dst = a.Yout + (int64_t)slot * a.L + (int64_t)s * npad;
+    sig = a.sigma ? a.sigma[slot * K + s] : 0.0;
+  } else {
+    const int ph = a.phase[slot];
+    if (ph == PH_ITER) {
+      dst = a.Qb + (int64_t)slot * a.qstride + (int64_t)(a.m[slot] + 1) * a.L + (int64_t)s * npad;
+    } else if (ph == PH_VERIFY) {
+      dst = a.Qb + (int64_t)slot * a.qstride + (int64_t)s * npad;
+      verify = true;
+    } else {
+      return;
+    }
+    sig = a.sigma[slot * K + s];
+    msk = a.mask[slot * K + s];
+  }
+  if (c >= ep.n) {  // zero padding stays zero
+    dst[c] = 0.0;
+    return;
+  }
+  if (c < ep.two_np) {
+    if (c & 1) return;  // the Re-coordinate thread writes both coordinates of the pair
+    const int rep = c >> 1;
+    cplx y = mk(0.0, 0.0);
+#pragma unroll
+    for (int t = 0; t < K; ++t) {
+      const cplx u = mk(ur[t], ur1[t]);
+      const cplx bl = mk(ep.btl[(int64_t)c * K + t], ep.btl[(int64_t)(c + 1) * K + t]);
+      const double* f = ep.F + (((int64_t)rep * K + s) * K + t) * 2;
+      const cplx xt = mk(x[(int64_t)t * npad + c], x[(int64_t)t * npad + c + 1]);
+      y = y + bl * u + mk(f[0], f[1]) * xt;
+    }
+    const cplx xv = mk(x[(int64_t)s * npad + c], x[(int64_t)s * npad + c + 1]);
+    cplx o = (msk != 0.0) ? (sig * xv - y) : xv;
+    if (verify) o = mk(msk * gsrc[(int64_t)s * npad + c], msk * gsrc[(int64_t)s * npad + c + 1]) - o;
+    dst[c] = o.re;
+    dst[c + 1] = o.im;
+  } else {
+    const int rep = c - ep.two_np + ep.npairs;
+    double y = 0.0;
+#pragma unroll
+    for (int t = 0; t < K; ++t) {
+      y += ep.btl[(int64_t)c * K + t] * ur[t];
+      y += ep.F[(((int64_t)rep * K + s) * K + t) * 2] * x[(int64_t)t * npad + c];
+    }
+    const double xv = x[(int64_t)s * npad + c];
+    double o = (msk != 0.0) ? (sig * xv - y) : xv;
+    if (verify) o = msk * gsrc[(int64_t)s * npad + c] - o;
+    dst[c] = o;
   }
 }
 

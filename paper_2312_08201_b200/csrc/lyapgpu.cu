@@ -260,6 +260,49 @@ void ensure_engine(lyap_ctx* ctx, int b, int mmax) {
 
 // ------------------------------------------------------------------ K1 launch (prologue, GEMM, epilogue)
 
+// K1 with the epilogue fused into the GEMM (k = 1, 2, 4: a slot's k^2 columns never straddle a CTA
+// tile): prologue + one GEMM launch; other k: prologue, GEMM, k1_epi
+inline bool k1_fused(int64_t k) { return k == 1 || k == 2 || k == 4; }
+
+template <int BM, int BN, int WM, int WN, int ST, int BK>
+void set_smem_attrs(lyap_ctx* ctx) {
+  using Cfg = DgemmCfg<BM, BN, WM, WN, ST, BK>;
+  CK(cudaFuncSetAttribute(k1_dgemm<BM, BN, WM, WN, ST, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM));
+  CK(cudaFuncSetAttribute(k1_dgemm<BM, BN, WM, WN, ST, BK, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)Cfg::SMEM));
+  CK(cudaFuncSetAttribute(k1_dgemm<BM, BN, WM, WN, ST, BK, 0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)Cfg::SMEM));
+  CK(cudaFuncSetAttribute(k1_dgemm<BM, BN, WM, WN, ST, BK, 0, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)Cfg::SMEM));
+}
+
+template <int BM, int BN, int WM, int WN, int ST, int BK>
+void launch_gemm(lyap_ctx* ctx, const Seed& s, const double* Bop, double* U, int64_t ncol, const K1Args& a,
+                 cudaStream_t st) {
+  using Cfg = DgemmCfg<BM, BN, WM, WN, ST, BK>;
+  const int kpad = (int)std::min<int64_t>(roundup(s.n, BK), s.npad);  // skip zero rows
+  dim3 grid((unsigned)((ncol / BN) * (s.npad / BM)));
+  K1EpiArgs ep{a, s.btl, s.F, s.g0, (int)s.npad, (int)(2 * s.npairs), (int)s.npairs, (int)s.n};
+  const int cpa = (int)(s.k * s.k);
+  switch (k1_fused(s.k) ? (int)s.k : 0) {
+    case 1:
+      k1_dgemm<BM, BN, WM, WN, ST, BK, 0, 1><<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(
+          s.Lf, Bop, nullptr, (int)s.npad, (int)ncol, kpad, (int)s.npad, a.nactive, cpa, DgemmOut{}, ep);
+      break;
+    case 2:
+      k1_dgemm<BM, BN, WM, WN, ST, BK, 0, 2><<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(
+          s.Lf, Bop, nullptr, (int)s.npad, (int)ncol, kpad, (int)s.npad, a.nactive, cpa, DgemmOut{}, ep);
+      break;
+    case 4:
+      k1_dgemm<BM, BN, WM, WN, ST, BK, 0, 4><<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(
+          s.Lf, Bop, nullptr, (int)s.npad, (int)ncol, kpad, (int)s.npad, a.nactive, cpa, DgemmOut{}, ep);
+      break;
+    default:
+      k1_dgemm<BM, BN, WM, WN, ST, BK><<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(s.Lf, Bop, U, (int)s.npad, (int)ncol,
+                                                                         kpad, (int)s.npad, a.nactive, cpa);
+  }
+}
+
 void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, cudaEvent_t evb = nullptr, cudaEvent_t eve = nullptr,
                unsigned evflags = 0, int group = 0) {
   const Seed& s = ctx->seed;
@@ -272,27 +315,21 @@ void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, cudaEvent_t evb 
     k1_gen<KK><<<grid, K1_THREADS, 0, st>>>(a, s.bhr, (int)s.npad, two_np, g.Bop, g.ncol);
   });
   LAUNCHED();
-  {
-    const int kpad = (int)std::min<int64_t>(roundup(s.n, s.n <= SMALL_N ? S_BK : G_BK), s.npad);  // skip zero rows
-    if (evb) CK(cudaEventRecordWithFlags(evb, st, evflags));
-    if (s.n <= SMALL_N) {
-      dim3 grid((unsigned)((g.ncol / S_BN) * (s.npad / S_BM)));
-      k1_dgemm<S_BM, S_BN, S_WM, S_WN, S_ST, S_BK><<<grid, SCfg::THREADS, SCfg::SMEM, st>>>(
-          s.Lf, g.Bop, g.U, (int)s.npad, (int)g.ncol, kpad, (int)s.npad, a.nactive, (int)(s.k * s.k));
-    } else {
-      dim3 grid((unsigned)((g.ncol / G_BN) * (s.npad / G_BM)));
-      k1_dgemm<G_BM, G_BN, G_WM, G_WN, G_ST, G_BK><<<grid, GCfg::THREADS, GCfg::SMEM, st>>>(
-          s.Lf, g.Bop, g.U, (int)s.npad, (int)g.ncol, kpad, (int)s.npad, a.nactive, (int)(s.k * s.k));
-    }
-    LAUNCHED();
-    if (eve) CK(cudaEventRecordWithFlags(eve, st, evflags));
-  }
-  K_DISPATCH(s.k, {
-    dim3 grid((unsigned)(s.npad / K1_TILE_C), (unsigned)((a.nslot + K1Tile<KK>::TS - 1) / K1Tile<KK>::TS));
-    k1_epi<KK><<<grid, K1_THREADS, 0, st>>>(a, g.U, g.ncol, s.btl, s.F, s.g0, (int)s.npad, two_np, (int)s.npairs,
-                                     (int)s.n);
-  });
+  if (evb) CK(cudaEventRecordWithFlags(evb, st, evflags));
+  if (s.n <= SMALL_N)
+    launch_gemm<S_BM, S_BN, S_WM, S_WN, S_ST, S_BK>(ctx, s, g.Bop, g.U, g.ncol, a, st);
+  else
+    launch_gemm<G_BM, G_BN, G_WM, G_WN, G_ST, G_BK>(ctx, s, g.Bop, g.U, g.ncol, a, st);
   LAUNCHED();
+  if (eve) CK(cudaEventRecordWithFlags(eve, st, evflags));
+  if (!k1_fused(s.k)) {
+    K_DISPATCH(s.k, {
+      dim3 grid((unsigned)(s.npad / K1_TILE_C), (unsigned)((a.nslot + K1Tile<KK>::TS - 1) / K1Tile<KK>::TS));
+      k1_epi<KK><<<grid, K1_THREADS, 0, st>>>(a, g.U, g.ncol, s.btl, s.F, s.g0, (int)s.npad, two_np, (int)s.npairs,
+                                              (int)s.n);
+    });
+    LAUNCHED();
+  }
 }
 
 
@@ -851,10 +888,8 @@ static int setup_core(int64_t n, int64_t k, const double* A0, const double* Bl, 
     CKB(cublasSetStream(ctx->cublas, ctx->stream));
     CKS(cusolverDnCreate(&ctx->cusolver));
     CKS(cusolverDnSetStream(ctx->cusolver, ctx->stream));
-    CK(cudaFuncSetAttribute(k1_dgemm<G_BM, G_BN, G_WM, G_WN, G_ST, G_BK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)GCfg::SMEM));
-    CK(cudaFuncSetAttribute(k1_dgemm<S_BM, S_BN, S_WM, S_WN, S_ST, S_BK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)SCfg::SMEM));
+    set_smem_attrs<G_BM, G_BN, G_WM, G_WN, G_ST, G_BK>(ctx);
+    set_smem_attrs<S_BM, S_BN, S_WM, S_WN, S_ST, S_BK>(ctx);
     cudaStream_t st = ctx->stream;
     CK(cudaEventRecord(ctx->ev0, st));
     Seed& s = ctx->seed;
