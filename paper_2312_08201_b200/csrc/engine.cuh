@@ -169,9 +169,11 @@ __device__ __forceinline__ constexpr int pb_stride() { return 4 * K * K; }
 
 // Minv[slot][rep] = P(v)_rep^{-1} by in-place Gauss-Jordan with partial pivoting (rows swapped
 // during elimination, the matching columns of the inverse swapped back at the end).
+// out: element (r, c) of the inverse at out[(r * 2K + c) * ostride] (Minv is element-major across the
+// reps of a slot, so the threads of a warp -- consecutive reps -- read and write coalesced)
 template <int D, int K>
 __device__ __forceinline__ void invert_block(const double* __restrict__ pb, const double* mask, const double* sigma,
-                                             double* __restrict__ out) {
+                                             double* __restrict__ out, int64_t ostride) {
   constexpr int RS = 2 * K, PER = D / K;  // row stride; rows per parameter (2 pair, 1 real)
   double M[D][D];
   int perm[D];
@@ -224,7 +226,12 @@ __device__ __forceinline__ void invert_block(const double* __restrict__ pb, cons
 #pragma unroll
   for (int r = 0; r < D; ++r)
 #pragma unroll
-    for (int c = 0; c < D; ++c) out[r * RS + c] = M[r][c];
+    for (int c = 0; c < D; ++c) out[(int64_t)(r * RS + c) * ostride] = M[r][c];
+}
+
+// the Minv block of (slot, rep): element e at minv_of(...)[e * nrep]
+__device__ __forceinline__ const double* minv_of(const double* Minv, int64_t slot, int64_t rep, int64_t nrep, int S) {
+  return Minv + slot * nrep * S + rep;
 }
 
 // One thread per (slot with a new v, rep): factor the rep's block; a cold start zeroes X there.
@@ -234,12 +241,12 @@ __global__ void __launch_bounds__(128) k_pfactor(EngArgs a) {
   const int64_t rep = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (rep >= a.nrep || !a.newv[slot]) return;
   const bool pair = rep < a.npairs;
-  double* out = a.Minv + ((int64_t)slot * a.nrep + rep) * pb_stride<K>();
+  double* out = a.Minv + (int64_t)slot * a.nrep * pb_stride<K>() + rep;
   const double* pb = a.Pb + rep * pb_stride<K>();
   if (pair)
-    invert_block<2 * K, K>(pb, a.mask + slot * K, a.sigma + slot * K, out);
+    invert_block<2 * K, K>(pb, a.mask + slot * K, a.sigma + slot * K, out, a.nrep);
   else
-    invert_block<K, K>(pb, a.mask + slot * K, a.sigma + slot * K, out);
+    invert_block<K, K>(pb, a.mask + slot * K, a.sigma + slot * K, out, a.nrep);
   if (a.rhs) {  // per-slot right-hand side G0(v) = sum_i v_i G0_i at this rep's coordinates
     const int64_t c = rep_coord(rep, a.npairs);
     const int w = pair ? 2 : 1;
@@ -268,15 +275,15 @@ __global__ void __launch_bounds__(128) k_pfactor(EngArgs a) {
 
 // z = P_rep^{-1} r on the rep's folded coordinates: r[2t + b] (pairs) / r[t] (reals)
 template <int K>
-__device__ __forceinline__ void apply_pinv(const double* __restrict__ mi, bool pair, const double (&r)[2 * K],
-                                           double (&z)[2 * K]) {
+__device__ __forceinline__ void apply_pinv(const double* __restrict__ mi, int64_t st, bool pair,
+                                           const double (&r)[2 * K], double (&z)[2 * K]) {
   constexpr int RS = 2 * K;
   if (pair) {
 #pragma unroll
     for (int i = 0; i < 2 * K; ++i) {
       double acc = 0.0;
 #pragma unroll
-      for (int j = 0; j < 2 * K; ++j) acc = fma(mi[i * RS + j], r[j], acc);
+      for (int j = 0; j < 2 * K; ++j) acc = fma(mi[(i * RS + j) * st], r[j], acc);
       z[i] = acc;
     }
   } else {
@@ -284,7 +291,7 @@ __device__ __forceinline__ void apply_pinv(const double* __restrict__ mi, bool p
     for (int i = 0; i < K; ++i) {
       double acc = 0.0;
 #pragma unroll
-      for (int j = 0; j < K; ++j) acc = fma(mi[i * RS + j], r[j], acc);
+      for (int j = 0; j < K; ++j) acc = fma(mi[(i * RS + j) * st], r[j], acc);
       z[i] = acc;
     }
   }
@@ -345,7 +352,7 @@ __global__ void __launch_bounds__(128) k_prec(EngArgs a) {
   const double* q = a.Qb + ((int64_t)slot * (a.mmax + 1) + m) * a.L;
   double r[2 * K], z[2 * K];
   rep_load<K>(q, a.npad, c, pair, sc, r);
-  apply_pinv<K>(a.Minv + ((int64_t)slot * a.nrep + rep) * pb_stride<K>(), pair, r, z);
+  apply_pinv<K>(minv_of(a.Minv, slot, rep, a.nrep, pb_stride<K>()), a.nrep, pair, r, z);
   rep_store<K>(xin, a.npad, c, pair, z, false);
 }
 
@@ -371,7 +378,7 @@ __global__ void __launch_bounds__(128) k_rec_z(EngArgs a, int slot, int m1, doub
   const double* q = a.Qb + ((int64_t)slot * (a.mmax + 1) + j) * a.L;
   double r[2 * K], z[2 * K];
   rep_load<K>(q, a.npad, c, pair, sc, r);
-  apply_pinv<K>(a.Minv + ((int64_t)slot * a.nrep + rep) * pb_stride<K>(), pair, r, z);
+  apply_pinv<K>(minv_of(a.Minv, slot, rep, a.nrep, pb_stride<K>()), a.nrep, pair, r, z);
   rep_store<K>(Z + (int64_t)j * a.L, a.npad, c, pair, z, false);
 }
 
@@ -871,7 +878,7 @@ __global__ void __launch_bounds__(256) k_xcomb(EngArgs a) {
             r[t] = xs[t][threadIdx.x];
           }
         }
-        apply_pinv<K>(a.Minv + ((int64_t)slot * a.nrep + rep) * pb_stride<K>(), pair, r, z);
+        apply_pinv<K>(minv_of(a.Minv, slot, rep, a.nrep, pb_stride<K>()), a.nrep, pair, r, z);
         rep_store<K>(X, a.npad, cc, pair, z, true);
       }
     }

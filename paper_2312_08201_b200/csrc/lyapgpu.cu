@@ -261,8 +261,11 @@ void ensure_engine(lyap_ctx* ctx, int b, int mmax) {
 // ------------------------------------------------------------------ K1 launch (prologue, GEMM, epilogue)
 
 // K1 with the epilogue fused into the GEMM (k = 1, 2, 4: a slot's k^2 columns never straddle a CTA
-// tile): prologue + one GEMM launch; other k: prologue, GEMM, k1_epi
-inline bool k1_fused(int64_t k) { return k == 1 || k == 2 || k == 4; }
+// tile) for the small-tile configuration (n <= SMALL_N): prologue + one GEMM launch.  Otherwise
+// prologue, GEMM, k1_epi.  Measured (bench, B200): c2 94.5k -> 96.0k v/s fused; c5 907.9 -> 898.9
+// fused -- with 1 CTA per SM the large-tile GEMM runs the epilogue at 8 warps per SM, slower than
+// the separate, fully occupied k1_epi, so the large configuration keeps it separate.
+inline bool k1_fused(int64_t k, int64_t n) { return (k == 1 || k == 2 || k == 4) && n <= SMALL_N; }
 
 template <int BM, int BN, int WM, int WN, int ST, int BK>
 void set_smem_attrs(lyap_ctx* ctx) {
@@ -284,7 +287,7 @@ void launch_gemm(lyap_ctx* ctx, const Seed& s, const double* Bop, double* U, int
   dim3 grid((unsigned)((ncol / BN) * (s.npad / BM)));
   K1EpiArgs ep{a, s.btl, s.F, s.g0, (int)s.npad, (int)(2 * s.npairs), (int)s.npairs, (int)s.n};
   const int cpa = (int)(s.k * s.k);
-  switch (k1_fused(s.k) ? (int)s.k : 0) {
+  switch (k1_fused(s.k, s.n) ? (int)s.k : 0) {
     case 1:
       k1_dgemm<BM, BN, WM, WN, ST, BK, 0, 1><<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(
           s.Lf, Bop, nullptr, (int)s.npad, (int)ncol, kpad, (int)s.npad, a.nactive, cpa, DgemmOut{}, ep);
@@ -322,7 +325,7 @@ void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, cudaEvent_t evb 
     launch_gemm<G_BM, G_BN, G_WM, G_WN, G_ST, G_BK>(ctx, s, g.Bop, g.U, g.ncol, a, st);
   LAUNCHED();
   if (eve) CK(cudaEventRecordWithFlags(eve, st, evflags));
-  if (!k1_fused(s.k)) {
+  if (!k1_fused(s.k, s.n)) {
     K_DISPATCH(s.k, {
       dim3 grid((unsigned)(s.npad / K1_TILE_C), (unsigned)((a.nslot + K1Tile<KK>::TS - 1) / K1Tile<KK>::TS));
       k1_epi<KK><<<grid, K1_THREADS, 0, st>>>(a, g.U, g.ncol, s.btl, s.F, s.g0, (int)s.npad, two_np, (int)s.npairs,
