@@ -117,6 +117,19 @@ def main():
         Pm = sm.pminv(Vt)
         minv = lambda r: sm.papply(Pm, r.reshape(1, k, n)).reshape(-1)
         out = [f"pair:{gmres_prec(sm, v, minv)}"]
+        sig = (1.0 / Vt).to(torch.complex128).repeat_interleave(n, dim=1)[0]
+        for p in ps:
+            # two-level (coarse-grid) preconditioner with a v-independent space Z: per v only the
+            # p x p Galerkin matrix E(v) = Z^H C(v) Z (cheap from Gram blocks) is factored
+            for zname, Z in (("V", V[:, :p]), ("UV", torch.linalg.qr(torch.cat([U[:, : p // 2], V[:, : p // 2]], 1))[0])):
+                TZ = sm.T(Z.T.reshape(-1, k, n)).reshape(-1, n * k).T
+                CZ = sig[:, None] * Z - TZ
+                Einv = torch.linalg.inv(Z.conj().T @ CZ)
+
+                def pinv2(r, Z=Z, CZ=CZ, Einv=Einv):
+                    w = Einv @ (Z.conj().T @ r)
+                    return Z @ w + minv(r - CZ @ w)
+                out.append(f"2L{zname}{p}:{gmres_prec(sm, v, pinv2)}")
         for p in ps:
             Up, Sp, Vp = U[:, :p], S[:p], V[:, :p]
             MU = torch.stack([minv(Up[:, i]) for i in range(p)], 1)  # N x p
