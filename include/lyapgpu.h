@@ -77,6 +77,12 @@ typedef struct {
                           A(v) has an eigenvalue with Re >= 0 are discarded) runs first; such v get
                           status LYAP_V_UNSTABLE and trace NaN, are not solved and do NOT make the
                           call return LYAP_EPARTIAL.  See lyap_stable_batch.  default 0 */
+  int32_t coarse;      /* size p of the coarse space of the two-level preconditioner:
+                          P(v)^{-1} r = y + M(v)^{-1}(r - C(v) y), y = Z E(v)^{-1} Z^T r, E(v) = Z^T C(v) Z,
+                          with M(v) the exact pair blocks and Z the p dominant right singular vectors
+                          of the off-block coupling T_o (randomized SVD at the first trace_batch).
+                          -1 (default) auto: 128 when n k >= 3000, else off; 0 off; > 0 that size
+                          (multiple of 8, <= 256).  Recycle spaces are not used together with it. */
 } lyap_opts;
 
 typedef struct {

@@ -42,7 +42,8 @@ class Problem:
 
     def __init__(self, A0, Bl, Br, Q, E, *, tol: float = 1e-12, max_dim: int = 0, max_restarts: int = 30,
                  batch: int = 0, warm_start: bool = False, max_cond_S: float = 1e8, device: int = -1,
-                 profile: bool = False, schedule: bool = True, recycle: int = -1, check_stable: bool = False):
+                 profile: bool = False, schedule: bool = True, recycle: int = -1, check_stable: bool = False,
+                 coarse: int = -1):
         A0 = _f64(A0)
         n = A0.shape[0]
         Bl = _f64(Bl)
@@ -64,6 +65,7 @@ class Problem:
         o.schedule = int(schedule)
         o.recycle = int(recycle)
         o.check_stable = int(check_stable)
+        o.coarse = int(coarse)
         self._ctx = C.c_void_p()
         setup = lib.lyap_setup_qlin if qlin else lib.lyap_setup
         rc = setup(n, k, _dp(A0), _dp(Bl), _dp(Br), _dp(Q), _dp(E), C.byref(o), C.byref(self._ctx))

@@ -28,7 +28,7 @@ class Opts(C.Structure):
     _fields_ = [("tol", C.c_double), ("max_dim", C.c_int32), ("max_restarts", C.c_int32),
                 ("batch", C.c_int32), ("warm_start", C.c_int32), ("max_cond_S", C.c_double),
                 ("device", C.c_int32), ("profile", C.c_int32), ("schedule", C.c_int32), ("recycle", C.c_int32),
-                ("check_stable", C.c_int32)]
+                ("check_stable", C.c_int32), ("coarse", C.c_int32)]
 
 
 class Info(C.Structure):

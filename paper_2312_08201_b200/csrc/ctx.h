@@ -79,6 +79,9 @@ struct Engine {
   double *cf = nullptr;                           // b x (mmax+1) projection coefficients
   double *Hraw = nullptr;                         // b x (mmax+1) x mmax unrotated Hessenberg (recycle build)
   int *phase = nullptr, *m = nullptr, *vidx = nullptr, *applies = nullptr, *restarts = nullptr;
+  // two-level preconditioner (coarse p > 0): flexible basis Zb = P^{-1} q_j, coarse scratch
+  double *Zb = nullptr, *Rbuf = nullptr, *Yz = nullptr, *TYz = nullptr, *Cc = nullptr, *Wc = nullptr, *Einv = nullptr;
+  int pc = 0;                                     // coarse size the buffers were made for
   int* ctrl = nullptr;                            // per group 8 ints: [2]=active slots, [4..5]=applied vectors;
                                                   // then 8 shared: [0]=next queue position, [1]=done count
   int* h_ctrl = nullptr;                          // pinned mirror
@@ -95,6 +98,14 @@ struct Engine {
 };
 
 }  // namespace lyap
+
+// Coarse space of the two-level preconditioner, built on first use.
+struct CoarseSpace {
+  int p = 0;                       // size (0: off)
+  double *Z = nullptr, *TZ = nullptr;     // L x p column-major: the space and T Z
+  double *Phi = nullptr, *Psi = nullptr;  // k x p x p column-major: Z_t^T Z_t, Z_t^T (T Z)_t
+  double build_ms = 0.0;
+};
 
 // Stability filter tables (stab.cuh), built on first use.
 struct StabTables {
@@ -127,6 +138,9 @@ struct lyap_ctx {
   cudaGraphExec_t gexec[4] = {};  // per slot group: the engine iteration graph, kept across calls
   std::vector<cudaEvent_t> prof_evs;  // K1 timing events of the graphs (opts.profile)
   StabTables stab;
+  CoarseSpace coarse;
+  cublasHandle_t cublas_eng[4] = {};  // per slot group: cuBLAS inside the captured engine iterations
+  double* cublas_ws[4] = {};
   double* Spad = nullptr;  // lyap_solution: padded S_r^T and S_r (row-major np x np each)
   cudaEvent_t xjoin[4] = {};
 };

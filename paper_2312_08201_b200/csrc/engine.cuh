@@ -56,6 +56,11 @@ struct EngArgs {
   int nterms;
   const double* t0t;
   double *rhs, *t0s;
+  // two-level preconditioner (pc > 0): coarse space Z (L x pc), T Z, Gram blocks
+  // Phi_t / Psi_t (k x pc x pc); per slot E(v)^{-1} (pc x pc), flexible basis Zb (as Qb), scratch
+  int pc;
+  const double *Zc, *TZc, *Phi, *Psi;
+  double *Einv, *Zb, *Rbuf, *Yz, *TYz, *Cc, *Wc;
   int32_t* status;
   int32_t* out_applies;
   double* out_resid;
@@ -352,8 +357,148 @@ __global__ void __launch_bounds__(128) k_prec(EngArgs a) {
   const double* q = a.Qb + ((int64_t)slot * (a.mmax + 1) + m) * a.L;
   double r[2 * K], z[2 * K];
   rep_load<K>(q, a.npad, c, pair, sc, r);
+  if (a.pc > 0) {
+    // two-level: z = y + M^{-1} (r - C(v) y), y = Z E^{-1} Z^T r (Yz), T y (TYz) from the coarse GEMMs;
+    // C(v) y = sigma o y - T y on unmasked rows, y on masked ones
+    double y[2 * K], ty[2 * K];
+    rep_load<K>(a.Yz + (int64_t)slot * a.L, a.npad, c, pair, 1.0, y);
+    rep_load<K>(a.TYz + (int64_t)slot * a.L, a.npad, c, pair, 1.0, ty);
+#pragma unroll
+    for (int t = 0; t < K; ++t) {
+      const double msk = a.mask[slot * K + t], sg = a.sigma[slot * K + t];
+#pragma unroll
+      for (int q2 = 0; q2 < 2; ++q2) {
+        const int i = pair ? 2 * t + q2 : t;
+        if (!pair && q2) break;
+        r[i] -= msk != 0.0 ? sg * y[i] - ty[i] : y[i];
+      }
+    }
+    apply_pinv<K>(minv_of(a.Minv, slot, rep, a.nrep, pb_stride<K>()), a.nrep, pair, r, z);
+#pragma unroll
+    for (int i = 0; i < 2 * K; ++i) z[i] += y[i];
+    rep_store<K>(xin, a.npad, c, pair, z, false);
+    rep_store<K>(a.Zb + ((int64_t)slot * (a.mmax + 1) + m) * a.L, a.npad, c, pair, z, false);
+    return;
+  }
   apply_pinv<K>(minv_of(a.Minv, slot, rep, a.nrep, pb_stride<K>()), a.nrep, pair, r, z);
   rep_store<K>(xin, a.npad, c, pair, z, false);
+}
+
+// ---------------------------------------------------------------- two-level preconditioner
+// k_cfactor (one CTA per slot with a new v): E(v) = sum_t (v_t != 0 ? sigma_t Phi_t - Psi_t : Phi_t)
+// (= Z^T C(v) Z, the Galerkin coarse matrix) and its inverse by Gauss-Jordan with partial pivoting in
+// shared memory; Einv[slot] (pc x pc, column-major).
+__global__ void __launch_bounds__(256) k_cfactor(EngArgs a) {
+  extern __shared__ double E[];  // pc x pc column-major, then pc (pivot scratch)
+  const int slot = blockIdx.x;
+  if (!a.newv[slot]) return;
+  const int p = a.pc, tid = threadIdx.x, nt = blockDim.x;
+  const int64_t pp = (int64_t)p * p;
+  for (int64_t e = tid; e < pp; e += nt) {
+    double v = 0.0;
+    for (int t = 0; t < a.K; ++t) {
+      const double phi = a.Phi[t * pp + e];
+      v += a.mask[slot * a.K + t] != 0.0 ? a.sigma[slot * a.K + t] * phi - a.Psi[t * pp + e] : phi;
+    }
+    E[e] = v;
+  }
+  __shared__ int piv_s;
+  __shared__ double pinv_s;
+  int* perm = reinterpret_cast<int*>(E + pp);
+  __syncthreads();
+  for (int c = 0; c < p; ++c) {
+    if (tid < 32) {  // pivot: largest |E(r, c)|, r >= c (first on ties)
+      double best = -1.0;
+      int arg = c;
+      for (int r = c + tid; r < p; r += 32) {
+        const double v = fabs(E[(int64_t)c * p + r]);
+        if (v > best) {
+          best = v;
+          arg = r;
+        }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_down_sync(0xffffffffu, best, o);
+        const int oa = __shfl_down_sync(0xffffffffu, arg, o);
+        if (ob > best || (ob == best && oa < arg)) {
+          best = ob;
+          arg = oa;
+        }
+      }
+      if (tid == 0) {
+        piv_s = arg;
+        perm[c] = arg;
+      }
+    }
+    __syncthreads();
+    const int pr = piv_s;
+    if (pr != c)
+      for (int j = tid; j < p; j += nt) {
+        const double t = E[(int64_t)j * p + c];
+        E[(int64_t)j * p + c] = E[(int64_t)j * p + pr];
+        E[(int64_t)j * p + pr] = t;
+      }
+    __syncthreads();
+    if (tid == 0) {
+      const double pv = E[(int64_t)c * p + c];
+      pinv_s = pv != 0.0 ? 1.0 / pv : 0.0;
+      E[(int64_t)c * p + c] = 1.0;
+    }
+    __syncthreads();
+    const double inv = pinv_s;
+    for (int j = tid; j < p; j += nt) E[(int64_t)j * p + c] *= inv;  // row c
+    __syncthreads();
+    // eliminate column c from every other row: E(r, j) -= E(r, c) E(c, j); the column-c factors
+    // are read before any thread overwrites them (E(r, c) is set to 0 -> the identity column)
+    for (int64_t e = tid; e < pp; e += nt) {
+      const int r = (int)(e % p), j = (int)(e / p);
+      if (r == c || j == c) continue;
+      E[e] = fma(-E[(int64_t)c * p + r], E[(int64_t)j * p + c], E[e]);
+    }
+    __syncthreads();
+    for (int r = tid; r < p; r += nt)
+      if (r != c) E[(int64_t)c * p + r] = -E[(int64_t)c * p + r] * E[(int64_t)c * p + c];
+    __syncthreads();
+  }
+  // undo the row swaps as column swaps of the inverse, in reverse order
+  for (int c = p - 1; c >= 0; --c) {
+    const int pr = perm[c];
+    if (pr != c)
+      for (int r = tid; r < p; r += nt) {
+        const double t = E[(int64_t)c * p + r];
+        E[(int64_t)c * p + r] = E[(int64_t)pr * p + r];
+        E[(int64_t)pr * p + r] = t;
+      }
+    __syncthreads();
+  }
+  double* out = a.Einv + (int64_t)slot * pp;
+  for (int64_t e = tid; e < pp; e += nt) out[e] = E[e];
+}
+
+// k_cpre: Rbuf[slot] = q^_m / eta_m for a slot whose next K1 input is a Krylov direction, else 0
+__global__ void __launch_bounds__(256) k_cpre(EngArgs a) {
+  const int slot = blockIdx.y;
+  const int ph = a.phase[slot];
+  const bool on = ph == PH_ITER && a.m[slot] >= a.su[slot];
+  double* rb = a.Rbuf + (int64_t)slot * a.L;
+  const int m = on ? a.m[slot] : 0;
+  const double sc = on ? 1.0 / a.eta[(int64_t)slot * (a.mmax + 1) + m] : 0.0;
+  const double* q = a.Qb + ((int64_t)slot * (a.mmax + 1) + m) * a.L;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < a.L; e += (int64_t)gridDim.x * blockDim.x)
+    rb[e] = on ? sc * q[e] : 0.0;
+}
+
+// k_cw: Wc[:, slot] = E(v)^{-1} Cc[:, slot]  (one block per slot; rows over threads)
+__global__ void __launch_bounds__(128) k_cw(EngArgs a) {
+  const int slot = blockIdx.x;
+  const int p = a.pc;
+  const double* Ei = a.Einv + (int64_t)slot * p * p;
+  const double* cc = a.Cc + (int64_t)slot * p;
+  for (int r = threadIdx.x; r < p; r += blockDim.x) {
+    double acc = 0.0;
+    for (int j = 0; j < p; ++j) acc = fma(Ei[(int64_t)j * p + r], cc[j], acc);
+    a.Wc[(int64_t)slot * p + r] = acc;
+  }
 }
 
 // lyap_build_recycle helpers: Z[:, j] = P(v)^{-1} q^_j / eta_j, or u_j for j < su (the search
@@ -668,7 +813,8 @@ __device__ __forceinline__ void warp_backsub(const EngArgs& a, int slot, int lan
         ev = (lane < c) ? fma(-Rr[c], yc, ev) : ev;
       }
     }
-    if (lane < nb) y[i] = i < su ? yl : yl / eta[i];  // u_i raw; P^{-1} q^_i / eta_i
+    // u_i raw; P^{-1} q^_i / eta_i (two-level: Zb_i = P^{-1} q^_i / eta_i is stored, coefficient raw)
+    if (lane < nb) y[i] = (i < su || a.pc > 0) ? yl : yl / eta[i];
     double yb[32];
 #pragma unroll
     for (int c = 0; c < 32; ++c) yb[c] = __shfl_sync(0xffffffffu, yl, c);
@@ -827,7 +973,7 @@ __global__ void __launch_bounds__(256) k_xcomb(EngArgs a) {
   const double* ysl = a.y + (int64_t)slot * a.mmax;
   for (int i = threadIdx.x; i < m1; i += blockDim.x) ys[i] = i < su ? 0.0 : ysl[i];
   __syncthreads();
-  const double* Q = a.Qb + (int64_t)slot * (a.mmax + 1) * a.L;
+  const double* Q = (a.pc > 0 ? a.Zb : a.Qb) + (int64_t)slot * (a.mmax + 1) * a.L;  // two-level: Z_j = P^{-1} q_j
   double* X = a.X + (int64_t)slot * a.L;
   const int el = threadIdx.x & 63, sl = threadIdx.x >> 6;
   for (int64_t c0 = (int64_t)blockIdx.x * 64; c0 < a.npad; c0 += (int64_t)gridDim.x * 64) {
@@ -862,6 +1008,14 @@ __global__ void __launch_bounds__(256) k_xcomb(EngArgs a) {
         X[e] += acc;
       }
       __syncthreads();
+    }
+    if (a.pc > 0) {  // flexible basis: the directions are already preconditioned
+      for (int idx = threadIdx.x; idx < K * 64; idx += blockDim.x) {
+        const int64_t cc = c0 + (idx & 63);
+        if (cc < a.npad) X[(int64_t)(idx >> 6) * a.npad + cc] += xs[idx >> 6][idx & 63];
+      }
+      __syncthreads();
+      continue;
     }
     if (threadIdx.x < 64) {
       const int64_t cc = c0 + threadIdx.x;

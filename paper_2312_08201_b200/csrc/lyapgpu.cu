@@ -133,7 +133,7 @@ void upload_seeds(lyap_ctx* ctx) {
 void free_engine(Engine& g, bool keep_order = true) {
   void* ps[] = {g.Bop, g.U, g.Xin, g.X, g.Qb, g.Minv, g.sigma, g.mask, g.eta, g.H, g.e, g.y,
                 g.bnorm, g.part, g.part3, g.phase, g.m, g.vidx, g.applies, g.restarts, g.ctrl,
-                g.part2, g.Gq, g.cf, g.Hraw, g.rhs, g.t0s};
+                g.part2, g.Gq, g.cf, g.Hraw, g.rhs, g.t0s, g.Zb, g.Rbuf, g.Yz, g.TYz, g.Cc, g.Wc, g.Einv};
   for (void* p : ps) dfree(p);
   if (g.h_ctrl) cudaFreeHost(g.h_ctrl);
   int* order = g.order;
@@ -207,10 +207,14 @@ void configure_run(const Seed& s, Engine& g, int b) {
 // The engine is allocated for a capacity of bcap slots and reused by any later call that needs
 // b <= bcap slots with the same restart length (NEXT row f3: optimizer-style callers change nv on
 // every call; reallocating the multi-GB Krylov basis each time dominated their run time).
+int coarse_size(const lyap_ctx* ctx);
+void ensure_coarse(lyap_ctx* ctx);
+
 void ensure_engine(lyap_ctx* ctx, int b, int mmax) {
   Engine& g = ctx->eng;
   const Seed& s = ctx->seed;
-  if (g.Qb && g.mmax == mmax && g.bcap >= b) {
+  const int pc = ctx->coarse.p;
+  if (g.Qb && g.mmax == mmax && g.bcap >= b && g.pc == pc) {
     configure_run(s, g, b);
     return;
   }
@@ -247,6 +251,16 @@ void ensure_engine(lyap_ctx* ctx, int b, int mmax) {
   if (s.qlin) {  // per-slot right-hand side G0(v) and t0(v) of a v-linear Q
     g.rhs = dalloc<double>(ctx, (size_t)b * g.L);
     g.t0s = dalloc<double>(ctx, b);
+  }
+  g.pc = pc;
+  if (pc > 0) {  // two-level preconditioner: flexible basis and coarse scratch
+    g.Zb = dalloc<double>(ctx, (size_t)b * (mmax + 1) * g.L, false);
+    g.Rbuf = dalloc<double>(ctx, (size_t)b * g.L);
+    g.Yz = dalloc<double>(ctx, (size_t)b * g.L);
+    g.TYz = dalloc<double>(ctx, (size_t)b * g.L);
+    g.Cc = dalloc<double>(ctx, (size_t)b * pc);
+    g.Wc = dalloc<double>(ctx, (size_t)b * pc);
+    g.Einv = dalloc<double>(ctx, (size_t)b * pc * pc);
   }
   g.phase = dalloc<int>(ctx, b);
   g.m = dalloc<int>(ctx, b);
@@ -351,6 +365,8 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   }
   const Seed& s = ctx->seed;
   const int b = auto_batch(ctx, nv), mmax = auto_mmax(ctx);
+  if (coarse_size(ctx) > 0 && !record) ensure_coarse(ctx);
+  const bool two_level = ctx->coarse.p > 0 && !record;
   ensure_engine(ctx, b, mmax);
   ctx->info.batch = b;
   Engine& g = ctx->eng;
@@ -380,6 +396,11 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   a.t0t = s.t0t;
   a.rhs = s.qlin ? g.rhs : nullptr;
   a.t0s = s.qlin ? g.t0s : nullptr;
+  a.pc = two_level ? g.pc : 0;
+  a.Zc = ctx->coarse.Z;
+  a.TZc = ctx->coarse.TZ;
+  a.Phi = ctx->coarse.Phi;
+  a.Psi = ctx->coarse.Psi;
   a.max_restarts = ctx->opts.max_restarts;
   a.warm = ctx->opts.warm_start;
   a.V = dV;
@@ -445,6 +466,15 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
       x.rhs = g.rhs + s0 * g.L;
       x.t0s = g.t0s + s0;
     }
+    if (x.pc > 0) {
+      x.Zb = g.Zb + s0 * ld * g.L;
+      x.Rbuf = g.Rbuf + s0 * g.L;
+      x.Yz = g.Yz + s0 * g.L;
+      x.TYz = g.TYz + s0 * g.L;
+      x.Cc = g.Cc + s0 * x.pc;
+      x.Wc = g.Wc + s0 * x.pc;
+      x.Einv = g.Einv + s0 * (int64_t)x.pc * x.pc;
+    }
     x.Hraw = g.Hraw + s0 * ld * mmax;
     x.ctrl = g.ctrl + 8 * gi;
     ga[gi] = x;
@@ -466,6 +496,16 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   }
 
   const size_t upd_smem = sizeof(double) * (mmax + 1);
+  const size_t cf_smem = sizeof(double) * (size_t)a.pc * a.pc + sizeof(int) * (size_t)a.pc + 16;
+  if (a.pc > 0) {
+    CK(cudaFuncSetAttribute(k_cfactor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cf_smem));
+    for (int gi = 0; gi < G; ++gi)
+      if (!ctx->cublas_eng[gi]) {  // a handle per slot group with its own workspace (graph capture)
+        CKB(cublasCreate(&ctx->cublas_eng[gi]));
+        ctx->cublas_ws[gi] = dalloc<double>(ctx, (32u << 20) / 8, false);
+        CKB(cublasSetWorkspace(ctx->cublas_eng[gi], ctx->cublas_ws[gi], 32u << 20));
+      }
+  }
   const size_t ctrl_smem = sizeof(double) * 16 * (size_t)(mmax + 2);
   const size_t gram_smem = sizeof(double) * (size_t)(mmax + 1);
   if (gram_smem > 48 * 1024) CK(cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_smem));
@@ -497,6 +537,21 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
     LAUNCHED();
     K_DISPATCH(s.k, (k_pfactor<KK><<<grep, 128, 0, sg>>>(x)));
     LAUNCHED();
+    if (x.pc > 0) {  // two-level preconditioner: coarse factor, Z^T r, E^{-1}, Z w and T Z w (cuBLAS)
+      const int p = x.pc, Li = (int)g.L;
+      const double one = 1.0, zero = 0.0;
+      cublasHandle_t hb = ctx->cublas_eng[gi];
+      CKB(cublasSetStream(hb, sg));
+      k_cfactor<<<bg, 256, cf_smem, sg>>>(x);
+      LAUNCHED();
+      k_cpre<<<dim3((unsigned)std::min<int64_t>((g.L + 255) / 256, 64), (unsigned)bg), 256, 0, sg>>>(x);
+      LAUNCHED();
+      CKB(cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, p, bg, Li, &one, x.Zc, Li, x.Rbuf, Li, &zero, x.Cc, p));
+      k_cw<<<bg, 128, 0, sg>>>(x);
+      LAUNCHED();
+      CKB(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, Li, bg, p, &one, x.Zc, Li, x.Wc, p, &zero, x.Yz, Li));
+      CKB(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, Li, bg, p, &one, x.TZc, Li, x.Wc, p, &zero, x.TYz, Li));
+    }
     K_DISPATCH(s.k, (k_prec<KK><<<grep, 128, 0, sg>>>(x)));
     LAUNCHED();
     if (x.s_rec > 0) {
@@ -770,6 +825,159 @@ void stab_count(lyap_ctx* ctx, int64_t nv, const double* dV, int32_t* dnu, cudaS
   LAUNCHED();
 }
 
+// size of the coarse space (opts.coarse): auto = 128 when n k >= 3000
+int coarse_size(const lyap_ctx* ctx) {
+  const Seed& s = ctx->seed;
+  int p = ctx->opts.coarse < 0 ? (s.n * s.k >= 3000 ? 128 : 0) : ctx->opts.coarse;
+  p = std::min<int>(p, 256);
+  p = std::min<int64_t>(p, (s.n * s.k) / 2);
+  return p < 8 ? 0 : p / 8 * 8;
+}
+
+// In-place orthonormal basis of the columns of A (m x l, column-major): Householder QR (cuSOLVER).
+void qr_inplace(lyap_ctx* ctx, double* A, int m, int l) {
+  cudaStream_t st = ctx->stream;
+  double* tau = dalloc<double>(ctx, l, false);
+  int* dinfo = dalloc<int>(ctx, 1);
+  int lw1 = 0, lw2 = 0;
+  CKS(cusolverDnDgeqrf_bufferSize(ctx->cusolver, m, l, A, m, &lw1));
+  CKS(cusolverDnDorgqr_bufferSize(ctx->cusolver, m, l, l, A, m, tau, &lw2));
+  double* work = dalloc<double>(ctx, std::max(lw1, lw2), false);
+  CKS(cusolverDnDgeqrf(ctx->cusolver, m, l, A, m, tau, work, std::max(lw1, lw2), dinfo));
+  CKS(cusolverDnDorgqr(ctx->cusolver, m, l, l, A, m, tau, work, std::max(lw1, lw2), dinfo));
+  CK(cudaStreamSynchronize(st));
+  dfree(tau);
+  dfree(dinfo);
+  dfree(work);
+}
+
+// Coarse space of the two-level preconditioner, built once per ctx: the explicit
+// folded T (K1 on unit vectors), minus its pair blocks (the part P(v) already inverts exactly) = T_o';
+// Z = the p dominant right singular vectors of T_o' (randomized range finder, two power iterations,
+// cuSOLVER QR/SVD of the tall sketches); T Z (K1); the Gram blocks Phi_t = Z_t^T Z_t and
+// Psi_t = Z_t^T (T Z)_t from which every v's coarse matrix E(v) = sum_t sigma_t Phi_t - Psi_t is formed.
+void ensure_coarse(lyap_ctx* ctx) {
+  CoarseSpace& C = ctx->coarse;
+  const int p = coarse_size(ctx);
+  if (p == 0 || (C.Z && C.p == p)) return;
+  const Seed& s = ctx->seed;
+  const int64_t L = s.k * s.npad, k = s.k;
+  const int l = p + 16, Li = (int)L;
+  cudaStream_t st = ctx->stream;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, st));
+  double *Tm = nullptr, *X = nullptr, *Y = nullptr, *Om = nullptr, *Ys = nullptr, *Bt = nullptr, *Sv = nullptr,
+         *U = nullptr, *work = nullptr, *rwork = nullptr;
+  int* dinfo = nullptr;
+  try {
+    for (double* q : {C.Z, C.TZ, C.Phi, C.Psi}) dfree(q);
+    C = CoarseSpace{};
+    // 1. explicit folded T, column-major L x L
+    Tm = dalloc<double>(ctx, (size_t)L * L, false);
+    const int64_t cb = 512;
+    X = dalloc<double>(ctx, (size_t)cb * L, false);
+    Y = dalloc<double>(ctx, (size_t)cb * L, false);
+    for (int64_t c0 = 0; c0 < L; c0 += cb) {
+      const int64_t nb = std::min(cb, L - c0);
+      k_unit_vectors<<<1024, 256, 0, st>>>(X, c0, nb, L);
+      LAUNCHED();
+      const int rc = lyap_apply_C(ctx, nb, X, nullptr, Y, st);
+      if (rc != LYAP_OK) throw Fail{rc};
+      k_neg_copy<<<1024, 256, 0, st>>>(Y, Tm + c0 * L, nb * L);
+      LAUNCHED();
+    }
+    // 2. minus the pair blocks
+    K_DISPATCH(k, (k_sub_pblocks<KK><<<(unsigned)((s.nrep + 127) / 128), 128, 0, st>>>(Tm, L, s.npad, s.Pb, s.npairs,
+                                                                                          s.nrep)));
+    LAUNCHED();
+    // 3. randomized SVD: right singular vectors of T_o'
+    {
+      std::vector<double> h((size_t)L * l);
+      uint64_t x = 0x2545f4914f6cdd1dULL;
+      for (double& e : h) {
+        x += 0x9e3779b97f4a7c15ULL;
+        uint64_t z = x;
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+        z ^= z >> 31;
+        e = (double)(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+      }
+      Om = dalloc<double>(ctx, h.size(), false);
+      CK(cudaMemcpy(Om, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
+    }
+    Ys = dalloc<double>(ctx, (size_t)L * l, false);
+    const double one = 1.0, zero = 0.0;
+    CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, Li, l, Li, &one, Tm, Li, Om, Li, &zero, Ys, Li));
+    for (int q = 0; q < 2; ++q) {  // power iterations: (T T^T)^q T Omega, re-orthonormalised
+      qr_inplace(ctx, Ys, Li, l);
+      CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_T, CUBLAS_OP_N, Li, l, Li, &one, Tm, Li, Ys, Li, &zero, Om, Li));
+      qr_inplace(ctx, Om, Li, l);
+      CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, Li, l, Li, &one, Tm, Li, Om, Li, &zero, Ys, Li));
+    }
+    qr_inplace(ctx, Ys, Li, l);  // Q: range of T_o'
+    Bt = Om;                     // B^T = T_o'^T Q  (L x l); B = Q^T T_o' = V S U^T, so the left singular
+    CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_T, CUBLAS_OP_N, Li, l, Li, &one, Tm, Li, Ys, Li, &zero, Bt, Li));
+    Sv = dalloc<double>(ctx, l, false);  // vectors of B^T are T_o''s right singular vectors
+    U = dalloc<double>(ctx, (size_t)L * l, false);
+    dinfo = dalloc<int>(ctx, 1);
+    int lwork = 0;
+    CKS(cusolverDnDgesvd_bufferSize(ctx->cusolver, Li, l, &lwork));
+    work = dalloc<double>(ctx, std::max(lwork, 1), false);
+    rwork = dalloc<double>(ctx, l, false);
+    signed char ju = 'S', jv = 'N';
+    CKS(cusolverDnDgesvd(ctx->cusolver, ju, jv, Li, l, Bt, Li, Sv, U, Li, nullptr, 1, work, lwork, rwork, dinfo));
+    int hinfo = 0;
+    CK(cudaMemcpyAsync(&hinfo, dinfo, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (hinfo != 0) {
+      set_err(ctx, "coarse space: gesvd info = %d", hinfo);
+      throw Fail{LYAP_ECUDA};
+    }
+    dfree(Tm);
+    Tm = nullptr;
+    // 4. Z = the first p columns; T Z through K1
+    C.Z = dalloc<double>(ctx, (size_t)L * p, false);
+    CK(cudaMemcpyAsync(C.Z, U, (size_t)L * p * 8, cudaMemcpyDeviceToDevice, st));
+    C.TZ = dalloc<double>(ctx, (size_t)L * p, false);
+    {
+      const int rc = lyap_apply_C(ctx, p, C.Z, nullptr, C.TZ, st);
+      if (rc != LYAP_OK) throw Fail{rc};
+      k_negate<<<(unsigned)std::min<int64_t>((L * p + 255) / 256, 65535), 256, 0, st>>>(C.TZ, L * p);
+      LAUNCHED();
+    }
+    // 5. Gram blocks per parameter t (row block t of Z / T Z)
+    C.Phi = dalloc<double>(ctx, (size_t)k * p * p, false);
+    C.Psi = dalloc<double>(ctx, (size_t)k * p * p, false);
+    const int np = (int)s.npad;
+    for (int64_t t = 0; t < k; ++t) {
+      CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_T, CUBLAS_OP_N, p, p, np, &one, C.Z + t * np, Li, C.Z + t * np, Li, &zero,
+                      C.Phi + t * p * p, p));
+      CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_T, CUBLAS_OP_N, p, p, np, &one, C.Z + t * np, Li, C.TZ + t * np, Li, &zero,
+                      C.Psi + t * p * p, p));
+    }
+    C.p = p;
+    CK(cudaEventRecord(e1, st));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    C.build_ms = ms;
+  } catch (Fail f) {
+    for (void* q : {(void*)Tm, (void*)X, (void*)Y, (void*)Om, (void*)Ys, (void*)Sv, (void*)U, (void*)work,
+                    (void*)rwork, (void*)dinfo})
+      dfree(q);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    throw;
+  }
+  for (void* q : {(void*)Tm, (void*)X, (void*)Y, (void*)Om, (void*)Ys, (void*)Sv, (void*)U, (void*)work, (void*)rwork,
+                  (void*)dinfo})
+    dfree(q);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+}
+
 }  // namespace
 
 // ====================================================================== C-ABI
@@ -788,6 +996,8 @@ void lyap_default_opts(lyap_opts* o) {
   o->profile = 0;
   o->schedule = 1;
   o->recycle = -1;
+  o->check_stable = 0;
+  o->coarse = -1;
 }
 
 const char* lyap_last_error(const lyap_ctx* c) { return c ? c->err.c_str() : g_last_error.c_str(); }
@@ -817,6 +1027,11 @@ static void destroy_impl(lyap_ctx* c) {
     if (c->xjoin[gi]) cudaEventDestroy(c->xjoin[gi]);
   }
   dfree(c->Spad);
+  for (double* q : {c->coarse.Z, c->coarse.TZ, c->coarse.Phi, c->coarse.Psi}) dfree(q);
+  for (int gi = 0; gi < 4; ++gi) {
+    if (c->cublas_eng[gi]) cublasDestroy(c->cublas_eng[gi]);
+    dfree(c->cublas_ws[gi]);
+  }
   dfree(c->stab.wgrid);
   dfree(c->stab.Gf);
   dfree(c->stab.Mm);

@@ -403,6 +403,36 @@ __global__ void k_pad_basis(const double* __restrict__ S, int64_t n, int64_t np,
   Srow[r * np + c] = in ? S[c * n + r] : 0.0;  // S_r[r][c]
 }
 
+// Coarse-space build helpers: unit vectors e_{c0 + j} (j < nb) as nb x L rows
+__global__ void k_unit_vectors(double* __restrict__ X, int64_t c0, int64_t nb, int64_t L) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nb * L; i += (int64_t)gridDim.x * blockDim.x)
+    X[i] = (i % L == c0 + i / L) ? 1.0 : 0.0;
+}
+// Tm[:, c0 + j] = -Y[j] (apply_C with sigma = 0 returns -T e)
+__global__ void k_neg_copy(const double* __restrict__ Y, double* __restrict__ Tcol, int64_t cnt) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
+    Tcol[i] = -Y[i];
+}
+// T_o' = T - (the pair blocks Pb): column-major L x L explicit folded T, one thread per rep
+template <int K>
+__global__ void k_sub_pblocks(double* __restrict__ Tm, int64_t L, int64_t npad, const double* __restrict__ Pb,
+                              int64_t npairs, int64_t nrep) {
+  const int64_t rep = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (rep >= nrep) return;
+  const bool pair = rep < npairs;
+  const int64_t c = pair ? 2 * rep : rep + npairs;
+  const int w = pair ? 2 : 1;
+  const double* pb = Pb + rep * 4 * K * K;
+  for (int t = 0; t < K; ++t)
+    for (int a = 0; a < w; ++a)
+      for (int u = 0; u < K; ++u)
+        for (int b = 0; b < w; ++b) {
+          const int64_t row = t * npad + c + a, col = u * npad + c + b;
+          const int pr = pair ? 2 * t + a : t, pcol = pair ? 2 * u + b : u;
+          Tm[col * L + row] -= pb[pr * 2 * K + pcol];
+        }
+}
+
 // deterministic sum of t0 partials (one block)
 __global__ void k_sum(const double* __restrict__ x, int64_t n, double* out) {
   __shared__ double red[32];
