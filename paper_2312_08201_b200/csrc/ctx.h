@@ -80,7 +80,7 @@ struct Engine {
   double *Hraw = nullptr;                         // b x (mmax+1) x mmax unrotated Hessenberg (recycle build)
   int *phase = nullptr, *m = nullptr, *vidx = nullptr, *applies = nullptr, *restarts = nullptr;
   // two-level preconditioner (coarse p > 0): flexible basis Zb = P^{-1} q_j, coarse scratch
-  double *Zb = nullptr, *Rbuf = nullptr, *Yz = nullptr, *TYz = nullptr, *Cc = nullptr, *Wc = nullptr, *Einv = nullptr;
+  double *Zb = nullptr, *Rbuf = nullptr, *Yz = nullptr, *Cc = nullptr, *Wc = nullptr, *Einv = nullptr;
   int pc = 0;                                     // coarse size the buffers were made for
   int* ctrl = nullptr;                            // per group 8 ints: [2]=active slots, [4..5]=applied vectors;
                                                   // then 8 shared: [0]=next queue position, [1]=done count
@@ -102,7 +102,7 @@ struct Engine {
 // Coarse space of the two-level preconditioner, built on first use.
 struct CoarseSpace {
   int p = 0;                       // size (0: off)
-  double *Z = nullptr, *TZ = nullptr;     // L x p column-major: the space and T Z
+  double *Z = nullptr, *TZ = nullptr;     // [Z; T Z]: 2L x p column-major (TZ = Z + L, leading dim 2L)
   double *Phi = nullptr, *Psi = nullptr;  // k x p x p column-major: Z_t^T Z_t, Z_t^T (T Z)_t
   double build_ms = 0.0;
 };

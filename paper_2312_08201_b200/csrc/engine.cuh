@@ -59,8 +59,8 @@ struct EngArgs {
   // two-level preconditioner (pc > 0): coarse space Z (L x pc), T Z, Gram blocks
   // Phi_t / Psi_t (k x pc x pc); per slot E(v)^{-1} (pc x pc), flexible basis Zb (as Qb), scratch
   int pc;
-  const double *Zc, *TZc, *Phi, *Psi;
-  double *Einv, *Zb, *Rbuf, *Yz, *TYz, *Cc, *Wc;
+  const double *Zc, *Phi, *Psi;  // Zc: [Z; T Z] interleaved, 2L x pc column-major
+  double *Einv, *Zb, *Rbuf, *Yz, *Cc, *Wc;  // Yz: per slot [Z w; T Z w] (2L)
   int32_t* status;
   int32_t* out_applies;
   double* out_resid;
@@ -358,11 +358,11 @@ __global__ void __launch_bounds__(128) k_prec(EngArgs a) {
   double r[2 * K], z[2 * K];
   rep_load<K>(q, a.npad, c, pair, sc, r);
   if (a.pc > 0) {
-    // two-level: z = y + M^{-1} (r - C(v) y), y = Z E^{-1} Z^T r (Yz), T y (TYz) from the coarse GEMMs;
+    // two-level: z = y + M^{-1} (r - C(v) y), y = Z E^{-1} Z^T r and T y (Yz = [Z w; T Z w]) from the coarse GEMMs;
     // C(v) y = sigma o y - T y on unmasked rows, y on masked ones
     double y[2 * K], ty[2 * K];
-    rep_load<K>(a.Yz + (int64_t)slot * a.L, a.npad, c, pair, 1.0, y);
-    rep_load<K>(a.TYz + (int64_t)slot * a.L, a.npad, c, pair, 1.0, ty);
+    rep_load<K>(a.Yz + (int64_t)slot * 2 * a.L, a.npad, c, pair, 1.0, y);       // Z w
+    rep_load<K>(a.Yz + (int64_t)slot * 2 * a.L + a.L, a.npad, c, pair, 1.0, ty);  // T Z w
 #pragma unroll
     for (int t = 0; t < K; ++t) {
       const double msk = a.mask[slot * K + t], sg = a.sigma[slot * K + t];

@@ -133,7 +133,7 @@ void upload_seeds(lyap_ctx* ctx) {
 void free_engine(Engine& g, bool keep_order = true) {
   void* ps[] = {g.Bop, g.U, g.Xin, g.X, g.Qb, g.Minv, g.sigma, g.mask, g.eta, g.H, g.e, g.y,
                 g.bnorm, g.part, g.part3, g.phase, g.m, g.vidx, g.applies, g.restarts, g.ctrl,
-                g.part2, g.Gq, g.cf, g.Hraw, g.rhs, g.t0s, g.Zb, g.Rbuf, g.Yz, g.TYz, g.Cc, g.Wc, g.Einv};
+                g.part2, g.Gq, g.cf, g.Hraw, g.rhs, g.t0s, g.Zb, g.Rbuf, g.Yz, g.Cc, g.Wc, g.Einv};
   for (void* p : ps) dfree(p);
   if (g.h_ctrl) cudaFreeHost(g.h_ctrl);
   int* order = g.order;
@@ -256,8 +256,7 @@ void ensure_engine(lyap_ctx* ctx, int b, int mmax) {
   if (pc > 0) {  // two-level preconditioner: flexible basis and coarse scratch
     g.Zb = dalloc<double>(ctx, (size_t)b * (mmax + 1) * g.L, false);
     g.Rbuf = dalloc<double>(ctx, (size_t)b * g.L);
-    g.Yz = dalloc<double>(ctx, (size_t)b * g.L);
-    g.TYz = dalloc<double>(ctx, (size_t)b * g.L);
+    g.Yz = dalloc<double>(ctx, (size_t)b * 2 * g.L);  // per slot [Z w; T Z w]
     g.Cc = dalloc<double>(ctx, (size_t)b * pc);
     g.Wc = dalloc<double>(ctx, (size_t)b * pc);
     g.Einv = dalloc<double>(ctx, (size_t)b * pc * pc);
@@ -398,7 +397,6 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   a.t0s = s.qlin ? g.t0s : nullptr;
   a.pc = two_level ? g.pc : 0;
   a.Zc = ctx->coarse.Z;
-  a.TZc = ctx->coarse.TZ;
   a.Phi = ctx->coarse.Phi;
   a.Psi = ctx->coarse.Psi;
   a.max_restarts = ctx->opts.max_restarts;
@@ -469,8 +467,7 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
     if (x.pc > 0) {
       x.Zb = g.Zb + s0 * ld * g.L;
       x.Rbuf = g.Rbuf + s0 * g.L;
-      x.Yz = g.Yz + s0 * g.L;
-      x.TYz = g.TYz + s0 * g.L;
+      x.Yz = g.Yz + s0 * 2 * g.L;
       x.Cc = g.Cc + s0 * x.pc;
       x.Wc = g.Wc + s0 * x.pc;
       x.Einv = g.Einv + s0 * (int64_t)x.pc * x.pc;
@@ -546,11 +543,10 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
       LAUNCHED();
       k_cpre<<<dim3((unsigned)std::min<int64_t>((g.L + 255) / 256, 64), (unsigned)bg), 256, 0, sg>>>(x);
       LAUNCHED();
-      CKB(cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, p, bg, Li, &one, x.Zc, Li, x.Rbuf, Li, &zero, x.Cc, p));
+      CKB(cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, p, bg, Li, &one, x.Zc, 2 * Li, x.Rbuf, Li, &zero, x.Cc, p));
       k_cw<<<bg, 128, 0, sg>>>(x);
       LAUNCHED();
-      CKB(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, Li, bg, p, &one, x.Zc, Li, x.Wc, p, &zero, x.Yz, Li));
-      CKB(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, Li, bg, p, &one, x.TZc, Li, x.Wc, p, &zero, x.TYz, Li));
+      CKB(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, 2 * Li, bg, p, &one, x.Zc, 2 * Li, x.Wc, p, &zero, x.Yz, 2 * Li));
     }
     K_DISPATCH(s.k, (k_prec<KK><<<grep, 128, 0, sg>>>(x)));
     LAUNCHED();
@@ -875,7 +871,7 @@ void ensure_coarse(lyap_ctx* ctx) {
          *U = nullptr, *work = nullptr, *rwork = nullptr;
   int* dinfo = nullptr;
   try {
-    for (double* q : {C.Z, C.TZ, C.Phi, C.Psi}) dfree(q);
+    for (double* q : {C.Z, C.Phi, C.Psi}) dfree(q);  // TZ lives inside Z
     C = CoarseSpace{};
     // 1. explicit folded T, column-major L x L
     Tm = dalloc<double>(ctx, (size_t)L * L, false);
@@ -940,25 +936,34 @@ void ensure_coarse(lyap_ctx* ctx) {
     }
     dfree(Tm);
     Tm = nullptr;
-    // 4. Z = the first p columns; T Z through K1
-    C.Z = dalloc<double>(ctx, (size_t)L * p, false);
-    CK(cudaMemcpyAsync(C.Z, U, (size_t)L * p * 8, cudaMemcpyDeviceToDevice, st));
-    C.TZ = dalloc<double>(ctx, (size_t)L * p, false);
+    // 4. Z = the first p columns; T Z through K1.  Stored interleaved as one 2L x p column-major
+    //    matrix [Z; T Z] (column i = [z_i; T z_i]): the engine forms Z w and T Z w with ONE GEMM
+    double* TZt = dalloc<double>(ctx, (size_t)L * p, false);
     {
-      const int rc = lyap_apply_C(ctx, p, C.Z, nullptr, C.TZ, st);
-      if (rc != LYAP_OK) throw Fail{rc};
-      k_negate<<<(unsigned)std::min<int64_t>((L * p + 255) / 256, 65535), 256, 0, st>>>(C.TZ, L * p);
+      const int rc = lyap_apply_C(ctx, p, U, nullptr, TZt, st);
+      if (rc != LYAP_OK) {
+        dfree(TZt);
+        throw Fail{rc};
+      }
+      k_negate<<<(unsigned)std::min<int64_t>((L * p + 255) / 256, 65535), 256, 0, st>>>(TZt, L * p);
       LAUNCHED();
     }
+    C.Z = dalloc<double>(ctx, (size_t)2 * L * p, false);
+    C.TZ = C.Z + L;  // rows L..2L of every column (leading dimension 2L)
+    CK(cudaMemcpy2DAsync(C.Z, 2 * L * 8, U, L * 8, L * 8, p, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpy2DAsync(C.Z + L, 2 * L * 8, TZt, L * 8, L * 8, p, cudaMemcpyDeviceToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    dfree(TZt);
     // 5. Gram blocks per parameter t (row block t of Z / T Z)
     C.Phi = dalloc<double>(ctx, (size_t)k * p * p, false);
     C.Psi = dalloc<double>(ctx, (size_t)k * p * p, false);
     const int np = (int)s.npad;
+    const int ld2 = 2 * Li;
     for (int64_t t = 0; t < k; ++t) {
-      CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_T, CUBLAS_OP_N, p, p, np, &one, C.Z + t * np, Li, C.Z + t * np, Li, &zero,
+      CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_T, CUBLAS_OP_N, p, p, np, &one, C.Z + t * np, ld2, C.Z + t * np, ld2, &zero,
                       C.Phi + t * p * p, p));
-      CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_T, CUBLAS_OP_N, p, p, np, &one, C.Z + t * np, Li, C.TZ + t * np, Li, &zero,
-                      C.Psi + t * p * p, p));
+      CKB(cublasDgemm(ctx->cublas, CUBLAS_OP_T, CUBLAS_OP_N, p, p, np, &one, C.Z + t * np, ld2, C.TZ + t * np, ld2,
+                      &zero, C.Psi + t * p * p, p));
     }
     C.p = p;
     CK(cudaEventRecord(e1, st));
@@ -1030,7 +1035,7 @@ static void destroy_impl(lyap_ctx* c) {
     if (c->xjoin[gi]) cudaEventDestroy(c->xjoin[gi]);
   }
   dfree(c->Spad);
-  for (double* q : {c->coarse.Z, c->coarse.TZ, c->coarse.Phi, c->coarse.Psi}) dfree(q);
+  for (double* q : {c->coarse.Z, c->coarse.Phi, c->coarse.Psi}) dfree(q);  // TZ lives inside Z
   for (int gi = 0; gi < 4; ++gi) {
     if (c->cublas_eng[gi]) cublasDestroy(c->cublas_eng[gi]);
     dfree(c->cublas_ws[gi]);
