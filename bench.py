@@ -358,6 +358,8 @@ def main():
                                                      "recycle_build_ms": recycle_ms,
                                                      "applies_per_v": st["k1_vectors"] / (len(idx) * args.steps),
                                                      "shard_cost_max_over_mean": balance,
+                                                     "coarse": P.info["coarse"],
+                                                     "coarse_build_ms": P.info["coarse_build_ms"],
                                                      "emulated_rank": args.emulate_rank or None}),
               "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
               "gpu_launches": st["kernel_launches"]})

@@ -97,6 +97,8 @@ typedef struct {
   int32_t batch, max_dim;
   double wcost[LYAP_KMAX]; /* ||B~l_t|| ||B^r_t||: weights of the scheduling cost proxy
                               sum_t |v_t| wcost[t] (opts.schedule; multi-GPU shard balancing) */
+  int32_t coarse;          /* size of the two-level preconditioner's coarse space once built (0: none) */
+  double coarse_build_ms;  /* device time of its build (explicit T, randomized SVD, T Z, Gram blocks) */
 } lyap_info;
 
 typedef struct {

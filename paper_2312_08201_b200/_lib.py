@@ -35,7 +35,8 @@ class Info(C.Structure):
     _fields_ = [("n", C.c_int64), ("k", C.c_int64), ("npad", C.c_int64), ("n_pairs", C.c_int64),
                 ("t0", C.c_double), ("cond_S", C.c_double), ("min_lam_sum", C.c_double),
                 ("max_abs_lam", C.c_double), ("setup_ms", C.c_double), ("batch", C.c_int32),
-                ("max_dim", C.c_int32), ("wcost", C.c_double * LYAP_KMAX)]
+                ("max_dim", C.c_int32), ("wcost", C.c_double * LYAP_KMAX), ("coarse", C.c_int32),
+                ("coarse_build_ms", C.c_double)]
 
 
 class Stats(C.Structure):

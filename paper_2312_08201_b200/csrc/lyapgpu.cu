@@ -974,6 +974,8 @@ void ensure_coarse(lyap_ctx* ctx) {
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, e0, e1));
     C.build_ms = ms;
+    ctx->info.coarse = p;
+    ctx->info.coarse_build_ms = ms;
   } catch (Fail f) {
     for (void* q : {(void*)Tm, (void*)X, (void*)Y, (void*)Om, (void*)Ys, (void*)Sv, (void*)U, (void*)work,
                     (void*)rwork, (void*)dinfo})
@@ -1410,6 +1412,8 @@ int lyap_setup_like(const lyap_ctx* base, int64_t k, const double* Bl, const dou
     LAUNCHED();
     ctx->info = base->info;
     ctx->info.k = k;
+    ctx->info.coarse = 0;  // this configuration builds its own coarse space on first use
+    ctx->info.coarse_build_ms = 0.0;
     build_config(ctx, Blc, Brc);
     CK(cudaEventRecord(ctx->ev1, st));
     CK(cudaEventSynchronize(ctx->ev1));
