@@ -385,87 +385,95 @@ __global__ void __launch_bounds__(128) k_prec(EngArgs a) {
 }
 
 // ---------------------------------------------------------------- two-level preconditioner
-// k_cfactor (one WARP per slot with a new v, `warps` slots per CTA): E(v) = sum_t (v_t != 0 ?
-// sigma_t Phi_t - Psi_t : Phi_t) (= Z^T C(v) Z, the Galerkin coarse matrix) and its inverse by in-place
-// Gauss-Jordan with partial pivoting in the warp's shared-memory tile (warp-synchronous: no block
-// barriers); Einv[slot] (pc x pc, column-major).
-__global__ void __launch_bounds__(128) k_cfactor(EngArgs a, int warps) {
-  extern __shared__ double Esm[];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int slot = blockIdx.x * warps + w;
-  if (w >= warps || slot >= a.b || !a.newv[slot]) return;
-  const int p = a.pc, pp = p * p;
-  double* E = Esm + (size_t)w * (pp + p);  // p x p column-major, then the pivot record (as ints)
-  int* perm = reinterpret_cast<int*>(E + pp);
-  double sg[LYAP_KMAX], mk_[LYAP_KMAX];
-  for (int t = 0; t < a.K; ++t) {
-    sg[t] = a.sigma[slot * a.K + t];
-    mk_[t] = a.mask[slot * a.K + t];
-  }
-  for (int e = lane; e < pp; e += 32) {
+// k_cfactor (one CTA per slot with a new v): E(v) = sum_t (v_t != 0 ? sigma_t Phi_t - Psi_t : Phi_t)
+// (= Z^T C(v) Z, the Galerkin coarse matrix) and its inverse by Gauss-Jordan with partial pivoting in
+// shared memory; Einv[slot] (pc x pc, column-major).
+__global__ void __launch_bounds__(256) k_cfactor(EngArgs a, int) {
+  extern __shared__ double E[];  // pc x pc column-major, then pc (pivot scratch)
+  const int slot = blockIdx.x;
+  if (!a.newv[slot]) return;
+  const int p = a.pc, tid = threadIdx.x, nt = blockDim.x;
+  const int64_t pp = (int64_t)p * p;
+  for (int64_t e = tid; e < pp; e += nt) {
     double v = 0.0;
     for (int t = 0; t < a.K; ++t) {
-      const double phi = a.Phi[(int64_t)t * pp + e];
-      v += mk_[t] != 0.0 ? sg[t] * phi - a.Psi[(int64_t)t * pp + e] : phi;
+      const double phi = a.Phi[t * pp + e];
+      v += a.mask[slot * a.K + t] != 0.0 ? a.sigma[slot * a.K + t] * phi - a.Psi[t * pp + e] : phi;
     }
     E[e] = v;
   }
-  __syncwarp();
+  __shared__ int piv_s;
+  __shared__ double pinv_s;
+  int* perm = reinterpret_cast<int*>(E + pp);
+  __syncthreads();
   for (int c = 0; c < p; ++c) {
-    double best = -1.0;
-    int arg = c;
-    for (int r = c + lane; r < p; r += 32) {
-      const double v = fabs(E[c * p + r]);
-      if (v > best) {
-        best = v;
-        arg = r;
+    if (tid < 32) {  // pivot: largest |E(r, c)|, r >= c (first on ties)
+      double best = -1.0;
+      int arg = c;
+      for (int r = c + tid; r < p; r += 32) {
+        const double v = fabs(E[(int64_t)c * p + r]);
+        if (v > best) {
+          best = v;
+          arg = r;
+        }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_down_sync(0xffffffffu, best, o);
+        const int oa = __shfl_down_sync(0xffffffffu, arg, o);
+        if (ob > best || (ob == best && oa < arg)) {
+          best = ob;
+          arg = oa;
+        }
+      }
+      if (tid == 0) {
+        piv_s = arg;
+        perm[c] = arg;
       }
     }
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
-      if (ob > best || (ob == best && oa < arg)) {
-        best = ob;
-        arg = oa;
+    __syncthreads();
+    const int pr = piv_s;
+    if (pr != c)
+      for (int j = tid; j < p; j += nt) {
+        const double t = E[(int64_t)j * p + c];
+        E[(int64_t)j * p + c] = E[(int64_t)j * p + pr];
+        E[(int64_t)j * p + pr] = t;
       }
+    __syncthreads();
+    if (tid == 0) {
+      const double pv = E[(int64_t)c * p + c];
+      pinv_s = pv != 0.0 ? 1.0 / pv : 0.0;
+      E[(int64_t)c * p + c] = 1.0;
     }
-    if (lane == 0) perm[c] = arg;
-    if (arg != c)
-      for (int j = lane; j < p; j += 32) {
-        const double t = E[j * p + c];
-        E[j * p + c] = E[j * p + arg];
-        E[j * p + arg] = t;
-      }
-    __syncwarp();
-    const double pv = E[c * p + c];
-    const double inv = pv != 0.0 ? 1.0 / pv : 0.0;
-    __syncwarp();
-    for (int j = lane; j < p; j += 32) E[j * p + c] = (j == c ? 1.0 : E[j * p + c]) * inv;  // row c scaled
-    __syncwarp();
-    // eliminate: E(r, j) -= E(r, c) E(c, j) for r, j != c, then column c = -E(r, c) / pivot
-    for (int j = 0; j < p; ++j) {
+    __syncthreads();
+    const double inv = pinv_s;
+    for (int j = tid; j < p; j += nt) E[(int64_t)j * p + c] *= inv;  // row c
+    __syncthreads();
+    // eliminate column c from every other row: E(r, j) -= E(r, c) E(c, j); the column-c factors
+    // are read before any thread overwrites them (E(r, c) is set to 0 -> the identity column)
+    for (int j = tid / 32; j < p; j += nt / 32) {  // warp per column, lanes over rows: coalesced
       if (j == c) continue;
       const double ecj = E[j * p + c];
-      for (int r = lane; r < p; r += 32)
+      for (int r = tid & 31; r < p; r += 32)
         if (r != c) E[j * p + r] = fma(-E[c * p + r], ecj, E[j * p + r]);
     }
-    __syncwarp();
-    for (int r = lane; r < p; r += 32)
-      if (r != c) E[c * p + r] = -E[c * p + r] * E[c * p + c];
-    __syncwarp();
+    __syncthreads();
+    for (int r = tid; r < p; r += nt)
+      if (r != c) E[(int64_t)c * p + r] = -E[(int64_t)c * p + r] * E[(int64_t)c * p + c];
+    __syncthreads();
   }
-  for (int c = p - 1; c >= 0; --c) {  // undo the row swaps as column swaps of the inverse
+  // undo the row swaps as column swaps of the inverse, in reverse order
+  for (int c = p - 1; c >= 0; --c) {
     const int pr = perm[c];
     if (pr != c)
-      for (int r = lane; r < p; r += 32) {
-        const double t = E[c * p + r];
-        E[c * p + r] = E[pr * p + r];
-        E[pr * p + r] = t;
+      for (int r = tid; r < p; r += nt) {
+        const double t = E[(int64_t)c * p + r];
+        E[(int64_t)c * p + r] = E[(int64_t)pr * p + r];
+        E[(int64_t)pr * p + r] = t;
       }
-    __syncwarp();
+    __syncthreads();
   }
   double* out = a.Einv + (int64_t)slot * pp;
-  for (int e = lane; e < pp; e += 32) out[e] = E[e];
+  for (int64_t e = tid; e < pp; e += nt) out[e] = E[e];
 }
 
 // k_cpre: Rbuf[slot] = q^_m / eta_m for a slot whose next K1 input is a Krylov direction, else 0

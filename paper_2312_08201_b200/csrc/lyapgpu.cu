@@ -493,10 +493,7 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   }
 
   const size_t upd_smem = sizeof(double) * (mmax + 1);
-  // k_cfactor: one warp per slot, up to 4 warps (slots) per CTA within ~100 KB of shared memory
-  const size_t cf_tile = sizeof(double) * ((size_t)a.pc * a.pc + a.pc);
-  const int cf_warps = a.pc > 0 ? (int)std::max<size_t>(1, std::min<size_t>(4, (100u << 10) / cf_tile)) : 1;
-  const size_t cf_smem = cf_tile * cf_warps;
+  const size_t cf_smem = sizeof(double) * (size_t)a.pc * a.pc + sizeof(int) * (size_t)a.pc + 16;
   if (a.pc > 0) {
     CK(cudaFuncSetAttribute(k_cfactor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cf_smem));
     for (int gi = 0; gi < G; ++gi)
@@ -542,7 +539,7 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
       const double one = 1.0, zero = 0.0;
       cublasHandle_t hb = ctx->cublas_eng[gi];
       CKB(cublasSetStream(hb, sg));
-      k_cfactor<<<(unsigned)((bg + cf_warps - 1) / cf_warps), 32 * cf_warps, cf_smem, sg>>>(x, cf_warps);
+      k_cfactor<<<bg, 256, cf_smem, sg>>>(x, 0);
       LAUNCHED();
       k_cpre<<<dim3((unsigned)std::min<int64_t>((g.L + 255) / 256, 64), (unsigned)bg), 256, 0, sg>>>(x);
       LAUNCHED();
