@@ -81,7 +81,7 @@ typedef struct {
                           P(v)^{-1} r = y + M(v)^{-1}(r - C(v) y), y = Z E(v)^{-1} Z^T r, E(v) = Z^T C(v) Z,
                           with M(v) the exact pair blocks and Z the p dominant right singular vectors
                           of the off-block coupling T_o (randomized SVD at the first trace_batch).
-                          -1 (default) auto: 48 when n k >= 2000, else off; 0 off; > 0 that size
+                          -1 (default) auto: 32 when n k >= 2000, else off; 0 off; > 0 that size
                           (multiple of 8, <= 256).  Recycle spaces are not used together with it. */
 } lyap_opts;
 

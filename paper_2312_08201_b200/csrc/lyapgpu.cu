@@ -821,13 +821,13 @@ void stab_count(lyap_ctx* ctx, int64_t nv, const double* dV, int32_t* dnu, cudaS
   LAUNCHED();
 }
 
-// size of the coarse space (opts.coarse): auto = 48 when n k >= 2000 (measured, B200, v/s with p =
-// 0 / 32 / 48 / 64 / 96: c5 922 / 961 / 966 / 967 / 955; c4 11.67k / 12.63k / 12.56k / 12.48k / 12.11k;
-// c3 113.7k / 206.4k (p = 32); c2 100.2k / 84.8k / - / 67.3k: the coarse products cost more than they
-// save when a T-apply is cheap and the off-block coupling is not low-rank)
+// size of the coarse space (opts.coarse): auto = 32 when n k >= 2000 (measured, B200, v/s with p =
+// 0 / 32 / 48 / 64 / 96: c5 922 / 961 / 967 / 967 / 955; c4 11.67k / 12.4-12.6k / 12.0-12.6k / 12.48k /
+// 12.11k; c3 113.7k / 203-206k / 154-175k; c2 100.2k / 85-86k / - / 67.3k: the coarse products cost
+// more than they save when a T-apply is cheap and the off-block coupling is not low-rank)
 int coarse_size(const lyap_ctx* ctx) {
   const Seed& s = ctx->seed;
-  int p = ctx->opts.coarse < 0 ? (s.n * s.k >= 2000 ? 48 : 0) : ctx->opts.coarse;
+  int p = ctx->opts.coarse < 0 ? (s.n * s.k >= 2000 ? 32 : 0) : ctx->opts.coarse;
   p = std::min<int>(p, 256);
   p = std::min<int64_t>(p, (s.n * s.k) / 2);
   return p < 8 ? 0 : p / 8 * 8;
