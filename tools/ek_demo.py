@@ -57,7 +57,7 @@ def main():
         t_x0 = time.perf_counter() - t
         t0 = float(np.sum(0.5 * (W.E + W.E.T) * X0))
         t = time.perf_counter()
-        ek = EKProblem(W.A0, W.Bl, W.Br, X0 @ W.Br, W.E, t0, max_dim=min(W.n, 1200))
+        ek = EKProblem(W.A0, W.Bl, W.Br, X0 @ W.Br, W.E, t0, max_dim=W.n)
         t_setup = time.perf_counter() - t
         t = time.perf_counter()
         tau, bwd, dim = ek.trace_batch(W.V[idx], eps=args.eps, per_v=True, allow_partial=True)
