@@ -476,6 +476,82 @@ __global__ void __launch_bounds__(256) k_cfactor(EngArgs a, int) {
   for (int64_t e = tid; e < pp; e += nt) out[e] = E[e];
 }
 
+// k_cfactor32 (coarse size p <= 32): one WARP per slot with a new v, E(v) held in registers -- lane j
+// owns column j (padded with the identity up to 32) -- and inverted by Gauss-Jordan with partial
+// pivoting using shuffles only (no shared memory, no barriers).  Same result as k_cfactor.
+__global__ void __launch_bounds__(128) k_cfactor32(EngArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int slot = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (slot >= a.b || !a.newv[slot]) return;
+  const int p = a.pc, pp = p * p;
+  double col[32];
+#pragma unroll
+  for (int r = 0; r < 32; ++r) {
+    double v = (r == lane) ? 1.0 : 0.0;
+    if (lane < p && r < p) {
+      v = 0.0;
+      for (int t = 0; t < a.K; ++t) {
+        const double phi = a.Phi[(int64_t)t * pp + lane * p + r];
+        v += a.mask[slot * a.K + t] != 0.0 ? a.sigma[slot * a.K + t] * phi - a.Psi[(int64_t)t * pp + lane * p + r] : phi;
+      }
+    }
+    col[r] = v;
+  }
+  int perm[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) {
+    int pr = c;
+    if (lane == c) {  // pivot: largest |E(r, c)|, r >= c (first on ties)
+      double best = -1.0;
+#pragma unroll
+      for (int r = c; r < 32; ++r)
+        if (fabs(col[r]) > best) {
+          best = fabs(col[r]);
+          pr = r;
+        }
+    }
+    pr = __shfl_sync(0xffffffffu, pr, c);
+    perm[c] = pr;
+    double vpr = 0.0;  // swap rows c and pr in every column
+#pragma unroll
+    for (int r = c; r < 32; ++r) vpr = (r == pr) ? col[r] : vpr;
+#pragma unroll
+    for (int r = c + 1; r < 32; ++r) col[r] = (r == pr) ? col[c] : col[r];
+    col[c] = vpr;
+    const double piv = __shfl_sync(0xffffffffu, col[c], c);
+    const double inv = piv != 0.0 ? 1.0 / piv : 0.0;
+    if (lane == c) col[c] = 1.0;
+    col[c] *= inv;  // row c scaled (E(c, c) = 1 / pivot in lane c)
+    const double ecj = col[c];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      if (r == c) continue;
+      const double erc = __shfl_sync(0xffffffffu, col[r], c);  // E(r, c) before the update
+      if (lane != c) col[r] = fma(-erc, ecj, col[r]);
+    }
+    if (lane == c) {
+#pragma unroll
+      for (int r = 0; r < 32; ++r)
+        if (r != c) col[r] = -col[r] * col[c];
+    }
+  }
+#pragma unroll
+  for (int c = 31; c >= 0; --c) {  // undo the row swaps as column swaps (lanes c <-> perm[c])
+    const int pr = perm[c];
+    if (pr != c) {
+      const int partner = lane == c ? pr : (lane == pr ? c : lane);
+#pragma unroll
+      for (int r = 0; r < 32; ++r) col[r] = __shfl_sync(0xffffffffu, col[r], partner);
+    }
+  }
+  if (lane < p) {
+    double* out = a.Einv + (int64_t)slot * pp + (int64_t)lane * p;
+#pragma unroll
+    for (int r = 0; r < 32; ++r)
+      if (r < p) out[r] = col[r];
+  }
+}
+
 // k_cpre: Rbuf[slot] = q^_m / eta_m for a slot whose next K1 input is a Krylov direction, else 0
 __global__ void __launch_bounds__(256) k_cpre(EngArgs a) {
   const int slot = blockIdx.y;

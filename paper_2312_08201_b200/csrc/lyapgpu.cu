@@ -539,7 +539,10 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
       const double one = 1.0, zero = 0.0;
       cublasHandle_t hb = ctx->cublas_eng[gi];
       CKB(cublasSetStream(hb, sg));
-      k_cfactor<<<bg, 256, cf_smem, sg>>>(x, 0);
+      if (p <= 32)
+        k_cfactor32<<<(unsigned)((bg + 3) / 4), 128, 0, sg>>>(x);
+      else
+        k_cfactor<<<bg, 256, cf_smem, sg>>>(x, 0);
       LAUNCHED();
       k_cpre<<<dim3((unsigned)std::min<int64_t>((g.L + 255) / 256, 64), (unsigned)bg), 256, 0, sg>>>(x);
       LAUNCHED();
