@@ -177,29 +177,52 @@ def config_dict(W, args, world, extra=None):
 
 # ------------------------------------------------------------------------------ reference arm
 def run_reference(args, rank, world):
+    """The reference arm: the CPU oracle (the paper's naive per-v Bartels-Stewart baseline) as it stands,
+    on the host cores, one single-threaded worker per core; every step is a bounded seeded sample of the
+    configuration's grid (at least one v per core, about args.cpu_seconds of work)."""
     if rank != 0:
         return
+    import multiprocessing as mp
+
     import workloads
     W = workloads.make(args.config)
-    per_step = max(2.0, min(args.cpu_seconds, 20.0))
-    for _ in range(args.warmup):
-        oracle_rate(args.config, per_step / 4, seed=1)
-    rates = []
-    t_all = time.perf_counter()
-    for s in range(args.steps):
-        r, cores, cnt, el = oracle_rate(args.config, per_step, seed=2 + s)
-        rates.append((r, cores, cnt, el))
-    wall = time.perf_counter() - t_all
-    value = statistics.median([r[0] for r in rates])
-    cores, cnt = rates[0][1], rates[0][2]
+    cores = os.cpu_count() or 1
+    saved = {v: os.environ.get(v) for v in _THREAD_VARS}
+    for v in _THREAD_VARS:
+        os.environ[v] = "1"
+    ctx = mp.get_context("spawn")
+    rates, counts = [], []
+    with ctx.Pool(cores, initializer=_oracle_worker_init, initargs=(args.config,)) as pool:
+        corner = W.corner_indices()
+        t = time.perf_counter()
+        pool.map(_oracle_one, [corner[-1]] * cores)  # sizes the per-step sample (one round)
+        t1 = time.perf_counter() - t
+        per_step = max(cores, min(W.nv, cores * max(1, int(args.cpu_seconds / max(t1, 1e-3)))))
+        for s_ in range(args.warmup):
+            pool.map(_oracle_one, [int(i) for i in W.sample_indices(cores, seed=100 + s_)], chunksize=1)
+        t_all = time.perf_counter()
+        for s_ in range(args.steps):
+            idx = W.sample_indices(per_step, seed=2 + s_)
+            t = time.perf_counter()
+            pool.map(_oracle_one, [int(i) for i in idx], chunksize=1)
+            rates.append(len(idx) / (time.perf_counter() - t))
+            counts.append(len(idx))
+        wall = time.perf_counter() - t_all
+    for v, val in saved.items():
+        if val is None:
+            os.environ.pop(v, None)
+        else:
+            os.environ[v] = val
+    value = statistics.median(rates)
     emit({"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / max(args.steps, 1),
           "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
           "data": "synthetic (seeded workloads.make)",
-          "config": config_dict(W, args, world, {"sample_per_step": cnt}),
+          "config": config_dict(W, args, world, {"sample_per_step": counts[0] if counts else 0}),
           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                           "sample": f"{cnt} grid points per step (2^k corners + centre + seeded uniform), "
-                                     "blocked Bartels-Stewart per v, one process per core, 1 BLAS thread"},
+                           "sample": f"{counts[0] if counts else 0} grid points per step (2^k corners + centre + "
+                                     "seeded uniform), blocked Bartels-Stewart per v, one process per core, "
+                                     "1 BLAS thread"},
           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
 
 
