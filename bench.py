@@ -54,6 +54,7 @@ def parse():
                     help="R/N: on this single process, solve only rank R's shard of an N-way strong split "
                          "(per-rank time of an N-GPU run, measured on one GPU)")
     ap.add_argument("--max-dim", type=int, default=0)
+    ap.add_argument("--no-profile", action="store_true", help="no per-launch K1 events (diagnostics)")
     ap.add_argument("--coarse", type=int, default=int(os.environ.get("BENCH_COARSE", "-1")),
                     help="two-level preconditioner coarse-space size (-1 auto, 0 off)")
     ap.add_argument("--recycle", type=int, default=int(os.environ.get("BENCH_RECYCLE", "0")),
@@ -247,7 +248,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     W = workloads.make(args.config)
-    P = Problem(W.A0, W.Bl, W.Br, W.Q, W.E, profile=True, device=local, batch=args.batch, max_dim=args.max_dim,
+    P = Problem(W.A0, W.Bl, W.Br, W.Q, W.E, profile=not args.no_profile, device=local, batch=args.batch, max_dim=args.max_dim,
                 coarse=args.coarse)
     cost = P.cost_proxy(W.V)  # the engine's scheduling proxy: balances the strong-scaling shards
     emu = None

@@ -480,23 +480,33 @@ __global__ void __launch_bounds__(256) k_cfactor(EngArgs a, int) {
 // owns column j (padded with the identity up to 32) -- and inverted by Gauss-Jordan with partial
 // pivoting using shuffles only (no shared memory, no barriers).  Same result as k_cfactor.
 __global__ void __launch_bounds__(128) k_cfactor32(EngArgs a) {
-  const int lane = threadIdx.x & 31;
-  const int slot = blockIdx.x * 4 + (threadIdx.x >> 5);
+  __shared__ double Es[4][32 * 33];  // per warp: the 32 x 32 tile, column stride 33 (no bank conflicts)
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int slot = blockIdx.x * 4 + w;
   if (slot >= a.b || !a.newv[slot]) return;
   const int p = a.pc, pp = p * p;
-  double col[32];
-#pragma unroll
-  for (int r = 0; r < 32; ++r) {
-    double v = (r == lane) ? 1.0 : 0.0;
-    if (lane < p && r < p) {
+  double* T = Es[w];
+  double sg[LYAP_KMAX], mk_[LYAP_KMAX];
+  for (int t = 0; t < a.K; ++t) {
+    sg[t] = a.sigma[slot * a.K + t];
+    mk_[t] = a.mask[slot * a.K + t];
+  }
+  for (int e = lane; e < 32 * 32; e += 32) {  // coalesced assembly of E(v), identity padding
+    const int r = e & 31, j = e >> 5;
+    double v = (r == j) ? 1.0 : 0.0;
+    if (r < p && j < p) {
       v = 0.0;
       for (int t = 0; t < a.K; ++t) {
-        const double phi = a.Phi[(int64_t)t * pp + lane * p + r];
-        v += a.mask[slot * a.K + t] != 0.0 ? a.sigma[slot * a.K + t] * phi - a.Psi[(int64_t)t * pp + lane * p + r] : phi;
+        const double phi = a.Phi[(int64_t)t * pp + j * p + r];
+        v += mk_[t] != 0.0 ? sg[t] * phi - a.Psi[(int64_t)t * pp + j * p + r] : phi;
       }
     }
-    col[r] = v;
+    T[j * 33 + r] = v;
   }
+  __syncwarp();
+  double col[32];
+#pragma unroll
+  for (int r = 0; r < 32; ++r) col[r] = T[lane * 33 + r];
   int perm[32];
 #pragma unroll
   for (int c = 0; c < 32; ++c) {
@@ -544,12 +554,12 @@ __global__ void __launch_bounds__(128) k_cfactor32(EngArgs a) {
       for (int r = 0; r < 32; ++r) col[r] = __shfl_sync(0xffffffffu, col[r], partner);
     }
   }
-  if (lane < p) {
-    double* out = a.Einv + (int64_t)slot * pp + (int64_t)lane * p;
+  __syncwarp();
 #pragma unroll
-    for (int r = 0; r < 32; ++r)
-      if (r < p) out[r] = col[r];
-  }
+  for (int r = 0; r < 32; ++r) T[lane * 33 + r] = col[r];
+  __syncwarp();
+  double* out = a.Einv + (int64_t)slot * pp;
+  for (int e = lane; e < pp; e += 32) out[e] = T[(e / p) * 33 + e % p];  // coalesced store
 }
 
 // k_cpre: Rbuf[slot] = q^_m / eta_m for a slot whose next K1 input is a Krylov direction, else 0
