@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--no-profile", action="store_true", help="no per-launch K1 events (diagnostics)")
     ap.add_argument("--coarse", type=int, default=int(os.environ.get("BENCH_COARSE", "-1")),
                     help="two-level preconditioner coarse-space size (-1 auto, 0 off)")
+    ap.add_argument("--mixed", type=int, default=int(os.environ.get("BENCH_MIXED", "-1")),
+                    help="mixed-precision iterative refinement (-1 auto: n > 1536, 0 off, 1 on; DESIGN.md §2.8)")
     ap.add_argument("--recycle", type=int, default=int(os.environ.get("BENCH_RECYCLE", "0")),
                     help="recycle-space size s (0: off); spaces built from the 2^k grid corners before timing")
     return ap.parse_args()
@@ -249,7 +251,7 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     W = workloads.make(args.config)
     P = Problem(W.A0, W.Bl, W.Br, W.Q, W.E, profile=not args.no_profile, device=local, batch=args.batch, max_dim=args.max_dim,
-                coarse=args.coarse)
+                coarse=args.coarse, mixed=args.mixed)
     cost = P.cost_proxy(W.V)  # the engine's scheduling proxy: balances the strong-scaling shards
     emu = None
     if args.emulate_rank:
@@ -381,6 +383,8 @@ def main():
                                                      "recycle_s": args.recycle if args.recycle > 0 else ("auto" if recycle_ms else 0),
                                                      "recycle_build_ms": recycle_ms,
                                                      "applies_per_v": st["k1_vectors"] / (len(idx) * args.steps),
+                                                     "exact_applies_per_v": st["k1_exact_vectors"] / (len(idx) * args.steps),
+                                                     "mixed": P.mixed,
                                                      "shard_cost_max_over_mean": balance,
                                                      "coarse": P.info["coarse"],
                                                      "coarse_build_ms": P.info["coarse_build_ms"],

@@ -83,6 +83,14 @@ typedef struct {
                           of the off-block coupling T_o (randomized SVD at the first trace_batch).
                           -1 (default) auto: 32 when n k >= 2000, else off; 0 off; > 0 that size
                           (multiple of 8, <= 256).  Recycle spaces are not used together with it. */
+  int32_t mixed;       /* mixed-precision iterative refinement: the Krylov steps apply
+                          the dense Cauchy part of T with an FP32-accurate tensor-core GEMM (3xTF32,
+                          operands split hi + lo), every cycle ends once its estimated residual has
+                          dropped by mixed_eta, and every cycle starts from the TRUE residual of the
+                          exact FP64 operator (DMMA GEMM), so the stopping test (tol, reading R14)
+                          is unchanged.  -1 (default) auto: on when n > 1536 (the large-tile
+                          K1 configuration, where the T-apply dominates); 0 off; 1 on. */
+  double mixed_eta;    /* residual reduction per refinement cycle (default 1e-4) */
 } lyap_opts;
 
 typedef struct {
@@ -112,6 +120,8 @@ typedef struct {
   double recycle_build_ms; /* time spent building recycle spaces (automatic or lyap_build_recycle) */
   int64_t graph_instantiations; /* engine CUDA graphs instantiated (a repeated call updates them in place) */
   int64_t graph_updates;        /* engine CUDA graphs updated in place (cudaGraphExecUpdate) */
+  int64_t k1_exact_vectors;     /* of k1_vectors, those applied with the exact FP64 GEMM (all of them
+                                   unless opts.mixed: then the VERIFY applications) */
 } lyap_stats;
 
 /* Fills *opts with the defaults above. */

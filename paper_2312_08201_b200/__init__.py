@@ -43,7 +43,7 @@ class Problem:
     def __init__(self, A0, Bl, Br, Q, E, *, tol: float = 1e-12, max_dim: int = 0, max_restarts: int = 30,
                  batch: int = 0, warm_start: bool = False, max_cond_S: float = 1e8, device: int = -1,
                  profile: bool = False, schedule: bool = True, recycle: int = -1, check_stable: bool = False,
-                 coarse: int = -1):
+                 coarse: int = -1, mixed: int = -1, mixed_eta: float = 1e-4):
         A0 = _f64(A0)
         n = A0.shape[0]
         Bl = _f64(Bl)
@@ -66,12 +66,15 @@ class Problem:
         o.recycle = int(recycle)
         o.check_stable = int(check_stable)
         o.coarse = int(coarse)
+        o.mixed, o.mixed_eta = int(mixed), float(mixed_eta)
         self._ctx = C.c_void_p()
         setup = lib.lyap_setup_qlin if qlin else lib.lyap_setup
         rc = setup(n, k, _dp(A0), _dp(Bl), _dp(Br), _dp(Q), _dp(E), C.byref(o), C.byref(self._ctx))
         if rc != LYAP_OK:
             raise LyapError(rc, lib.lyap_last_error(None).decode())
         self.n, self.k = n, k
+        # mixed-precision mode in effect (opts.mixed -1 = auto: on for n > 1536)
+        self.mixed = int(mixed) if int(mixed) >= 0 else int(n > 1536)
 
     def like(self, Bl, Br=None) -> "Problem":
         """Same A0, Q, E with another (Bl, Br) configuration (NEXT row f4): reuses this problem's

@@ -28,7 +28,8 @@ class Opts(C.Structure):
     _fields_ = [("tol", C.c_double), ("max_dim", C.c_int32), ("max_restarts", C.c_int32),
                 ("batch", C.c_int32), ("warm_start", C.c_int32), ("max_cond_S", C.c_double),
                 ("device", C.c_int32), ("profile", C.c_int32), ("schedule", C.c_int32), ("recycle", C.c_int32),
-                ("check_stable", C.c_int32), ("coarse", C.c_int32)]
+                ("check_stable", C.c_int32), ("coarse", C.c_int32), ("mixed", C.c_int32),
+                ("mixed_eta", C.c_double)]
 
 
 class Info(C.Structure):
@@ -43,7 +44,8 @@ class Stats(C.Structure):
     _fields_ = [("k1_launches", C.c_int64), ("k1_vectors", C.c_int64), ("k1_ms", C.c_double),
                 ("k1_flops", C.c_double), ("iterations", C.c_int64), ("kernel_launches", C.c_int64),
                 ("batch_ms", C.c_double), ("recycle_build_ms", C.c_double),
-                ("graph_instantiations", C.c_int64), ("graph_updates", C.c_int64)]
+                ("graph_instantiations", C.c_int64), ("graph_updates", C.c_int64),
+                ("k1_exact_vectors", C.c_int64)]
 
 
 def _load():

@@ -22,10 +22,13 @@ struct Basis {
   double* Sinv = nullptr;  // S_r^{-1}
   double* Qr = nullptr;    // S_r^{-1} Q S_r^{-T} (nterms matrices for a v-linear Q)
   double* Er = nullptr;    // S_r^T E S_r
+  float* Lf32 = nullptr;   // mixed precision: [hi | lo] float planes of Lf (npad x 2 npad), built on first use
+  int lf32_mode = 0;       // split mode Lf32 was built with (1: 3xTF32 hi/lo, 2: one float plane)
   ~Basis() {
     cudaSetDevice(device);
     for (double* p : {lam, Lf, Sr, Sinv, Qr, Er})
       if (p) cudaFree(p);
+    if (Lf32) cudaFree(Lf32);
   }
 };
 
@@ -65,6 +68,8 @@ struct Engine {
   int nchunk = 0;   // chunks of the vector length for the reductions
   int groups = 1;   // slot groups, each on its own stream (K1 of one overlaps the Krylov kernels of the other)
   double *Bop = nullptr, *U = nullptr;            // groups x npad x ncol  (ncol per group)
+  float *Bop32 = nullptr, *U32 = nullptr;         // mixed precision: groups x 2 npad x ncol (lo | hi), groups x npad x ncol
+  int mp = 0;                                     // mixed-precision mode the buffers were made for
   double *Xin = nullptr, *X = nullptr;            // b x L
   double *rhs = nullptr, *t0s = nullptr;          // qlin: per-slot G0(v) (b x L) and t0(v) (b)
   double* Qb = nullptr;                           // b x (mmax+1) x L  (unnormalised basis)
@@ -82,7 +87,8 @@ struct Engine {
   // two-level preconditioner (coarse p > 0): flexible basis Zb = P^{-1} q_j, coarse scratch
   double *Zb = nullptr, *Rbuf = nullptr, *Yz = nullptr, *Cc = nullptr, *Wc = nullptr, *Einv = nullptr;
   int pc = 0;                                     // coarse size the buffers were made for
-  int* ctrl = nullptr;                            // per group 8 ints: [2]=active slots, [4..5]=applied vectors;
+  int* ctrl = nullptr;                            // per group 8 ints: [2]=active slots, [3]=of them VERIFY,
+                                                  // [4..5]=applied vectors, [6..7]=of them VERIFY;
                                                   // then 8 shared: [0]=next queue position, [1]=done count
   int* h_ctrl = nullptr;                          // pinned mirror
   int* order = nullptr;                           // queue order (nv_cap)
@@ -143,4 +149,8 @@ struct lyap_ctx {
   double* cublas_ws[4] = {};
   double* Spad = nullptr;  // lyap_solution: padded S_r^T and S_r (row-major np x np each)
   cudaEvent_t xjoin[4] = {};
+  // mixed precision: per slot group a side stream for the exact (VERIFY) DMMA GEMM, which runs beside
+  // the 3xTF32 GEMM of the Krylov steps, and the fork / join events around it
+  cudaStream_t mpstream[4] = {};
+  cudaEvent_t mpfork[4] = {}, mpjoin[4] = {};
 };

@@ -29,6 +29,8 @@ struct EngArgs {
   int64_t L, npad, nrep, npairs, two_np, n;
   int nchunk;
   double tol, tol_inner, t0;
+  double eta_rel;  // mixed precision: a cycle also ends once its estimated residual is
+                   // eta_rel times the cycle's true starting residual (iterative refinement); 0: off
   int max_restarts, warm;
   const double *V, *g0, *hf, *Pb;  // Pb: per-rep diagonal blocks of T (preconditioner, k_pfactor)
   const int* order;  // queue position -> row of V (null: identity)
@@ -132,29 +134,47 @@ __global__ void k_assign(EngArgs a) {
     }
   }
   __syncthreads();
-  // active slots after assignment (VERIFY or ITER), compacted in slot order for K1
+  // active slots after assignment (VERIFY or ITER), compacted for K1: VERIFY slots first (positions
+  // [0, nver): with mixed precision they take the exact FP64 apply), then ITER slots, each in slot order.
   // K1-active: VERIFY, and ITER past the recycled directions (those steps need no T-apply)
-  int isact = 0;
+  int isver = 0, isit = 0;
   if (tid < a.b) {
     const int ph = a.phase[tid];
-    isact = (ph == PH_VERIFY) || (ph == PH_ITER && a.m[tid] >= a.su[tid]);
+    isver = ph == PH_VERIFY;
+    isit = ph == PH_ITER && a.m[tid] >= a.su[tid];
   }
-  int xa = isact;
+  int xv = isver, xi = isit;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    int y = __shfl_up_sync(0xffffffffu, xa, o);
-    if (lane >= o) xa += y;
+    const int yv = __shfl_up_sync(0xffffffffu, xv, o), yi = __shfl_up_sync(0xffffffffu, xi, o);
+    if (lane >= o) {
+      xv += yv;
+      xi += yi;
+    }
+  }
+  __shared__ int wsum2[32];
+  __syncthreads();
+  if (lane == 31) {
+    wsum[w] = xv;
+    wsum2[w] = xi;
   }
   __syncthreads();
-  if (lane == 31) wsum[w] = xa;
-  __syncthreads();
-  int offa = 0;
-  for (int i = 0; i < w; ++i) offa += wsum[i];
-  if (isact) a.alist[offa + xa - 1] = tid;
-  const int act = __syncthreads_count(isact);
+  int offv = 0, offi = 0, nver = 0;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+    if (i < w) {
+      offv += wsum[i];
+      offi += wsum2[i];
+    }
+    nver += wsum[i];
+  }
+  if (isver) a.alist[offv + xv - 1] = tid;
+  if (isit) a.alist[nver + offi + xi - 1] = tid;
+  const int act = __syncthreads_count(isver || isit);
   if (tid == 0) {
     a.ctrl[2] = act;
-    *reinterpret_cast<unsigned long long*>(a.ctrl + 4) += (unsigned long long)act;  // applied vectors
+    a.ctrl[3] = nver;
+    *reinterpret_cast<unsigned long long*>(a.ctrl + 4) += (unsigned long long)act;   // applied vectors
+    *reinterpret_cast<unsigned long long*>(a.ctrl + 6) += (unsigned long long)nver;  // of them VERIFY
   }
 }
 
@@ -1004,7 +1024,8 @@ __global__ void __launch_bounds__(128) k_ctrl(EngArgs a) {
     e[m] = c * e[m];
     const double est = fabs(e[m + 1]);
     const bool breakdown = !(hn > 1e-300 * a.bnorm[slot]);
-    done = (est <= a.tol_inner * a.bnorm[slot]) || (m + 1 >= a.mmax) || breakdown || !isfinite(est);
+    done = (est <= fmax(a.tol_inner * a.bnorm[slot], a.eta_rel * eta[0])) || (m + 1 >= a.mmax) || breakdown ||
+           !isfinite(est);
     // a recycled direction dependent on the current space is not a "lucky" breakdown: finish the
     // cycle and run this v's restarts as plain GMRES
     // (su itself must stay until this cycle's update: its first su search directions are u_i;

@@ -40,7 +40,16 @@ struct K1Args {
   const int* nactive;  // engine: number of active slots (null: all nslot vectors are active)
   const int* alist;    // engine: active slot ids, compacted (null: identity)
   const double* rhs;   // engine, v-linear Q: per-slot right-hand side (nslot x L); null: g0
+  // mixed precision (engine mode): active positions [0, *nver) are VERIFY slots (exact
+  // FP64 apply through the DMMA GEMM), positions [*nver, *nactive) ITER slots (apply through the
+  // FP32-accurate tensor-core GEMM on the float planes B32 / U32).  nver == null: all FP64.
+  const int* nver;
 };
+
+// float split of a double for the 3xTF32 GEMM: hi = x rounded to TF32 (10-bit mantissa), lo = x - hi
+__device__ __forceinline__ float tf32_rn(float f) {
+  return __uint_as_float((__float_as_uint(f) + 0x1000u) & 0xFFFFE000u);
+}
 
 // Fused-epilogue arguments of the K1 GEMM (EPI = k > 0): the k1_epi contraction done from the CTA's
 // accumulator tile in shared memory, so U never goes to global memory and k1_epi is not launched.
@@ -58,11 +67,16 @@ enum : int { PH_FREE = 0, PH_IDLE = 1, PH_VERIFY = 2, PH_ITER = 3, PH_XUPD = 4, 
 
 // ------------------------------------------------------------------------------------------
 // K1a prologue: Bop[i][(slot*k + s)*k + t] = folded (B^r_is * X_ti)   (the Hadamard B operand)
-template <int K>
+// MP = 0: FP64 operand only.  MP = 1 (3xTF32) / 2 (one float plane): also the float operand B32
+// (2 npad x ncol: rows [0, npad) lo parts, rows [npad, 2 npad) hi parts) for every active position,
+// and the FP64 operand only for the VERIFY positions [0, nver).
+template <int K, int MP = 0>
 __global__ void __launch_bounds__(256) k1_gen(K1Args a, const double* __restrict__ bhr, int npad,
-                                               int two_np, double* __restrict__ Bop, int64_t ncol) {
+                                               int two_np, double* __restrict__ Bop, int64_t ncol,
+                                               float* __restrict__ B32 = nullptr) {
   constexpr int TS = K1Tile<K>::TS, NC = K1Tile<K>::NC, TC = K1_TILE_C;
   const int nact = k1_nact(a);
+  const int nver = MP ? *a.nver : nact;
   const int i0 = blockIdx.x * TC, s0 = blockIdx.y * TS;
   if (s0 >= nact) return;
   __shared__ double xs[TS][K][TC];
@@ -90,7 +104,29 @@ __global__ void __launch_bounds__(256) k1_gen(K1Args a, const double* __restrict
     } else {
       val = bs[r][s] * xs[sl][t][r];
     }
-    Bop[(int64_t)c * ncol + (int64_t)(s0 + sl) * K * K + col % (K * K)] = val;
+    const int64_t o = (int64_t)c * ncol + (int64_t)(s0 + sl) * K * K + col % (K * K);
+    if (!MP || s0 + sl < nver) Bop[o] = val;
+    if (MP) {
+      const float f = (float)val;
+      const float hi = MP == 1 ? tf32_rn(f) : f;
+      B32[(int64_t)npad * ncol + o] = hi;
+      if (MP == 1) B32[o] = (float)(val - (double)hi);
+    }
+  }
+}
+
+// mixed precision: Lf32 = [hi | lo] float planes of the folded Cauchy matrix (npad x 2 npad row-major;
+// MP = 2: lo = 0), built once per seed
+template <int MP>
+__global__ void k_split_Lf(const double* __restrict__ Lf, int64_t npad, float* __restrict__ Lf32) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < npad * npad;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / npad, i = e % npad;
+    const double x = Lf[e];
+    const float f = (float)x;
+    const float hi = MP == 1 ? tf32_rn(f) : f;
+    Lf32[j * 2 * npad + i] = hi;
+    Lf32[j * 2 * npad + npad + i] = MP == 1 ? (float)(x - (double)hi) : 0.f;
   }
 }
 
@@ -322,21 +358,25 @@ __device__ __forceinline__ void k1_out_element(const K1EpiArgs& ep, int slot, in
 
 // ------------------------------------------------------------------------------------------
 // K1c epilogue: contract U over t with B~l, add T_d, form C(v) X (or the VERIFY residual).
-template <int K>
+// MP: positions [0, nver) read the FP64 GEMM output U, the others the float output U32 (same layout)
+template <int K, bool MP = false>
 __global__ void __launch_bounds__(256) k1_epi(K1Args a, const double* __restrict__ U, int64_t ncol,
                                                const double* __restrict__ btl, const double* __restrict__ F,
                                                const double* __restrict__ g0, int npad, int two_np, int npairs,
-                                               int n) {
+                                               int n, const float* __restrict__ U32 = nullptr) {
   constexpr int TS = K1Tile<K>::TS, NC = K1Tile<K>::NC, TC = K1_TILE_C;
   const int nact = k1_nact(a);
   const int i0 = blockIdx.x * TC, s0 = blockIdx.y * TS;
   if (s0 >= nact) return;
   __shared__ double us[TC][NC + 1];
   __shared__ double xs[TS][K][TC];
+  const int nver = MP ? *a.nver : nact;
 #pragma unroll
   for (int idx = threadIdx.x; idx < TC * NC; idx += K1_THREADS) {
     int r = idx / NC, col = idx % NC;
-    us[r][col] = (s0 + col / (K * K) < nact) ? U[(int64_t)(i0 + r) * ncol + (int64_t)s0 * K * K + col] : 0.0;
+    const int pos = s0 + col / (K * K);
+    const int64_t o = (int64_t)(i0 + r) * ncol + (int64_t)s0 * K * K + col;
+    us[r][col] = pos < nact ? ((MP && pos >= nver) ? (double)U32[o] : U[o]) : 0.0;
   }
 #pragma unroll
   for (int idx = threadIdx.x; idx < TS * K * TC; idx += K1_THREADS) {

@@ -131,7 +131,7 @@ void upload_seeds(lyap_ctx* ctx) {
 
 // ------------------------------------------------------------------ engine allocation
 void free_engine(Engine& g, bool keep_order = true) {
-  void* ps[] = {g.Bop, g.U, g.Xin, g.X, g.Qb, g.Minv, g.sigma, g.mask, g.eta, g.H, g.e, g.y,
+  void* ps[] = {g.Bop, g.U, g.Bop32, g.U32, g.Xin, g.X, g.Qb, g.Minv, g.sigma, g.mask, g.eta, g.H, g.e, g.y,
                 g.bnorm, g.part, g.part3, g.phase, g.m, g.vidx, g.applies, g.restarts, g.ctrl,
                 g.part2, g.Gq, g.cf, g.Hraw, g.rhs, g.t0s, g.Zb, g.Rbuf, g.Yz, g.Cc, g.Wc, g.Einv};
   for (void* p : ps) dfree(p);
@@ -210,11 +210,44 @@ void configure_run(const Seed& s, Engine& g, int b) {
 int coarse_size(const lyap_ctx* ctx);
 void ensure_coarse(lyap_ctx* ctx);
 
+// Mixed-precision iterative refinement (opts.mixed): 0 off, 1 3xTF32 (operands split
+// hi + lo, two cuBLAS TF32 GEMMs), 2 one float plane with the cuBLAS compute type LYAP_MP_GEMM names
+// (bf16x9 | tf32 | fp32: measurement alternatives).
+int mp_mode(const lyap_ctx* ctx) {
+  const int o = ctx->opts.mixed;
+  if (!(o > 0 || (o < 0 && ctx->seed.n > SMALL_N))) return 0;
+  const char* ev = std::getenv("LYAP_MP_GEMM");
+  return (ev && std::strcmp(ev, "3xtf32") != 0) ? 2 : 1;
+}
+cublasComputeType_t mp_compute(int mode) {
+  if (mode == 1) return CUBLAS_COMPUTE_32F_FAST_TF32;
+  const char* ev = std::getenv("LYAP_MP_GEMM");
+  if (ev && std::strcmp(ev, "bf16x9") == 0) return CUBLAS_COMPUTE_32F_EMULATED_16BFX9;
+  if (ev && std::strcmp(ev, "tf32") == 0) return CUBLAS_COMPUTE_32F_FAST_TF32;
+  return CUBLAS_COMPUTE_32F;
+}
+// float planes of the folded Cauchy matrix for the mixed-precision GEMM (once per seed basis)
+void ensure_lf32(lyap_ctx* ctx, int mode) {
+  Basis& B = *ctx->basis;
+  if (B.Lf32 && B.lf32_mode == mode) return;
+  if (B.Lf32) cudaFree(B.Lf32);
+  B.Lf32 = nullptr;
+  const int64_t np = ctx->seed.npad;
+  B.Lf32 = dalloc<float>(ctx, (size_t)np * 2 * np, false);
+  B.lf32_mode = mode;
+  if (mode == 1)
+    k_split_Lf<1><<<1184, 256, 0, ctx->stream>>>(B.Lf, np, B.Lf32);
+  else
+    k_split_Lf<2><<<1184, 256, 0, ctx->stream>>>(B.Lf, np, B.Lf32);
+  LAUNCHED();
+}
+
 void ensure_engine(lyap_ctx* ctx, int b, int mmax) {
   Engine& g = ctx->eng;
   const Seed& s = ctx->seed;
   const int pc = ctx->coarse.p;
-  if (g.Qb && g.mmax == mmax && g.bcap >= b && g.pc == pc) {
+  const int mp = mp_mode(ctx);
+  if (g.Qb && g.mmax == mmax && g.bcap >= b && g.pc == pc && g.mp == mp) {
     configure_run(s, g, b);
     return;
   }
@@ -231,6 +264,11 @@ void ensure_engine(lyap_ctx* ctx, int b, int mmax) {
   g.nchunk = (int)((g.L + RED_CE - 1) / RED_CE);
   g.Bop = dalloc<double>(ctx, (size_t)s.npad * colcap);
   g.U = dalloc<double>(ctx, (size_t)s.npad * colcap);
+  g.mp = mp;
+  if (mp) {
+    g.Bop32 = dalloc<float>(ctx, (size_t)2 * s.npad * colcap);
+    g.U32 = dalloc<float>(ctx, (size_t)s.npad * colcap);
+  }
   g.Xin = dalloc<double>(ctx, (size_t)b * g.L);
   g.X = dalloc<double>(ctx, (size_t)b * g.L);
   g.Qb = dalloc<double>(ctx, (size_t)b * (mmax + 1) * g.L);
@@ -278,7 +316,7 @@ void ensure_engine(lyap_ctx* ctx, int b, int mmax) {
 // prologue, GEMM, k1_epi.  Measured (bench, B200): c2 94.5k -> 96.0k v/s fused; c5 907.9 -> 898.9
 // fused -- with 1 CTA per SM the large-tile GEMM runs the epilogue at 8 warps per SM, slower than
 // the separate, fully occupied k1_epi, so the large configuration keeps it separate.
-inline bool k1_fused(int64_t k, int64_t n) { return (k == 1 || k == 2 || k == 4) && n <= SMALL_N; }
+inline bool k1_fused(int64_t k, int64_t n, int mp = 0) { return (k == 1 || k == 2 || k == 4) && n <= SMALL_N && !mp; }
 
 template <int BM, int BN, int WM, int WN, int ST, int BK>
 void set_smem_attrs(lyap_ctx* ctx) {
@@ -294,13 +332,13 @@ void set_smem_attrs(lyap_ctx* ctx) {
 
 template <int BM, int BN, int WM, int WN, int ST, int BK>
 void launch_gemm(lyap_ctx* ctx, const Seed& s, const double* Bop, double* U, int64_t ncol, const K1Args& a,
-                 cudaStream_t st) {
+                 cudaStream_t st, bool fuse) {
   using Cfg = DgemmCfg<BM, BN, WM, WN, ST, BK>;
   const int kpad = (int)std::min<int64_t>(roundup(s.n, BK), s.npad);  // skip zero rows
   dim3 grid((unsigned)((ncol / BN) * (s.npad / BM)));
   K1EpiArgs ep{a, s.btl, s.F, s.g0, (int)s.npad, (int)(2 * s.npairs), (int)s.npairs, (int)s.n};
   const int cpa = (int)(s.k * s.k);
-  switch (k1_fused(s.k, s.n) ? (int)s.k : 0) {
+  switch (fuse ? (int)s.k : 0) {
     case 1:
       k1_dgemm<BM, BN, WM, WN, ST, BK, 0, 1><<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(
           s.Lf, Bop, nullptr, (int)s.npad, (int)ncol, kpad, (int)s.npad, a.nactive, cpa, DgemmOut{}, ep);
@@ -320,25 +358,80 @@ void launch_gemm(lyap_ctx* ctx, const Seed& s, const double* Bop, double* U, int
 }
 
 void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, cudaEvent_t evb = nullptr, cudaEvent_t eve = nullptr,
-               unsigned evflags = 0, int group = 0) {
+               unsigned evflags = 0, int group = 0, int mp = 0) {
   const Seed& s = ctx->seed;
   Engine g = ctx->eng;  // copy: operand buffers of this slot group
   g.Bop += (size_t)group * s.npad * g.ncol;
   g.U += (size_t)group * s.npad * g.ncol;
   const int two_np = (int)(2 * s.npairs);
+  const bool fuse = k1_fused(s.k, s.n, mp);
+  float* B32 = mp ? g.Bop32 + (size_t)group * 2 * s.npad * g.ncol : nullptr;
+  float* U32 = mp ? g.U32 + (size_t)group * s.npad * g.ncol : nullptr;
   K_DISPATCH(s.k, {
     dim3 grid((unsigned)(s.npad / K1_TILE_C), (unsigned)((a.nslot + K1Tile<KK>::TS - 1) / K1Tile<KK>::TS));
-    k1_gen<KK><<<grid, K1_THREADS, 0, st>>>(a, s.bhr, (int)s.npad, two_np, g.Bop, g.ncol);
+    if (mp == 1)
+      k1_gen<KK, 1><<<grid, K1_THREADS, 0, st>>>(a, s.bhr, (int)s.npad, two_np, g.Bop, g.ncol, B32);
+    else if (mp == 2)
+      k1_gen<KK, 2><<<grid, K1_THREADS, 0, st>>>(a, s.bhr, (int)s.npad, two_np, g.Bop, g.ncol, B32);
+    else
+      k1_gen<KK><<<grid, K1_THREADS, 0, st>>>(a, s.bhr, (int)s.npad, two_np, g.Bop, g.ncol);
   });
   LAUNCHED();
   if (evb) CK(cudaEventRecordWithFlags(evb, st, evflags));
-  if (s.n <= SMALL_N)
-    launch_gemm<S_BM, S_BN, S_WM, S_WN, S_ST, S_BK>(ctx, s, g.Bop, g.U, g.ncol, a, st);
-  else
-    launch_gemm<G_BM, G_BN, G_WM, G_WN, G_ST, G_BK>(ctx, s, g.Bop, g.U, g.ncol, a, st);
-  LAUNCHED();
+  if (!mp) {
+    if (s.n <= SMALL_N)
+      launch_gemm<S_BM, S_BN, S_WM, S_WN, S_ST, S_BK>(ctx, s, g.Bop, g.U, g.ncol, a, st, fuse);
+    else
+      launch_gemm<G_BM, G_BN, G_WM, G_WN, G_ST, G_BK>(ctx, s, g.Bop, g.U, g.ncol, a, st, fuse);
+    LAUNCHED();
+  } else {
+    // mixed precision: the exact FP64 GEMM of the VERIFY positions [0, nver) (few
+    // columns: the small-tile DMMA configuration) on the group's side stream, beside the float GEMM
+    // of all positions on the tensor cores; k1_epi picks U or U32 per position
+    if (!ctx->mpstream[group]) {
+      CK(cudaStreamCreateWithFlags(&ctx->mpstream[group], cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&ctx->mpfork[group], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ctx->mpjoin[group], cudaEventDisableTiming));
+    }
+    cudaStream_t ss = ctx->mpstream[group];
+    CK(cudaEventRecord(ctx->mpfork[group], st));
+    CK(cudaStreamWaitEvent(ss, ctx->mpfork[group], 0));
+    K1Args av = a;
+    av.nactive = a.nver;
+    launch_gemm<S_BM, S_BN, S_WM, S_WN, S_ST, S_BK>(ctx, s, g.Bop, g.U, g.ncol, av, ss, false);
+    LAUNCHED();
+    CK(cudaEventRecord(ctx->mpjoin[group], ss));
+    cublasHandle_t hb = ctx->cublas_eng[group];
+    CKB(cublasSetStream(hb, st));
+    const int Nc = (int)g.ncol, M = (int)s.npad;
+    const int Kd = (int)std::min<int64_t>(roundup(s.n, 16), s.npad);  // zero rows skipped
+    const float one = 1.f, zero = 0.f;
+    const float* A32 = ctx->basis->Lf32;  // row-major npad x 2 npad: [hi | lo]
+    const float* Bhi = B32 + (size_t)s.npad * g.ncol;
+    // row-major U32 = A B is column-major U32^T = B^T A^T (m = columns, n = rows)
+    if (mp == 1) {
+      // U32 = A_hi B_lo + A_lo B_hi (one GEMM over the stacked K), then U32 += A_hi B_hi
+      CKB(cublasGemmEx(hb, CUBLAS_OP_N, CUBLAS_OP_N, Nc, M, Kd, &one, B32, CUDA_R_32F, Nc, A32, CUDA_R_32F,
+                       (int)(2 * s.npad), &zero, U32, CUDA_R_32F, Nc, CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT));
+      CKB(cublasGemmEx(hb, CUBLAS_OP_N, CUBLAS_OP_N, Nc, M, Kd, &one, Bhi, CUDA_R_32F, Nc, A32 + s.npad, CUDA_R_32F,
+                       (int)(2 * s.npad), &one, U32, CUDA_R_32F, Nc, CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT));
+      CKB(cublasGemmEx(hb, CUBLAS_OP_N, CUBLAS_OP_N, Nc, M, Kd, &one, Bhi, CUDA_R_32F, Nc, A32, CUDA_R_32F,
+                       (int)(2 * s.npad), &one, U32, CUDA_R_32F, Nc, CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT));
+    } else {
+      CKB(cublasGemmEx(hb, CUBLAS_OP_N, CUBLAS_OP_N, Nc, M, Kd, &one, Bhi, CUDA_R_32F, Nc, A32, CUDA_R_32F,
+                       (int)(2 * s.npad), &zero, U32, CUDA_R_32F, Nc, mp_compute(mp), CUBLAS_GEMM_DEFAULT));
+    }
+    CK(cudaStreamWaitEvent(st, ctx->mpjoin[group], 0));
+  }
   if (eve) CK(cudaEventRecordWithFlags(eve, st, evflags));
-  if (!k1_fused(s.k, s.n)) {
+  if (mp) {
+    K_DISPATCH(s.k, {
+      dim3 grid((unsigned)(s.npad / K1_TILE_C), (unsigned)((a.nslot + K1Tile<KK>::TS - 1) / K1Tile<KK>::TS));
+      k1_epi<KK, true><<<grid, K1_THREADS, 0, st>>>(a, g.U, g.ncol, s.btl, s.F, s.g0, (int)s.npad, two_np,
+                                                    (int)s.npairs, (int)s.n, U32);
+    });
+    LAUNCHED();
+  } else if (!fuse) {
     K_DISPATCH(s.k, {
       dim3 grid((unsigned)(s.npad / K1_TILE_C), (unsigned)((a.nslot + K1Tile<KK>::TS - 1) / K1Tile<KK>::TS));
       k1_epi<KK><<<grid, K1_THREADS, 0, st>>>(a, g.U, g.ncol, s.btl, s.F, s.g0, (int)s.npad, two_np, (int)s.npairs,
@@ -390,6 +483,9 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   a.nchunk = g.nchunk;
   a.tol = ctx->opts.tol;
   a.tol_inner = 0.5 * ctx->opts.tol;
+  const int mp = record ? 0 : mp_mode(ctx);
+  a.eta_rel = mp ? ctx->opts.mixed_eta : 0.0;
+  if (mp) ensure_lf32(ctx, mp);
   a.t0 = s.t0;
   a.nterms = s.qlin ? s.nterms : 0;
   a.t0t = s.t0t;
@@ -489,13 +585,14 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
     k1.nactive = x.ctrl + 2;
     k1.alist = x.alist;
     k1.rhs = x.rhs;
+    k1.nver = mp ? x.ctrl + 3 : nullptr;
     gk[gi] = k1;
   }
 
   const size_t upd_smem = sizeof(double) * (mmax + 1);
   const size_t cf_smem = sizeof(double) * (size_t)a.pc * a.pc + sizeof(int) * (size_t)a.pc + 16;
-  if (a.pc > 0) {
-    CK(cudaFuncSetAttribute(k_cfactor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cf_smem));
+  if (a.pc > 0) CK(cudaFuncSetAttribute(k_cfactor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cf_smem));
+  if (a.pc > 0 || mp) {
     for (int gi = 0; gi < G; ++gi)
       if (!ctx->cublas_eng[gi]) {  // a handle per slot group with its own workspace (graph capture)
         CKB(cublasCreate(&ctx->cublas_eng[gi]));
@@ -557,7 +654,7 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
       k_uapply<<<dim3((unsigned)std::min<int64_t>((g.L + 255) / 256, 64), (unsigned)bg), 256, 0, sg>>>(x);
       LAUNCHED();
     }
-    launch_k1(ctx, gk[gi], sg, evb, eve, evflags, gi);
+    launch_k1(ctx, gk[gi], sg, evb, eve, evflags, gi, mp);
     k_dots<<<dim3((unsigned)g.nchunk, (unsigned)bg, (unsigned)((mmax + DOT_IG) / DOT_IG)), 256, 0, sg>>>(x);
     LAUNCHED();
     k_gram<<<bg, 256, gram_smem, sg>>>(x);
@@ -659,6 +756,9 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
     unsigned long long nvec = 0;
     std::memcpy(&nvec, g.h_ctrl + 8 * gi + 4, 8);
     ctx->stats.k1_vectors += (int64_t)nvec;
+    unsigned long long nexact = nvec;
+    if (mp) std::memcpy(&nexact, g.h_ctrl + 8 * gi + 6, 8);
+    ctx->stats.k1_exact_vectors += (int64_t)nexact;
     ctx->stats.k1_flops += 2.0 * (double)s.n * s.n * s.k * s.k * (double)nvec;
   }
   return rc;
@@ -1011,6 +1111,8 @@ void lyap_default_opts(lyap_opts* o) {
   o->recycle = -1;
   o->check_stable = 0;
   o->coarse = -1;
+  o->mixed = -1;
+  o->mixed_eta = 1e-4;
 }
 
 const char* lyap_last_error(const lyap_ctx* c) { return c ? c->err.c_str() : g_last_error.c_str(); }
@@ -1098,6 +1200,7 @@ static int setup_core(int64_t n, int64_t k, const double* A0, const double* Bl, 
   if (!(ctx->opts.tol > 0)) ctx->opts.tol = 1e-12;
   if (ctx->opts.max_restarts <= 0) ctx->opts.max_restarts = 30;
   if (!(ctx->opts.max_cond_S > 0)) ctx->opts.max_cond_S = 1e8;
+  if (!(ctx->opts.mixed_eta > 0 && ctx->opts.mixed_eta < 1)) ctx->opts.mixed_eta = 1e-4;
   // scratch
   double *dA = nullptr, *dBl = nullptr, *dBr = nullptr, *dQ = nullptr, *dE = nullptr, *Acm = nullptr, *Qs = nullptr,
          *Es = nullptr, *Blc = nullptr, *Brc = nullptr, *VR = nullptr, *Sr = nullptr, *Sinv = nullptr, *LU = nullptr,

@@ -598,3 +598,45 @@ def test_two_level_preconditioner_configs(name, p):
     assert a1 < a0, (a0, a1)
     P0.close()
     P1.close()
+
+
+# ----------------------------------------------------------------------------- mixed precision
+@pytest.mark.parametrize("n,k,seed", [(30, 3, 0), (64, 2, 1), (13, 1, 2), (40, 4, 3)])
+def test_mixed_precision_random(n, k, seed):
+    """opts.mixed = 1: Krylov steps with the 3xTF32 T-apply, every cycle restarted from
+    the exact FP64 true residual.  The stopping test is the FP64 one, so every v meets tol = 1e-12 and
+    the traces match the oracle; only the VERIFY applications are exact."""
+    rng = np.random.default_rng(120 + seed)
+    A0, Bl, Br, Q, E = workloads.random_stable(n, k, rng)
+    V = rng.uniform(0.05, 3.0, (29, k))
+    V[3, 0] = 0.0  # a masked column
+    P = _problem(A0, Bl, Br, Q, E, mixed=1, batch=8)
+    tau, st, ap, rs = P.trace_batch(V, return_diagnostics=True)
+    assert np.all(st == 0), (st, rs)
+    assert np.all(rs <= 1e-12)
+    assert rel_err(tau, oracle.trace_batch(A0, Bl, Br, Q, E, V)).max() <= RTOL
+    s = P.stats
+    assert 0 < s["k1_exact_vectors"] < s["k1_vectors"], s
+    P.close()
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_mixed_precision_configs(name):
+    """mixed = 1 forced on the small configurations (auto turns it on only for n > 1536): oracle
+    goldens at 1e-9, and the mixed and FP64-only engines agree to the solver tolerance."""
+    W = workloads.make(name)
+    g = _golden(name)
+    idx = np.array(g["indices"])
+    P1 = _problem(W.A0, W.Bl, W.Br, W.Q, W.E, mixed=1)
+    tau1, st, ap, rs = P1.trace_batch(W.V, return_diagnostics=True)
+    assert np.all(st == 0)
+    assert np.all(rs <= 1e-12)
+    assert rel_err(tau1[idx], np.array(g["traces"])).max() <= RTOL
+    exact = P1.stats["k1_exact_vectors"]
+    assert exact < 0.5 * P1.stats["k1_vectors"]
+    P0 = _problem(W.A0, W.Bl, W.Br, W.Q, W.E, mixed=0)
+    tau0 = P0.trace_batch(W.V)
+    assert P0.stats["k1_exact_vectors"] == P0.stats["k1_vectors"]
+    assert rel_err(tau1, tau0).max() <= 1e-10
+    P0.close()
+    P1.close()
