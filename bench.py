@@ -59,6 +59,8 @@ def parse():
                     help="two-level preconditioner coarse-space size (-1 auto, 0 off)")
     ap.add_argument("--mixed", type=int, default=int(os.environ.get("BENCH_MIXED", "-1")),
                     help="mixed-precision iterative refinement (-1 auto: n > 1536, 0 off, 1 on; DESIGN.md §2.8)")
+    ap.add_argument("--mixed-eta", type=float, default=float(os.environ.get("BENCH_MIXED_ETA", "1e-4")),
+                    help="residual reduction per mixed-precision refinement cycle")
     ap.add_argument("--recycle", type=int, default=int(os.environ.get("BENCH_RECYCLE", "0")),
                     help="recycle-space size s (0: off); spaces built from the 2^k grid corners before timing")
     return ap.parse_args()
@@ -251,7 +253,8 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     W = workloads.make(args.config)
     P = Problem(W.A0, W.Bl, W.Br, W.Q, W.E, profile=not args.no_profile, device=local, batch=args.batch, max_dim=args.max_dim,
-                coarse=args.coarse, mixed=args.mixed)
+                coarse=args.coarse, mixed=args.mixed,
+                mixed_eta=args.mixed_eta)
     cost = P.cost_proxy(W.V)  # the engine's scheduling proxy: balances the strong-scaling shards
     emu = None
     if args.emulate_rank:

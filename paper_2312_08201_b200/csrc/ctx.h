@@ -1,6 +1,7 @@
 // Internal state of one lyap_ctx (one seed A0).  Not part of the C-ABI.
 #pragma once
 #include <cublas_v2.h>
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
 
@@ -70,6 +71,7 @@ struct Engine {
   double *Bop = nullptr, *U = nullptr;            // groups x npad x ncol  (ncol per group)
   float *Bop32 = nullptr, *U32 = nullptr;         // mixed precision: groups x 2 npad x ncol (lo | hi), groups x npad x ncol
   int mp = 0;                                     // mixed-precision mode the buffers were made for
+  int* umctr = nullptr;                           // tcgen05 GEMM tile counters (2 per slot group)
   double *Xin = nullptr, *X = nullptr;            // b x L
   double *rhs = nullptr, *t0s = nullptr;          // qlin: per-slot G0(v) (b x L) and t0(v) (b)
   double* Qb = nullptr;                           // b x (mmax+1) x L  (unnormalised basis)
@@ -152,5 +154,11 @@ struct lyap_ctx {
   // mixed precision: per slot group a side stream for the exact (VERIFY) DMMA GEMM, which runs beside
   // the 3xTF32 GEMM of the Krylov steps, and the fork / join events around it
   cudaStream_t mpstream[4] = {};
+  // tcgen05 3xTF32 GEMM (umma.cuh): TMA tensor maps of Lf32 and of each slot group's float B operand,
+  // rebuilt when the buffers move
+  CUtensorMap um_ta{}, um_tb[4]{};
+  const void* um_ta_ptr = nullptr;
+  const void* um_tb_ptr[4] = {};
+  int64_t um_tb_ncol[4] = {};
   cudaEvent_t mpfork[4] = {}, mpjoin[4] = {};
 };

@@ -67,9 +67,21 @@ enum : int { PH_FREE = 0, PH_IDLE = 1, PH_VERIFY = 2, PH_ITER = 3, PH_XUPD = 4, 
 
 // ------------------------------------------------------------------------------------------
 // K1a prologue: Bop[i][(slot*k + s)*k + t] = folded (B^r_is * X_ti)   (the Hadamard B operand)
-// MP = 0: FP64 operand only.  MP = 1 (3xTF32) / 2 (one float plane): also the float operand B32
-// (2 npad x ncol: rows [0, npad) lo parts, rows [npad, 2 npad) hi parts) for every active position,
-// and the FP64 operand only for the VERIFY positions [0, nver).
+// one element of the B operand: fold(B^r_is X_ti) at tile row r (x: the slot's X_t tile, bs: B^r tile)
+template <int K>
+__device__ __forceinline__ double k1_bval(const double* x, const double (*bs)[K], int r, int s, bool pair) {
+  if (pair) {  // conjugate pair: (br + i bi)(x + i y)
+    const int ce = r & ~1;
+    const double xr = x[ce], yi = x[ce + 1];
+    const double br = bs[ce][s], bi = bs[ce + 1][s];
+    return (r & 1) ? (br * yi + bi * xr) : (br * xr - bi * yi);
+  }
+  return bs[r][s] * x[r];
+}
+
+// MP = 0: FP64 operand only.  MP = 1 (3xTF32) / 2 (one float plane): also the float operand B32, K-major
+// (2 ncol x npad: rows [0, ncol) lo parts, rows [ncol, 2 ncol) hi parts; umma.cuh) for every active
+// position, and the FP64 operand only for the VERIFY positions [0, nver).
 template <int K, int MP = 0>
 __global__ void __launch_bounds__(256) k1_gen(K1Args a, const double* __restrict__ bhr, int npad,
                                                int two_np, double* __restrict__ Bop, int64_t ncol,
@@ -89,28 +101,30 @@ __global__ void __launch_bounds__(256) k1_gen(K1Args a, const double* __restrict
 #pragma unroll
   for (int idx = threadIdx.x; idx < TC * K; idx += K1_THREADS) bs[idx / K][idx % K] = bhr[(int64_t)i0 * K + idx];
   __syncthreads();
+  if constexpr (MP == 0) {
 #pragma unroll
-  for (int idx = threadIdx.x; idx < TC * NC; idx += K1_THREADS) {
-    int r = idx / NC, col = idx % NC;
-    int sl = col / (K * K), s = (col / K) % K, t = col % K;
-    if (s0 + sl >= nact) continue;
-    int c = i0 + r;
-    double val;
-    if (c < two_np) {  // conjugate pair: (br + i bi)(x + i y)
-      int ce = r & ~1;
-      double x = xs[sl][t][ce], y = xs[sl][t][ce + 1];
-      double br = bs[ce][s], bi = bs[ce + 1][s];
-      val = (r & 1) ? (br * y + bi * x) : (br * x - bi * y);
-    } else {
-      val = bs[r][s] * xs[sl][t][r];
+    for (int idx = threadIdx.x; idx < TC * NC; idx += K1_THREADS) {
+      int r = idx / NC, col = idx % NC;
+      int sl = col / (K * K), s = (col / K) % K, t = col % K;
+      if (s0 + sl >= nact) continue;
+      Bop[(int64_t)(i0 + r) * ncol + (int64_t)(s0 + sl) * K * K + col % (K * K)] =
+          k1_bval<K>(xs[sl][t], bs, r, s, i0 + r < two_np);
     }
-    const int64_t o = (int64_t)c * ncol + (int64_t)(s0 + sl) * K * K + col % (K * K);
-    if (!MP || s0 + sl < nver) Bop[o] = val;
-    if (MP) {
+  } else {
+    // float planes, K-major (row = GEMM column n, contiguous along the coordinate): consecutive threads
+    // take consecutive coordinates, so the stores coalesce
+#pragma unroll
+    for (int idx = threadIdx.x; idx < TC * NC; idx += K1_THREADS) {
+      const int r = idx % TC, col = idx / TC;
+      const int sl = col / (K * K), s = (col / K) % K, t = col % K;
+      if (s0 + sl >= nact) continue;
+      const double val = k1_bval<K>(xs[sl][t], bs, r, s, i0 + r < two_np);
+      const int64_t nn = (int64_t)(s0 + sl) * K * K + col % (K * K);
+      if (s0 + sl < nver) Bop[(int64_t)(i0 + r) * ncol + nn] = val;  // FP64 operand of the exact apply
       const float f = (float)val;
       const float hi = MP == 1 ? tf32_rn(f) : f;
-      B32[(int64_t)npad * ncol + o] = hi;
-      if (MP == 1) B32[o] = (float)(val - (double)hi);
+      B32[(ncol + nn) * npad + i0 + r] = hi;
+      if (MP == 1) B32[nn * npad + i0 + r] = (float)(val - (double)hi);
     }
   }
 }
@@ -363,7 +377,7 @@ template <int K, bool MP = false>
 __global__ void __launch_bounds__(256) k1_epi(K1Args a, const double* __restrict__ U, int64_t ncol,
                                                const double* __restrict__ btl, const double* __restrict__ F,
                                                const double* __restrict__ g0, int npad, int two_np, int npairs,
-                                               int n, const float* __restrict__ U32 = nullptr) {
+                                               int n, const float* __restrict__ U32 = nullptr, int which = 0) {
   constexpr int TS = K1Tile<K>::TS, NC = K1Tile<K>::NC, TC = K1_TILE_C;
   const int nact = k1_nact(a);
   const int i0 = blockIdx.x * TC, s0 = blockIdx.y * TS;
@@ -373,10 +387,17 @@ __global__ void __launch_bounds__(256) k1_epi(K1Args a, const double* __restrict
   const int nver = MP ? *a.nver : nact;
 #pragma unroll
   for (int idx = threadIdx.x; idx < TC * NC; idx += K1_THREADS) {
-    int r = idx / NC, col = idx % NC;
+    // MP: the float product is column-major (U32t[n][m]): coordinate-fast mapping for coalesced loads
+    const int r = MP ? idx % TC : idx / NC, col = MP ? idx / TC : idx % NC;
     const int pos = s0 + col / (K * K);
-    const int64_t o = (int64_t)(i0 + r) * ncol + (int64_t)s0 * K * K + col;
-    us[r][col] = pos < nact ? ((MP && pos >= nver) ? (double)U32[o] : U[o]) : 0.0;
+    double u = 0.0;
+    if (pos < nact) {
+      if (MP && pos >= nver)
+        u = (double)U32[((int64_t)s0 * K * K + col) * npad + i0 + r];
+      else
+        u = U[(int64_t)(i0 + r) * ncol + (int64_t)s0 * K * K + col];
+    }
+    us[r][col] = u;
   }
 #pragma unroll
   for (int idx = threadIdx.x; idx < TS * K * TC; idx += K1_THREADS) {
@@ -387,6 +408,8 @@ __global__ void __launch_bounds__(256) k1_epi(K1Args a, const double* __restrict
   for (int idx = threadIdx.x; idx < TS * K * TC; idx += K1_THREADS) {
     int sl = idx / (K * TC), s = (idx / TC) % K, r = idx % TC;
     if (s0 + sl >= nact) continue;
+    // MP, which = 1 / 2: only the VERIFY / only the ITER positions (the other part's epilogue is fused)
+    if (MP && ((which == 1 && s0 + sl >= nver) || (which == 2 && s0 + sl < nver))) continue;
     const int slot = k1_slot(a, s0 + sl);
     const double* gsrc = a.rhs ? a.rhs + (int64_t)slot * a.L : g0;
     int c = i0 + r;

@@ -2,6 +2,7 @@
 // the .cuh files next to this one; this file holds the host control (setup flow, engine loop).
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <cusolverDn.h>
 
 #include <algorithm>
@@ -19,6 +20,7 @@
 #include "ctx.h"
 #include "engine.cuh"
 #include "k1.cuh"
+#include "umma.cuh"
 #include "sched.cuh"
 #include "stab.cuh"
 #include "setup.cuh"
@@ -131,7 +133,7 @@ void upload_seeds(lyap_ctx* ctx) {
 
 // ------------------------------------------------------------------ engine allocation
 void free_engine(Engine& g, bool keep_order = true) {
-  void* ps[] = {g.Bop, g.U, g.Bop32, g.U32, g.Xin, g.X, g.Qb, g.Minv, g.sigma, g.mask, g.eta, g.H, g.e, g.y,
+  void* ps[] = {g.Bop, g.U, g.Bop32, g.U32, g.umctr, g.Xin, g.X, g.Qb, g.Minv, g.sigma, g.mask, g.eta, g.H, g.e, g.y,
                 g.bnorm, g.part, g.part3, g.phase, g.m, g.vidx, g.applies, g.restarts, g.ctrl,
                 g.part2, g.Gq, g.cf, g.Hraw, g.rhs, g.t0s, g.Zb, g.Rbuf, g.Yz, g.Cc, g.Wc, g.Einv};
   for (void* p : ps) dfree(p);
@@ -198,10 +200,12 @@ int engine_groups(int b) {
 }
 
 // Sets the run shape (slots b, slot groups, K1 columns per group) of an allocated engine.
+// K1 GEMM column tile: the tcgen05 mixed-precision GEMM takes 256 columns per CTA
+int64_t col_tile(const Seed& s, int mp) { return mp ? 256 : (s.n <= SMALL_N ? S_BN : G_BN); }
 void configure_run(const Seed& s, Engine& g, int b) {
   g.b = b;
   g.groups = engine_groups(b);
-  g.ncol = roundup((int64_t)((b + g.groups - 1) / g.groups) * s.k * s.k, s.n <= SMALL_N ? S_BN : G_BN);
+  g.ncol = roundup((int64_t)((b + g.groups - 1) / g.groups) * s.k * s.k, col_tile(s, g.mp));
 }
 
 // The engine is allocated for a capacity of bcap slots and reused by any later call that needs
@@ -218,6 +222,46 @@ int mp_mode(const lyap_ctx* ctx) {
   if (!(o > 0 || (o < 0 && ctx->seed.n > SMALL_N))) return 0;
   const char* ev = std::getenv("LYAP_MP_GEMM");
   return (ev && std::strcmp(ev, "3xtf32") != 0) ? 2 : 1;
+}
+// the 3xTF32 product runs on the repo's tcgen05 kernel (umma.cuh); LYAP_MP_GEMM=cublas: three cuBLAS
+// TF32 GEMMs instead (measurement alternative)
+bool mp_umma() {
+  const char* ev = std::getenv("LYAP_MP_GEMM");
+  return !(ev && std::strcmp(ev, "cublas") == 0);
+}
+// UMMA column tile (LYAP_UM_BN=128: the 128 x 128, 3-stage configuration; measurement alternative)
+int um_bn() {
+  static const int bn = [] {
+    const char* ev = std::getenv("LYAP_UM_BN");
+    return (ev && std::atoi(ev) == 128) ? 128 : UM_BN;
+  }();
+  return bn;
+}
+CUtensorMap make_tmap_f32(lyap_ctx* ctx, const float* p, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                          uint32_t box_outer) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+    if (!f || q != cudaDriverEntryPointSuccess) {
+      set_err(ctx, "cuTensorMapEncodeTiled unavailable");
+      throw Fail{LYAP_ECUDA};
+    }
+    encode = (PFN_cuTensorMapEncodeTiled_v12000)f;
+  }
+  CUtensorMap m;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 4};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  if (encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)p, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+      CUDA_SUCCESS) {
+    set_err(ctx, "cuTensorMapEncodeTiled failed");
+    throw Fail{LYAP_ECUDA};
+  }
+  return m;
 }
 cublasComputeType_t mp_compute(int mode) {
   if (mode == 1) return CUBLAS_COMPUTE_32F_FAST_TF32;
@@ -254,20 +298,21 @@ void ensure_engine(lyap_ctx* ctx, int b, int mmax) {
   free_engine(g);
   g.bcap = b;
   g.mmax = mmax;
+  g.mp = mp;
   g.L = s.k * s.npad;
   // K1 operand columns for any run b' <= b and any group count (sum over groups of the rounded
   // per-group widths)
   int64_t colcap = 0;
   for (int G = 1; G <= 4; ++G)
-    colcap = std::max<int64_t>(colcap, G * roundup((int64_t)((b + G - 1) / G) * s.k * s.k, s.n <= SMALL_N ? S_BN : G_BN));
+    colcap = std::max<int64_t>(colcap, G * roundup((int64_t)((b + G - 1) / G) * s.k * s.k, col_tile(s, mp)));
   configure_run(s, g, b);
   g.nchunk = (int)((g.L + RED_CE - 1) / RED_CE);
   g.Bop = dalloc<double>(ctx, (size_t)s.npad * colcap);
   g.U = dalloc<double>(ctx, (size_t)s.npad * colcap);
-  g.mp = mp;
   if (mp) {
     g.Bop32 = dalloc<float>(ctx, (size_t)2 * s.npad * colcap);
     g.U32 = dalloc<float>(ctx, (size_t)s.npad * colcap);
+    g.umctr = dalloc<int>(ctx, 8);  // tile counters of the persistent tcgen05 GEMM (2 per slot group), zeroed
   }
   g.Xin = dalloc<double>(ctx, (size_t)b * g.L);
   g.X = dalloc<double>(ctx, (size_t)b * g.L);
@@ -357,6 +402,48 @@ void launch_gemm(lyap_ctx* ctx, const Seed& s, const double* Bop, double* U, int
   }
 }
 
+// persistent tcgen05 3xTF32 GEMM (umma.cuh), one CTA per SM over the active tiles; epi = k fuses the K1
+// epilogue (k = 1, 2, 4), epi = 0 writes U32t for k1_epi
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+template <int BN, int ST>
+void launch_umma(lyap_ctx* ctx, int epi, const CUtensorMap& ta, const CUtensorMap& tb, float* U32, int npad, int Nc,
+                 int Kd, const int* nactive, int cpa, const K1EpiArgs& ep, cudaStream_t st, int* tctr) {
+  const int tiles = (Nc / BN) * (npad / UM_BM);
+  const dim3 grid((unsigned)std::max(1, std::min(num_sms(), tiles)));
+  constexpr int SM = UmCfg<BN, ST>::SMEM;
+  switch (epi) {
+    case 1:
+      k1_umma_persistent<BN, ST, 1><<<grid, 192, SM, st>>>(ta, tb, U32, npad, Nc, Kd, nactive, cpa, ep, tctr);
+      break;
+    case 2:
+      k1_umma_persistent<BN, ST, 2><<<grid, 192, SM, st>>>(ta, tb, U32, npad, Nc, Kd, nactive, cpa, ep, tctr);
+      break;
+    case 4:
+      k1_umma_persistent<BN, ST, 4><<<grid, 192, SM, st>>>(ta, tb, U32, npad, Nc, Kd, nactive, cpa, ep, tctr);
+      break;
+    default:
+      k1_umma_persistent<BN, ST, 0><<<grid, 192, SM, st>>>(ta, tb, U32, npad, Nc, Kd, nactive, cpa, ep, tctr);
+  }
+  LAUNCHED();
+}
+template <int BN, int ST>
+void set_umma_attrs(lyap_ctx* ctx) {
+  constexpr int SM = UmCfg<BN, ST>::SMEM;
+  CK(cudaFuncSetAttribute(k1_umma_persistent<BN, ST, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM));
+  CK(cudaFuncSetAttribute(k1_umma_persistent<BN, ST, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM));
+  CK(cudaFuncSetAttribute(k1_umma_persistent<BN, ST, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM));
+  CK(cudaFuncSetAttribute(k1_umma_persistent<BN, ST, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM));
+}
+
 void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, cudaEvent_t evb = nullptr, cudaEvent_t eve = nullptr,
                unsigned evflags = 0, int group = 0, int mp = 0) {
   const Seed& s = ctx->seed;
@@ -365,6 +452,14 @@ void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, cudaEvent_t evb 
   g.U += (size_t)group * s.npad * g.ncol;
   const int two_np = (int)(2 * s.npairs);
   const bool fuse = k1_fused(s.k, s.n, mp);
+  // mixed precision with the tcgen05 kernel and k = 1, 2, 4: both GEMMs carry the K1 epilogue (the
+  // DMMA one for the VERIFY positions, the tcgen05 one for the ITER positions), k1_epi is not launched
+  const bool fuse_mp = mp == 1 && mp_umma() && s.npad % UM_BM == 0 && (s.k == 1 || s.k == 2 || s.k == 4);
+  static const int fmask = [] {  // LYAP_MP_FUSE (diagnostics): bit 0 tcgen05 epilogue, bit 1 DMMA epilogue
+    const char* ev = std::getenv("LYAP_MP_FUSE");
+    return ev ? std::atoi(ev) : 3;
+  }();
+  const bool fuse_um = fuse_mp && (fmask & 1), fuse_dm = fuse_mp && (fmask & 2);
   float* B32 = mp ? g.Bop32 + (size_t)group * 2 * s.npad * g.ncol : nullptr;
   float* U32 = mp ? g.U32 + (size_t)group * s.npad * g.ncol : nullptr;
   K_DISPATCH(s.k, {
@@ -393,45 +488,71 @@ void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, cudaEvent_t evb 
       CK(cudaEventCreateWithFlags(&ctx->mpfork[group], cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&ctx->mpjoin[group], cudaEventDisableTiming));
     }
-    cudaStream_t ss = ctx->mpstream[group];
+    static const bool serial = std::getenv("LYAP_MP_SERIAL") != nullptr;  // diagnostics: no side stream
+    cudaStream_t ss = serial ? st : ctx->mpstream[group];
     CK(cudaEventRecord(ctx->mpfork[group], st));
     CK(cudaStreamWaitEvent(ss, ctx->mpfork[group], 0));
     K1Args av = a;
     av.nactive = a.nver;
-    launch_gemm<S_BM, S_BN, S_WM, S_WN, S_ST, S_BK>(ctx, s, g.Bop, g.U, g.ncol, av, ss, false);
+    launch_gemm<S_BM, S_BN, S_WM, S_WN, S_ST, S_BK>(ctx, s, g.Bop, g.U, g.ncol, av, ss, fuse_dm);
     LAUNCHED();
     CK(cudaEventRecord(ctx->mpjoin[group], ss));
-    cublasHandle_t hb = ctx->cublas_eng[group];
-    CKB(cublasSetStream(hb, st));
     const int Nc = (int)g.ncol, M = (int)s.npad;
-    const int Kd = (int)std::min<int64_t>(roundup(s.n, 16), s.npad);  // zero rows skipped
-    const float one = 1.f, zero = 0.f;
     const float* A32 = ctx->basis->Lf32;  // row-major npad x 2 npad: [hi | lo]
-    const float* Bhi = B32 + (size_t)s.npad * g.ncol;
-    // row-major U32 = A B is column-major U32^T = B^T A^T (m = columns, n = rows)
-    if (mp == 1) {
-      // U32 = A_hi B_lo + A_lo B_hi (one GEMM over the stacked K), then U32 += A_hi B_hi
-      CKB(cublasGemmEx(hb, CUBLAS_OP_N, CUBLAS_OP_N, Nc, M, Kd, &one, B32, CUDA_R_32F, Nc, A32, CUDA_R_32F,
-                       (int)(2 * s.npad), &zero, U32, CUDA_R_32F, Nc, CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT));
-      CKB(cublasGemmEx(hb, CUBLAS_OP_N, CUBLAS_OP_N, Nc, M, Kd, &one, Bhi, CUDA_R_32F, Nc, A32 + s.npad, CUDA_R_32F,
-                       (int)(2 * s.npad), &one, U32, CUDA_R_32F, Nc, CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT));
-      CKB(cublasGemmEx(hb, CUBLAS_OP_N, CUBLAS_OP_N, Nc, M, Kd, &one, Bhi, CUDA_R_32F, Nc, A32, CUDA_R_32F,
-                       (int)(2 * s.npad), &one, U32, CUDA_R_32F, Nc, CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT));
+    if (mp == 1 && mp_umma() && s.npad % UM_BM == 0) {
+      // tcgen05 3xTF32 GEMM (umma.cuh): U32t = A_hi B_lo + A_lo B_hi + A_hi B_hi in one TMEM accumulator
+      if (ctx->um_ta_ptr != A32) {
+        ctx->um_ta = make_tmap_f32(ctx, A32, 2 * (uint64_t)s.npad, (uint64_t)s.npad, UM_BK, UM_BM);
+        ctx->um_ta_ptr = A32;
+      }
+      if (ctx->um_tb_ptr[group] != B32 || ctx->um_tb_ncol[group] != g.ncol) {
+        ctx->um_tb[group] = make_tmap_f32(ctx, B32, (uint64_t)s.npad, 2 * (uint64_t)g.ncol, UM_BK, (uint32_t)um_bn());
+        ctx->um_tb_ptr[group] = B32;
+        ctx->um_tb_ncol[group] = g.ncol;
+      }
+      const int Kd = (int)std::min<int64_t>(roundup(s.n, UM_BK), s.npad);  // zero rows skipped
+      K1EpiArgs ep{a, s.btl, s.F, s.g0, (int)s.npad, two_np, (int)s.npairs, (int)s.n};
+      const int cpa = (int)(s.k * s.k), epi = fuse_um ? (int)s.k : 0;
+      if (um_bn() == 128)
+        launch_umma<128, 3>(ctx, epi, ctx->um_ta, ctx->um_tb[group], U32, (int)s.npad, Nc, Kd, a.nactive, cpa, ep, st,
+                            g.umctr + 2 * group);
+      else
+        launch_umma<UM_BN, UM_STAGES>(ctx, epi, ctx->um_ta, ctx->um_tb[group], U32, (int)s.npad, Nc, Kd, a.nactive, cpa,
+                                      ep, st, g.umctr + 2 * group);
     } else {
-      CKB(cublasGemmEx(hb, CUBLAS_OP_N, CUBLAS_OP_N, Nc, M, Kd, &one, Bhi, CUDA_R_32F, Nc, A32, CUDA_R_32F,
-                       (int)(2 * s.npad), &zero, U32, CUDA_R_32F, Nc, mp_compute(mp), CUBLAS_GEMM_DEFAULT));
+      cublasHandle_t hb = ctx->cublas_eng[group];
+      CKB(cublasSetStream(hb, st));
+      const int Kd = (int)std::min<int64_t>(roundup(s.n, 16), s.npad);  // zero rows skipped
+      const float one = 1.f, zero = 0.f;
+      const float* Bhi = B32 + (size_t)s.npad * g.ncol;
+      // column-major U32t (M x Nc, ld npad) = op(A32^T) B32t, B32t K-major (ld npad)
+      if (mp == 1) {
+        CKB(cublasGemmEx(hb, CUBLAS_OP_T, CUBLAS_OP_N, M, Nc, Kd, &one, A32, CUDA_R_32F, (int)(2 * s.npad), B32,
+                         CUDA_R_32F, (int)s.npad, &zero, U32, CUDA_R_32F, M, CUBLAS_COMPUTE_32F_FAST_TF32,
+                         CUBLAS_GEMM_DEFAULT));
+        CKB(cublasGemmEx(hb, CUBLAS_OP_T, CUBLAS_OP_N, M, Nc, Kd, &one, A32 + s.npad, CUDA_R_32F, (int)(2 * s.npad), Bhi,
+                         CUDA_R_32F, (int)s.npad, &one, U32, CUDA_R_32F, M, CUBLAS_COMPUTE_32F_FAST_TF32,
+                         CUBLAS_GEMM_DEFAULT));
+        CKB(cublasGemmEx(hb, CUBLAS_OP_T, CUBLAS_OP_N, M, Nc, Kd, &one, A32, CUDA_R_32F, (int)(2 * s.npad), Bhi,
+                         CUDA_R_32F, (int)s.npad, &one, U32, CUDA_R_32F, M, CUBLAS_COMPUTE_32F_FAST_TF32,
+                         CUBLAS_GEMM_DEFAULT));
+      } else {
+        CKB(cublasGemmEx(hb, CUBLAS_OP_T, CUBLAS_OP_N, M, Nc, Kd, &one, A32, CUDA_R_32F, (int)(2 * s.npad), Bhi,
+                         CUDA_R_32F, (int)s.npad, &zero, U32, CUDA_R_32F, M, mp_compute(mp), CUBLAS_GEMM_DEFAULT));
+      }
     }
     CK(cudaStreamWaitEvent(st, ctx->mpjoin[group], 0));
   }
   if (eve) CK(cudaEventRecordWithFlags(eve, st, evflags));
-  if (mp) {
+  if (mp && !(fuse_um && fuse_dm)) {
+    const int which = fuse_um ? 1 : (fuse_dm ? 2 : 0);
     K_DISPATCH(s.k, {
       dim3 grid((unsigned)(s.npad / K1_TILE_C), (unsigned)((a.nslot + K1Tile<KK>::TS - 1) / K1Tile<KK>::TS));
       k1_epi<KK, true><<<grid, K1_THREADS, 0, st>>>(a, g.U, g.ncol, s.btl, s.F, s.g0, (int)s.npad, two_np,
-                                                    (int)s.npairs, (int)s.n, U32);
+                                                    (int)s.npairs, (int)s.n, U32, which);
     });
     LAUNCHED();
-  } else if (!fuse) {
+  } else if (!mp && !fuse) {
     K_DISPATCH(s.k, {
       dim3 grid((unsigned)(s.npad / K1_TILE_C), (unsigned)((a.nslot + K1Tile<KK>::TS - 1) / K1Tile<KK>::TS));
       k1_epi<KK><<<grid, K1_THREADS, 0, st>>>(a, g.U, g.ncol, s.btl, s.F, s.g0, (int)s.npad, two_np, (int)s.npairs,
@@ -1224,6 +1345,8 @@ static int setup_core(int64_t n, int64_t k, const double* A0, const double* Bl, 
     CKS(cusolverDnSetStream(ctx->cusolver, ctx->stream));
     set_smem_attrs<G_BM, G_BN, G_WM, G_WN, G_ST, G_BK>(ctx);
     set_smem_attrs<S_BM, S_BN, S_WM, S_WN, S_ST, S_BK>(ctx);
+    set_umma_attrs<UM_BN, UM_STAGES>(ctx);
+    set_umma_attrs<128, 3>(ctx);
     cudaStream_t st = ctx->stream;
     CK(cudaEventRecord(ctx->ev0, st));
     Seed& s = ctx->seed;
@@ -2178,6 +2301,7 @@ int lyap_apply_C(lyap_ctx* ctx, int64_t nvec, const double* X, const double* sig
       launch_k1(ctx, a, st);
       ctx->stats.k1_launches++;
       ctx->stats.k1_vectors += nb;
+      ctx->stats.k1_exact_vectors += nb;
       ctx->stats.k1_flops += 2.0 * (double)ctx->seed.n * ctx->seed.n * ctx->seed.k * ctx->seed.k * nb;
     }
   } catch (Fail f) {

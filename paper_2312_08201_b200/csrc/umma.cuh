@@ -1,0 +1,380 @@
+// K1 inner GEMM on the 5th-generation tensor cores (tcgen05, TMEM accumulators, TMA operand staging):
+// the FP32-accurate T-apply of the mixed-precision Krylov steps.
+//
+//   U32t[n][m] = sum_k Lf[m][k] * Bop[k][n]      (the dense Cauchy coupling of eqs. (N2M1)/(N1M2),
+//                                                 PAPER.md:336-362, for every ITER slot's vector)
+//
+// evaluated as 3xTF32: with x = x_hi + x_lo (x_hi = x rounded to TF32, x_lo = x - x_hi, both stored
+// as float planes by k_split_Lf / k1_gen), A B ~ A_hi B_lo + A_lo B_hi + A_hi B_hi, all three
+// products accumulated in one FP32 TMEM accumulator (relative error ~1e-6 instead of TF32's ~1e-3).
+//
+// Layouts (all K-major, so both operands use the canonical 128-byte-swizzled K-major UMMA layout):
+//   A32 : npad x 2 npad fp32 row-major, row m = [hi(m, 0..npad) | lo(m, 0..npad)]
+//   B32t: 2 ncol x npad fp32 row-major, rows [0, ncol) lo planes, [ncol, 2 ncol) hi planes (row = GEMM
+//         column n, contiguous along k)
+//   U32t: ncol x npad fp32 row-major (column n of the product contiguous along m: coalesced epilogue)
+// Tile 128 (m) x 256 (n) x 32 (k), one CTA per tile, 4 warps: warp 0 lane 0 issues the TMA loads, warp 1
+// lane 0 issues the MMAs (12 tcgen05.mma.kind::tf32 of 128x256x8 per k-block), then all four warps drain
+// TMEM (warp w owns TMEM lanes 32w..32w+31 = rows m0 + 32w + lane).
+#pragma once
+#include <cuda.h>
+#include <cstdint>
+
+#include "k1.cuh"
+
+namespace lyap {
+
+constexpr int UM_BM = 128, UM_BK = 32;
+constexpr int UM_A_BYTES = UM_BM * UM_BK * 4;  // one A plane per stage: 16 KB
+// BN: GEMM columns per CTA (one tcgen05.mma N), STAGES: TMA pipeline depth
+template <int BN, int STAGES>
+struct UmCfg {
+  static constexpr int B_BYTES = BN * UM_BK * 4;                       // one B plane per stage
+  static constexpr int STAGE_BYTES = 2 * UM_A_BYTES + 2 * B_BYTES;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;       // + alignment slack + barriers
+  static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  // instruction descriptor: D fp32, A/B tf32, both K-major, M = 128, N = BN
+  static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                    ((uint32_t)(UM_BM >> 4) << 24);
+};
+constexpr int UM_BN = 256, UM_STAGES = 2;  // production configuration (tools/microbench/umma_tf32x3.cu)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+// UMMA shared-memory matrix descriptor, K-major, 128-byte swizzle: rows of 128 B, 8-row atoms 1024 B apart
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);        // start address
+  d |= (uint64_t)1 << 16;                        // leading byte offset (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;              // stride byte offset: next 8-row atom
+  d |= (uint64_t)1 << 46;                        // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                        // layout: SWIZZLE_128B
+  return d;
+}
+template <uint32_t IDESC>
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+// U32t = A32 (3xTF32) B32t over the active columns (n0 < (*nactive) * cpa; nactive null: all).
+// grid: (ncol / BN) x (npad / 128); Kd = multiple of 32 (zero rows of the padding skipped).
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(128, 1)
+    k1_umma_tf32x3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   float* __restrict__ U32t, int npad, int ncol, int Kd, const int* __restrict__ nactive, int cpa) {
+  using Cfg = UmCfg<BN, STAGES>;
+  constexpr int UM_STAGE_BYTES = Cfg::STAGE_BYTES, UM_B_BYTES = Cfg::B_BYTES, UM_TMEM_COLS = Cfg::TMEM_COLS;
+  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * UM_BM;
+  if (nactive && n0 >= (*nactive) * cpa) return;
+  extern __shared__ __align__(1024) uint8_t um_smem[];
+  // 1024-byte aligned operand stages (the 128-byte swizzle pattern repeats every 1024 B)
+  const uint32_t base = (smem_u32(um_smem) + 1023) & ~1023u;
+  uint8_t* gbase = um_smem + (base - smem_u32(um_smem));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(gbase + STAGES * UM_STAGE_BYTES);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 1);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES), accb = smem_u32(bars + 2 * STAGES);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    mbar_init(accb, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(UM_TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  const int KB = Kd / UM_BK;
+
+  if (warp == 0 && lane == 0) {
+    // TMA producer: per k-block A_hi, A_lo (x = k, npad + k; y = m0), B_lo, B_hi (x = k; y = n0, ncol + n0)
+    for (int kb = 0; kb < KB; ++kb) {
+      const int s = kb % STAGES;
+      if (kb >= STAGES) mbar_wait(empty0 + 8 * s, ((kb / STAGES) - 1) & 1);
+      const uint32_t st = base + s * UM_STAGE_BYTES, fb = full0 + 8 * s;
+      mbar_expect_tx(fb, UM_STAGE_BYTES);
+      const int k = kb * UM_BK;
+      tma_load_2d(st, &tmA, fb, k, m0);
+      tma_load_2d(st + UM_A_BYTES, &tmA, fb, npad + k, m0);
+      tma_load_2d(st + 2 * UM_A_BYTES, &tmB, fb, k, n0);
+      tma_load_2d(st + 2 * UM_A_BYTES + UM_B_BYTES, &tmB, fb, k, ncol + n0);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // MMA issuer: 3 products x 4 k-steps of 8 per k-block into one accumulator
+    for (int kb = 0; kb < KB; ++kb) {
+      const int s = kb % STAGES;
+      mbar_wait(full0 + 8 * s, (kb / STAGES) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t ah = base + s * UM_STAGE_BYTES, al = ah + UM_A_BYTES, bl = ah + 2 * UM_A_BYTES,
+                     bh = bl + UM_B_BYTES;
+#pragma unroll
+      for (int j = 0; j < UM_BK / 8; ++j) {
+        const uint32_t o = 32 * j;  // 8 tf32 = 32 bytes along the swizzled 128-byte row
+        const uint32_t acc0 = (kb > 0 || j > 0) ? 1u : 0u;
+        umma_tf32<Cfg::IDESC>(tmem, umma_desc_sw128(ah + o), umma_desc_sw128(bl + o), acc0);
+        umma_tf32<Cfg::IDESC>(tmem, umma_desc_sw128(al + o), umma_desc_sw128(bh + o), 1u);
+        umma_tf32<Cfg::IDESC>(tmem, umma_desc_sw128(ah + o), umma_desc_sw128(bh + o), 1u);
+      }
+      umma_commit(empty0 + 8 * s);  // frees the stage once these MMAs have read it
+    }
+    umma_commit(accb);  // accumulator complete
+  }
+  __syncwarp();
+  // epilogue: TMEM lane (32 warp + lane) = row m0 + 32 warp + lane; 32 columns per tcgen05.ld
+  mbar_wait(accb, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const int m = m0 + 32 * warp + lane;
+#pragma unroll 1
+  for (int c0 = 0; c0 < BN; c0 += 32) {
+    uint32_t r[32];
+    const uint32_t taddr = tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)c0;
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < 32; ++j) U32t[(int64_t)(n0 + c0 + j) * npad + m] = __uint_as_float(r[j]);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(UM_TMEM_COLS));
+  }
+}
+
+
+// ------------------------------------------------------------------------------------------------
+// Persistent, warp-specialised form (the engine's kernel): grid = one CTA per SM; tiles (M-tile fastest,
+// only the tiles that hold active columns) are claimed dynamically from a global counter (tctr[0]; the
+// last CTA to run dry resets it), so CTAs that start late -- the other slot group's kernels hold some
+// SMs -- simply take fewer tiles.  The producer publishes each claimed tile id through a 4-deep shared
+// ring (tid_full / tid_empty mbarriers) to the MMA thread and the epilogue warps.  6 warps:
+//   warp 0 lane 0: TMA producer over a STAGES-deep shared-memory ring (full / empty mbarriers)
+//   warp 1       : TMEM allocation (2 accumulators of BN columns); lane 0 issues the MMAs
+//   warps 2..5   : epilogue, warp w draining TMEM lanes 32 (w % 4) .. +31 (the lane quarter a warp may
+//                  access), overlapped with the next tile's main loop (accumulator double buffer:
+//                  tfull / tempty mbarriers)
+// EPI = k (1, 2, 4): the K1 epilogue is fused -- each thread holds row m (coordinate c) of 32
+// consecutive GEMM columns = whole (slot, s, t) groups, contracts them with B~l, adds T_d and sigma x
+// (k1_out_element, the same code as the DMMA path's fused epilogue) and writes C(v)x straight into the
+// slot's Krylov basis; the Im row of a conjugate pair comes from the neighbouring lane (shfl).  VERIFY
+// positions [0, nver) are skipped (their exact FP64 apply comes from the DMMA GEMM).  EPI = 0: U32t.
+template <int BN, int STAGES, int EPI>
+__global__ void __launch_bounds__(192, 1)
+    k1_umma_persistent(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                       float* __restrict__ U32t, int npad, int ncol, int Kd, const int* __restrict__ nactive, int cpa,
+                       const K1EpiArgs ep, int* __restrict__ tctr) {
+  using Cfg = UmCfg<BN, STAGES>;
+  constexpr int SB = Cfg::STAGE_BYTES, BB = Cfg::B_BYTES, TCOLS = 2 * BN <= 256 ? 256 : 512;
+  extern __shared__ __align__(1024) uint8_t um_smem[];
+  const uint32_t base = (smem_u32(um_smem) + 1023) & ~1023u;
+  uint8_t* gbase = um_smem + (base - smem_u32(um_smem));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(gbase + STAGES * SB);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 12);
+  int* tile_ring = reinterpret_cast<int*>(bars + 2 * STAGES + 13);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES);
+  const uint32_t tfull0 = smem_u32(bars + 2 * STAGES), tempty0 = smem_u32(bars + 2 * STAGES + 2);
+  const uint32_t rfull0 = smem_u32(bars + 2 * STAGES + 4), rempty0 = smem_u32(bars + 2 * STAGES + 8);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int MT = npad / UM_BM;
+  const int ncols_act = nactive ? min(ncol, (*nactive) * cpa) : ncol;
+  const int ntiles = ((ncols_act + BN - 1) / BN) * MT;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull0 + 8 * a, 1);
+      mbar_init(tempty0 + 8 * a, 128);
+    }
+    for (int r = 0; r < 4; ++r) {
+      mbar_init(rfull0 + 8 * r, 1);
+      mbar_init(rempty0 + 8 * r, 129);  // the MMA thread + 128 epilogue threads
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  const int KB = Kd / UM_BK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;
+      for (int li = 0;; ++li) {
+        const int rs = li & 3;
+        if (li >= 4) mbar_wait(rempty0 + 8 * rs, ((li >> 2) - 1) & 1);
+        const int t = atomicAdd(tctr, 1);
+        tile_ring[rs] = t;
+        mbar_arrive(rfull0 + 8 * rs);
+        if (t >= ntiles) {
+          if (atomicAdd(tctr + 1, 1) == (int)gridDim.x - 1) {  // every CTA has run dry: reset for the next launch
+            tctr[0] = 0;
+            tctr[1] = 0;
+          }
+          break;
+        }
+        const int m0 = (t % MT) * UM_BM, n0 = (t / MT) * BN;
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(empty0 + 8 * s, ((it / STAGES) & 1) ^ 1);
+          const uint32_t st = base + s * SB, fb = full0 + 8 * s;
+          mbar_expect_tx(fb, SB);
+          const int k = kb * UM_BK;
+          tma_load_2d(st, &tmA, fb, k, m0);
+          tma_load_2d(st + UM_A_BYTES, &tmA, fb, npad + k, m0);
+          tma_load_2d(st + 2 * UM_A_BYTES, &tmB, fb, k, n0);
+          tma_load_2d(st + 2 * UM_A_BYTES + BB, &tmB, fb, k, ncol + n0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int it = 0;
+      for (int li = 0;; ++li) {
+        mbar_wait(rfull0 + 8 * (li & 3), (li >> 2) & 1);
+        const int t = tile_ring[li & 3];
+        mbar_arrive(rempty0 + 8 * (li & 3));
+        if (t >= ntiles) break;
+        const int acc = li & 1;
+        const uint32_t td = tmem + (uint32_t)(acc * BN);
+        mbar_wait(tempty0 + 8 * acc, ((li >> 1) & 1) ^ 1);  // the epilogue has drained this accumulator
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(full0 + 8 * s, (it / STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t ah = base + s * SB, al = ah + UM_A_BYTES, bl = ah + 2 * UM_A_BYTES, bh = bl + BB;
+#pragma unroll
+          for (int j = 0; j < UM_BK / 8; ++j) {
+            const uint32_t o = 32 * j;
+            umma_tf32<Cfg::IDESC>(td, umma_desc_sw128(ah + o), umma_desc_sw128(bl + o), (kb > 0 || j > 0) ? 1u : 0u);
+            umma_tf32<Cfg::IDESC>(td, umma_desc_sw128(al + o), umma_desc_sw128(bh + o), 1u);
+            umma_tf32<Cfg::IDESC>(td, umma_desc_sw128(ah + o), umma_desc_sw128(bh + o), 1u);
+          }
+          umma_commit(empty0 + 8 * s);
+        }
+        umma_commit(tfull0 + 8 * acc);
+      }
+    }
+  } else {
+    // epilogue warps 2..5
+    const int q = warp & 3;  // TMEM lane quarter
+    const int nver = EPI ? *ep.a.nver : 0;
+    const int nact = EPI ? k1_nact(ep.a) : 0;
+    for (int li = 0;; ++li) {
+      mbar_wait(rfull0 + 8 * (li & 3), (li >> 2) & 1);
+      const int t = tile_ring[li & 3];
+      mbar_arrive(rempty0 + 8 * (li & 3));
+      if (t >= ntiles) break;
+      const int m0 = (t % MT) * UM_BM, n0 = (t / MT) * BN;
+      const int acc = li & 1;
+      mbar_wait(tfull0 + 8 * acc, (li >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int m = m0 + 32 * q + lane;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN + c0);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+            "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+              "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+              "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if constexpr (EPI == 0) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) U32t[(int64_t)(n0 + c0 + j) * npad + m] = __uint_as_float(r[j]);
+        } else {
+          constexpr int KK = EPI * EPI, PP = 32 / KK;
+          static_assert(32 % KK == 0, "whole (slot, s, t) groups per 32-column chunk");
+#pragma unroll
+          for (int pp = 0; pp < PP; ++pp) {
+            double u[KK], u1[KK];
+#pragma unroll
+            for (int j = 0; j < KK; ++j) {
+              u[j] = (double)__uint_as_float(r[pp * KK + j]);
+              u1[j] = __shfl_down_sync(0xffffffffu, u[j], 1);  // row m + 1: the Im row of a pair
+            }
+            const int pos = (n0 + c0) / KK + pp;
+            if (pos < nver || pos >= nact) continue;  // VERIFY (exact path) or inactive
+            const int slot = k1_slot(ep.a, pos);
+#pragma unroll
+            for (int s = 0; s < EPI; ++s) k1_out_element<EPI>(ep, slot, s, m, u + s * EPI, u1 + s * EPI, 0);
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(tempty0 + 8 * acc);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TCOLS));
+  }
+}
+
+}  // namespace lyap

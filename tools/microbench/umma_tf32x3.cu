@@ -1,0 +1,206 @@
+// Standalone check + timing of the tcgen05 3xTF32 K1 GEMM (paper_2312_08201_b200/csrc/umma.cuh)
+// against an FP64 reference on sampled entries, and against three cuBLAS TF32 GEMMs.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo umma_tf32x3.cu -lcublas -o umma_tf32x3
+// ./umma_tf32x3 [npad] [ncol] [Kd]
+#include <cublas_v2.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <random>
+#include <vector>
+
+#include "../../paper_2312_08201_b200/csrc/umma.cuh"
+
+#define CK(x)                                                                            \
+  do {                                                                                   \
+    cudaError_t e = (x);                                                                 \
+    if (e != cudaSuccess) {                                                              \
+      printf("CUDA error %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__);     \
+      exit(1);                                                                           \
+    }                                                                                    \
+  } while (0)
+
+static float tf32_host(float f) {
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  u = (u + 0x1000u) & 0xFFFFE000u;
+  float r;
+  memcpy(&r, &u, 4);
+  return r;
+}
+
+static CUtensorMap tmap(const float* p, uint64_t inner, uint64_t outer, uint32_t bi, uint32_t bo) {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+    fn = (PFN_cuTensorMapEncodeTiled_v12000)f;
+  }
+  CUtensorMap m;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 4};
+  cuuint32_t box[2] = {bi, bo};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)p, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    printf("cuTensorMapEncodeTiled failed %d\n", (int)r);
+    exit(1);
+  }
+  return m;
+}
+
+int main(int argc, char** argv) {
+  const int npad = argc > 1 ? atoi(argv[1]) : 4096;
+  const int ncol = argc > 2 ? atoi(argv[2]) : 4864;
+  const int Kd = argc > 3 ? atoi(argv[3]) : 4000;
+  std::mt19937_64 rng(1);
+  std::normal_distribution<double> nd;
+  std::vector<double> A((size_t)npad * npad, 0.0), B((size_t)npad * ncol, 0.0);  // A[m][k], B[k][n]
+  for (int m = 0; m < npad; ++m)
+    for (int k = 0; k < Kd; ++k) A[(size_t)m * npad + k] = nd(rng) / (1.0 + std::abs(m - k));
+  for (int k = 0; k < Kd; ++k)
+    for (int n = 0; n < ncol; ++n) B[(size_t)k * ncol + n] = nd(rng);
+  std::vector<float> A32((size_t)npad * 2 * npad), B32((size_t)2 * ncol * npad, 0.f);
+  for (int m = 0; m < npad; ++m)
+    for (int k = 0; k < npad; ++k) {
+      const double x = A[(size_t)m * npad + k];
+      const float hi = tf32_host((float)x);
+      A32[(size_t)m * 2 * npad + k] = hi;
+      A32[(size_t)m * 2 * npad + npad + k] = (float)(x - (double)hi);
+    }
+  for (int k = 0; k < npad; ++k)
+    for (int n = 0; n < ncol; ++n) {
+      const double x = B[(size_t)k * ncol + n];
+      const float hi = tf32_host((float)x);
+      B32[(size_t)(ncol + n) * npad + k] = hi;
+      B32[(size_t)n * npad + k] = (float)(x - (double)hi);
+    }
+  float *dA, *dB, *dU, *dU2;
+  CK(cudaMalloc(&dA, A32.size() * 4));
+  CK(cudaMalloc(&dB, B32.size() * 4));
+  CK(cudaMalloc(&dU, (size_t)ncol * npad * 4));
+  CK(cudaMalloc(&dU2, (size_t)ncol * npad * 4));
+  CK(cudaMemcpy(dA, A32.data(), A32.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dB, B32.data(), B32.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemset(dU, 0, (size_t)ncol * npad * 4));
+  const int Kr = (Kd + 31) / 32 * 32;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int R = 10;
+  float ms;
+  const double fl = 3.0 * 2.0 * npad * (double)ncol * Kr;
+  std::vector<float> U((size_t)ncol * npad);
+  CUtensorMap ta = tmap(dA, 2 * (uint64_t)npad, npad, lyap::UM_BK, lyap::UM_BM);
+  auto variant = [&](auto kern, int BN, int smem, const char* name) {
+    if (ncol % BN) return;
+    CUtensorMap tb = tmap(dB, npad, 2 * (uint64_t)ncol, lyap::UM_BK, BN);
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    dim3 grid(ncol / BN, npad / lyap::UM_BM);
+    CK(cudaMemset(dU, 0, (size_t)ncol * npad * 4));
+    kern<<<grid, 128, smem>>>(ta, tb, dU, npad, ncol, Kr, nullptr, 1);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(U.data(), dU, U.size() * 4, cudaMemcpyDeviceToHost));
+    double maxrel = 0;
+    std::mt19937_64 r2(5);
+    std::uniform_int_distribution<int> um(0, npad - 1), un(0, ncol - 1);
+    for (int t = 0; t < 2000; ++t) {
+      const int m = um(r2), n = un(r2);
+      double ref = 0, mag = 0;
+      for (int k = 0; k < Kd; ++k) {
+        ref += A[(size_t)m * npad + k] * B[(size_t)k * ncol + n];
+        mag += std::abs(A[(size_t)m * npad + k] * B[(size_t)k * ncol + n]);
+      }
+      maxrel = std::max(maxrel, std::abs(U[(size_t)n * npad + m] - ref) / mag);
+    }
+    cudaEventRecord(e0);
+    for (int r = 0; r < R; ++r) kern<<<grid, 128, smem>>>(ta, tb, dU, npad, ncol, Kr, nullptr, 1);
+    cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1));
+    cudaEventElapsedTime(&ms, e0, e1);
+    ms /= R;
+    printf("umma %-10s: err/sum|ab| %.2e  %.3f ms  %.1f TFLOP/s (3 passes)\n", name, maxrel, ms, fl / ms * 1e-9);
+  };
+  variant(lyap::k1_umma_tf32x3<256, 2>, 256, lyap::UmCfg<256, 2>::SMEM, "256x2");
+  variant(lyap::k1_umma_tf32x3<128, 3>, 128, lyap::UmCfg<128, 3>::SMEM, "128x3");
+  variant(lyap::k1_umma_tf32x3<128, 2>, 128, lyap::UmCfg<128, 2>::SMEM, "128x2");
+  variant(lyap::k1_umma_tf32x3<192, 2>, 192, lyap::UmCfg<192, 2>::SMEM, "192x2");
+  variant(lyap::k1_umma_tf32x3<64, 4>, 64, lyap::UmCfg<64, 4>::SMEM, "64x4");
+  variant(lyap::k1_umma_tf32x3<256, 2>, 256, lyap::UmCfg<256, 2>::SMEM, "256x2");
+  auto pvariant = [&](auto kern, int BN, int smem, const char* name) {
+    if (ncol % BN) return;
+    CUtensorMap tb = tmap(dB, npad, 2 * (uint64_t)ncol, lyap::UM_BK, BN);
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int nsm = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    const int tiles = (ncol / BN) * (npad / lyap::UM_BM);
+    dim3 grid(std::min(nsm, tiles));
+    CK(cudaMemset(dU, 0, (size_t)ncol * npad * 4));
+    lyap::K1EpiArgs ep{};
+    int* tctr = nullptr;
+    CK(cudaMalloc(&tctr, 8));
+    CK(cudaMemset(tctr, 0, 8));
+    kern<<<grid, 192, smem>>>(ta, tb, dU, npad, ncol, Kr, nullptr, 1, ep, tctr);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(U.data(), dU, U.size() * 4, cudaMemcpyDeviceToHost));
+    double maxrel = 0;
+    std::mt19937_64 r2(5);
+    std::uniform_int_distribution<int> um(0, npad - 1), un(0, ncol - 1);
+    for (int t = 0; t < 2000; ++t) {
+      const int m = um(r2), n = un(r2);
+      double ref = 0, mag = 0;
+      for (int k = 0; k < Kd; ++k) {
+        ref += A[(size_t)m * npad + k] * B[(size_t)k * ncol + n];
+        mag += std::abs(A[(size_t)m * npad + k] * B[(size_t)k * ncol + n]);
+      }
+      maxrel = std::max(maxrel, std::abs(U[(size_t)n * npad + m] - ref) / mag);
+    }
+    cudaEventRecord(e0);
+    for (int r = 0; r < R; ++r) kern<<<grid, 192, smem>>>(ta, tb, dU, npad, ncol, Kr, nullptr, 1, ep, tctr);
+    cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1));
+    cudaEventElapsedTime(&ms, e0, e1);
+    ms /= R;
+    printf("persistent %-10s: err/sum|ab| %.2e  %.3f ms  %.1f TFLOP/s (3 passes)\n", name, maxrel, ms, fl / ms * 1e-9);
+  };
+  pvariant(lyap::k1_umma_persistent<256, 2, 0>, 256, lyap::UmCfg<256, 2>::SMEM, "256x2");
+  pvariant(lyap::k1_umma_persistent<128, 3, 0>, 128, lyap::UmCfg<128, 3>::SMEM, "128x3");
+  // cuBLAS: three TF32 GEMMs (column-major C (npad x ncol, ld npad) = A^T(op T) * Bt)
+  cublasHandle_t h;
+  cublasCreate(&h);
+  const float one = 1.f, zero = 0.f;
+  auto cub = [&]() {
+    cublasGemmEx(h, CUBLAS_OP_T, CUBLAS_OP_N, npad, ncol, Kr, &one, dA, CUDA_R_32F, 2 * npad, dB, CUDA_R_32F, npad, &zero,
+                 dU2, CUDA_R_32F, npad, CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT);
+    cublasGemmEx(h, CUBLAS_OP_T, CUBLAS_OP_N, npad, ncol, Kr, &one, dA + npad, CUDA_R_32F, 2 * npad,
+                 dB + (size_t)ncol * npad, CUDA_R_32F, npad, &one, dU2, CUDA_R_32F, npad, CUBLAS_COMPUTE_32F_FAST_TF32,
+                 CUBLAS_GEMM_DEFAULT);
+    cublasGemmEx(h, CUBLAS_OP_T, CUBLAS_OP_N, npad, ncol, Kr, &one, dA, CUDA_R_32F, 2 * npad, dB + (size_t)ncol * npad,
+                 CUDA_R_32F, npad, &one, dU2, CUDA_R_32F, npad, CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT);
+  };
+  cub();
+  CK(cudaDeviceSynchronize());
+  cudaEventRecord(e0);
+  for (int r = 0; r < R; ++r) cub();
+  cudaEventRecord(e1);
+  CK(cudaEventSynchronize(e1));
+  cudaEventElapsedTime(&ms, e0, e1);
+  ms /= R;
+  printf("cublas 3 x tf32: %.3f ms  %.1f TFLOP/s (3 passes)\n", ms, fl / ms * 1e-9);
+  std::vector<float> U2((size_t)ncol * npad);
+  CK(cudaMemcpy(U2.data(), dU2, U2.size() * 4, cudaMemcpyDeviceToHost));
+  double d = 0, nrm = 0;
+  for (size_t i = 0; i < U.size(); ++i) {
+    d = std::max(d, (double)std::abs(U[i] - U2[i]));
+    nrm = std::max(nrm, (double)std::abs(U2[i]));
+  }
+  printf("last umma vs cublas: max diff %.3e (max |U| %.3e)\n", d, nrm);
+  return 0;
+}
