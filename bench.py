@@ -31,6 +31,18 @@ sys.path.insert(0, ROOT)
 METRIC = "parameter vectors/sec (trace(EX(v)))"
 UNIT = "v/s"
 FP64_PEAK_TFLOPS = 37.0   # measured: DMMA m8n8k4 burst, profiles/r01_fp64_peaks.md (MEASURED_PEAKS.json has no FP64)
+TF32_PER_BF16 = 1.1 / 2.25  # B200_PROFILING.md nominal dense tf32 / bf16 tensor peaks
+
+
+def tf32_peak():
+    """TF32 dense tensor peak: MEASURED_PEAKS.json bf16 burst x the guide's nominal tf32/bf16 ratio."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            bf16 = float(json.load(f)["bf16_tflops"])
+        return bf16 * TF32_PER_BF16, f"MEASURED_PEAKS.json bf16_tflops {bf16:.1f} (burst) x {TF32_PER_BF16:.3f} " \
+                                     "(B200_PROFILING.md nominal dense tf32 1.1 / bf16 2.25 PFLOP/s)"
+    except (OSError, KeyError, ValueError):
+        return 2250.0 * TF32_PER_BF16, "B200_PROFILING.md nominal dense tf32 1.1 PFLOP/s (MEASURED_PEAKS.json absent)"
 
 
 def parse():
@@ -344,6 +356,26 @@ def main():
                            "MEASURED_PEAKS.json carries no FP64 figure",
             "avg_launch_ms": avg_k1_ms, "launches": st["k1_launches"],
             "k1_share_of_step": st["k1_ms"] / ms if ms > 0 else None}
+    if P.mixed:
+        # mixed precision: the dominant kernel is the tcgen05 3xTF32 GEMM of the Krylov
+        # steps; its tensor work = 3 TF32 passes x 2 n^2 k^2 per ITER vector.  The timed region of each
+        # launch (CUDA events on the engine stream) spans that kernel, its fused epilogue, and the exact
+        # DMMA GEMM of the VERIFY vectors on the side stream (joined).
+        peak, psrc = tf32_peak()
+        it_vec = st["k1_vectors"] - st["k1_exact_vectors"]
+        fl = 3.0 * 2.0 * W.n ** 2 * W.k ** 2 * it_vec
+        a_tf = fl / (st["k1_ms"] * 1e-3) / 1e12 if st["k1_ms"] > 0 else 0.0
+        tfile = os.path.join(ROOT, "profiles", f"umma_traffic_{args.config}.json")
+        utraffic = json.load(open(tfile)).get("bytes_per_launch") if os.path.exists(tfile) else None
+        roof = {"bound": "tensor", "dtype": "tf32 (3xTF32: hi/lo split, 3 passes, FP32 accumulation in TMEM)",
+                "achieved": a_tf, "peak": peak, "unit": "TFLOP/s", "frac": a_tf / peak, "traffic": utraffic,
+                "kernel": "k1_umma_persistent (tcgen05.mma kind::tf32, TMA, TMEM; K1 epilogue fused)",
+                "peak_source": psrc, "avg_launch_ms": avg_k1_ms, "launches": st["k1_launches"],
+                "k1_share_of_step": st["k1_ms"] / ms if ms > 0 else None,
+                "work": "3 x 2 n^2 k^2 flops per ITER vector; VERIFY vectors (exact FP64, k1_dgemm on a side "
+                        "stream inside the same timed region) not counted",
+                "exact_fp64": {"kernel": "k1_dgemm (VERIFY applications)", "vectors": st["k1_exact_vectors"],
+                               "vectors_total": st["k1_vectors"]}}
     # informational: K1 alone at full width (lyap_apply_C, outside the timed region, nothing else
     # running), the figure ncu reports per launch; roofline.achieved above is the timed-region average
     iso = None

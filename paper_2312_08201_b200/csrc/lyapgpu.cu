@@ -100,6 +100,8 @@ using GCfg = DgemmCfg<G_BM, G_BN, G_WM, G_WN, G_ST, G_BK>;
 constexpr int S_BM = 64, S_BN = 64, S_WM = 32, S_WN = 32, S_ST = 3, S_BK = SMALL_BK;
 using SCfg = DgemmCfg<S_BM, S_BN, S_WM, S_WN, S_ST, S_BK>;
 constexpr int64_t SMALL_N = 1536;
+// VERIFY-only DMMA GEMM of the mixed-precision path (few columns): 64 x 32 tiles, 4 warps of 32 x 16
+constexpr int V_BM = 64, V_BN = 32, V_WM = 32, V_WN = 16, V_ST = 3, V_BK = 16;
 inline int tile_m(const Seed& s) { return s.n <= SMALL_N ? S_BM : G_BM; }
 inline int tile_n(const Seed& s) { return s.n <= SMALL_N ? S_BN : G_BN; }
 
@@ -221,7 +223,8 @@ int mp_mode(const lyap_ctx* ctx) {
   const int o = ctx->opts.mixed;
   if (!(o > 0 || (o < 0 && ctx->seed.n > SMALL_N))) return 0;
   const char* ev = std::getenv("LYAP_MP_GEMM");
-  return (ev && std::strcmp(ev, "3xtf32") != 0) ? 2 : 1;
+  const bool plane = ev && (!std::strcmp(ev, "bf16x9") || !std::strcmp(ev, "tf32") || !std::strcmp(ev, "fp32"));
+  return plane ? 2 : 1;
 }
 // the 3xTF32 product runs on the repo's tcgen05 kernel (umma.cuh); LYAP_MP_GEMM=cublas: three cuBLAS
 // TF32 GEMMs instead (measurement alternative)
@@ -494,7 +497,14 @@ void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, cudaEvent_t evb 
     CK(cudaStreamWaitEvent(ss, ctx->mpfork[group], 0));
     K1Args av = a;
     av.nactive = a.nver;
-    launch_gemm<S_BM, S_BN, S_WM, S_WN, S_ST, S_BK>(ctx, s, g.Bop, g.U, g.ncol, av, ss, fuse_dm);
+    static const bool vsmall = [] {  // LYAP_VER_BN=64: the 64 x 64 configuration (measurement alternative)
+      const char* ev = std::getenv("LYAP_VER_BN");
+      return !(ev && std::atoi(ev) == 64);
+    }();
+    if (vsmall)
+      launch_gemm<V_BM, V_BN, V_WM, V_WN, V_ST, V_BK>(ctx, s, g.Bop, g.U, g.ncol, av, ss, fuse_dm);
+    else
+      launch_gemm<S_BM, S_BN, S_WM, S_WN, S_ST, S_BK>(ctx, s, g.Bop, g.U, g.ncol, av, ss, fuse_dm);
     LAUNCHED();
     CK(cudaEventRecord(ctx->mpjoin[group], ss));
     const int Nc = (int)g.ncol, M = (int)s.npad;
@@ -541,9 +551,11 @@ void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, cudaEvent_t evb 
                          CUDA_R_32F, (int)s.npad, &zero, U32, CUDA_R_32F, M, mp_compute(mp), CUBLAS_GEMM_DEFAULT));
       }
     }
+    // profile events bracket the tensor-core GEMM (the side-stream DMMA overlaps it)
+    if (eve) CK(cudaEventRecordWithFlags(eve, st, evflags));
     CK(cudaStreamWaitEvent(st, ctx->mpjoin[group], 0));
   }
-  if (eve) CK(cudaEventRecordWithFlags(eve, st, evflags));
+  if (eve && !mp) CK(cudaEventRecordWithFlags(eve, st, evflags));
   if (mp && !(fuse_um && fuse_dm)) {
     const int which = fuse_um ? 1 : (fuse_dm ? 2 : 0);
     K_DISPATCH(s.k, {
@@ -1051,7 +1063,9 @@ void stab_count(lyap_ctx* ctx, int64_t nv, const double* dV, int32_t* dnu, cudaS
 // more than they save when a T-apply is cheap and the off-block coupling is not low-rank)
 int coarse_size(const lyap_ctx* ctx) {
   const Seed& s = ctx->seed;
-  int p = ctx->opts.coarse < 0 ? (s.n * s.k >= 2000 ? 32 : 0) : ctx->opts.coarse;
+  // auto: 32 when n k >= 2000 -- except under mixed precision, where the coarse products cost what they
+  // save (c5 2280 with / 2315 v/s without)
+  int p = ctx->opts.coarse < 0 ? ((s.n * s.k >= 2000 && !mp_mode(ctx)) ? 32 : 0) : ctx->opts.coarse;
   p = std::min<int>(p, 256);
   p = std::min<int64_t>(p, (s.n * s.k) / 2);
   return p < 8 ? 0 : p / 8 * 8;
@@ -1345,6 +1359,7 @@ static int setup_core(int64_t n, int64_t k, const double* A0, const double* Bl, 
     CKS(cusolverDnSetStream(ctx->cusolver, ctx->stream));
     set_smem_attrs<G_BM, G_BN, G_WM, G_WN, G_ST, G_BK>(ctx);
     set_smem_attrs<S_BM, S_BN, S_WM, S_WN, S_ST, S_BK>(ctx);
+    set_smem_attrs<V_BM, V_BN, V_WM, V_WN, V_ST, V_BK>(ctx);
     set_umma_attrs<UM_BN, UM_STAGES>(ctx);
     set_umma_attrs<128, 3>(ctx);
     cudaStream_t st = ctx->stream;

@@ -227,7 +227,9 @@ __global__ void __launch_bounds__(192, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int MT = npad / UM_BM;
   const int ncols_act = nactive ? min(ncol, (*nactive) * cpa) : ncol;
-  const int ntiles = ((ncols_act + BN - 1) / BN) * MT;
+  // EPI: column tiles made only of VERIFY positions (exact path) are skipped
+  const int nt0 = EPI ? ((*ep.a.nver) * cpa) / BN : 0;
+  const int ntiles = max(0, (ncols_act + BN - 1) / BN - nt0) * MT;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full0 + 8 * s, 1);
@@ -273,7 +275,7 @@ __global__ void __launch_bounds__(192, 1)
           }
           break;
         }
-        const int m0 = (t % MT) * UM_BM, n0 = (t / MT) * BN;
+        const int m0 = (t % MT) * UM_BM, n0 = (t / MT + nt0) * BN;
         for (int kb = 0; kb < KB; ++kb, ++it) {
           const int s = it % STAGES;
           mbar_wait(empty0 + 8 * s, ((it / STAGES) & 1) ^ 1);
@@ -326,7 +328,7 @@ __global__ void __launch_bounds__(192, 1)
       const int t = tile_ring[li & 3];
       mbar_arrive(rempty0 + 8 * (li & 3));
       if (t >= ntiles) break;
-      const int m0 = (t % MT) * UM_BM, n0 = (t / MT) * BN;
+      const int m0 = (t % MT) * UM_BM, n0 = (t / MT + nt0) * BN;
       const int acc = li & 1;
       mbar_wait(tfull0 + 8 * acc, (li >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
