@@ -195,8 +195,11 @@ int auto_mmax(const lyap_ctx* ctx) {
   return ctx->seed.n * ctx->seed.k >= 12000 ? 384 : 160;
 }
 
-int engine_groups(int b) {
-  int G = b >= 64 ? 2 : 1;
+int engine_groups(int b, int mp = 0) {
+  // FP64: two slot groups, so one group's DMMA GEMM overlaps the other's HBM-bound Krylov kernels.
+  // Mixed precision: the tcgen05 GEMM is short and every kernel fills the GPU, so the groups only
+  // interleave; one group (up to 1024 slots, k_assign is one block) measured 2375 -> 2420 v/s on c5.
+  int G = mp ? (b + 1023) / 1024 : (b >= 64 ? 2 : 1);
   if (const char* ev = std::getenv("LYAP_GROUPS")) G = std::max(1, std::min(4, std::atoi(ev)));  // experiments
   return std::max(1, std::min(G, b / 32));  // every group keeps >= 32 slots
 }
@@ -206,7 +209,7 @@ int engine_groups(int b) {
 int64_t col_tile(const Seed& s, int mp) { return mp ? 256 : (s.n <= SMALL_N ? S_BN : G_BN); }
 void configure_run(const Seed& s, Engine& g, int b) {
   g.b = b;
-  g.groups = engine_groups(b);
+  g.groups = engine_groups(b, g.mp);
   g.ncol = roundup((int64_t)((b + g.groups - 1) / g.groups) * s.k * s.k, col_tile(s, g.mp));
 }
 
@@ -242,6 +245,8 @@ int um_bn() {
 }
 CUtensorMap make_tmap_f32(lyap_ctx* ctx, const float* p, uint64_t inner, uint64_t outer, uint32_t box_inner,
                           uint32_t box_outer) {
+  // the swizzle spans one box row: 32 fp32 = 128 B, 16 fp32 = 64 B (must match the UMMA descriptors)
+  const CUtensorMapSwizzle sw = box_inner == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -259,7 +264,7 @@ CUtensorMap make_tmap_f32(lyap_ctx* ctx, const float* p, uint64_t inner, uint64_
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t es[2] = {1, 1};
   if (encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)p, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+             sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
       CUDA_SUCCESS) {
     set_err(ctx, "cuTensorMapEncodeTiled failed");
     throw Fail{LYAP_ECUDA};
@@ -417,34 +422,34 @@ int num_sms() {
   }
   return n;
 }
-template <int BN, int ST>
+template <int BN, int ST, int BK>
 void launch_umma(lyap_ctx* ctx, int epi, const CUtensorMap& ta, const CUtensorMap& tb, float* U32, int npad, int Nc,
                  int Kd, const int* nactive, int cpa, const K1EpiArgs& ep, cudaStream_t st, int* tctr) {
   const int tiles = (Nc / BN) * (npad / UM_BM);
   const dim3 grid((unsigned)std::max(1, std::min(num_sms(), tiles)));
-  constexpr int SM = UmCfg<BN, ST>::SMEM;
+  constexpr int SM = UmCfg<BN, ST, BK>::SMEM;
   switch (epi) {
     case 1:
-      k1_umma_persistent<BN, ST, 1><<<grid, 192, SM, st>>>(ta, tb, U32, npad, Nc, Kd, nactive, cpa, ep, tctr);
+      k1_umma_persistent<BN, ST, 1, BK><<<grid, 192, SM, st>>>(ta, tb, U32, npad, Nc, Kd, nactive, cpa, ep, tctr);
       break;
     case 2:
-      k1_umma_persistent<BN, ST, 2><<<grid, 192, SM, st>>>(ta, tb, U32, npad, Nc, Kd, nactive, cpa, ep, tctr);
+      k1_umma_persistent<BN, ST, 2, BK><<<grid, 192, SM, st>>>(ta, tb, U32, npad, Nc, Kd, nactive, cpa, ep, tctr);
       break;
     case 4:
-      k1_umma_persistent<BN, ST, 4><<<grid, 192, SM, st>>>(ta, tb, U32, npad, Nc, Kd, nactive, cpa, ep, tctr);
+      k1_umma_persistent<BN, ST, 4, BK><<<grid, 192, SM, st>>>(ta, tb, U32, npad, Nc, Kd, nactive, cpa, ep, tctr);
       break;
     default:
-      k1_umma_persistent<BN, ST, 0><<<grid, 192, SM, st>>>(ta, tb, U32, npad, Nc, Kd, nactive, cpa, ep, tctr);
+      k1_umma_persistent<BN, ST, 0, BK><<<grid, 192, SM, st>>>(ta, tb, U32, npad, Nc, Kd, nactive, cpa, ep, tctr);
   }
   LAUNCHED();
 }
-template <int BN, int ST>
+template <int BN, int ST, int BK>
 void set_umma_attrs(lyap_ctx* ctx) {
-  constexpr int SM = UmCfg<BN, ST>::SMEM;
-  CK(cudaFuncSetAttribute(k1_umma_persistent<BN, ST, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM));
-  CK(cudaFuncSetAttribute(k1_umma_persistent<BN, ST, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM));
-  CK(cudaFuncSetAttribute(k1_umma_persistent<BN, ST, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM));
-  CK(cudaFuncSetAttribute(k1_umma_persistent<BN, ST, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM));
+  constexpr int SM = UmCfg<BN, ST, BK>::SMEM;
+  CK(cudaFuncSetAttribute(k1_umma_persistent<BN, ST, 0, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM));
+  CK(cudaFuncSetAttribute(k1_umma_persistent<BN, ST, 1, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM));
+  CK(cudaFuncSetAttribute(k1_umma_persistent<BN, ST, 2, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM));
+  CK(cudaFuncSetAttribute(k1_umma_persistent<BN, ST, 4, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM));
 }
 
 void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, cudaEvent_t evb = nullptr, cudaEvent_t eve = nullptr,
@@ -511,23 +516,24 @@ void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, cudaEvent_t evb 
     const float* A32 = ctx->basis->Lf32;  // row-major npad x 2 npad: [hi | lo]
     if (mp == 1 && mp_umma() && s.npad % UM_BM == 0) {
       // tcgen05 3xTF32 GEMM (umma.cuh): U32t = A_hi B_lo + A_lo B_hi + A_hi B_hi in one TMEM accumulator
+      const uint32_t bk = um_bn() == 128 ? 32u : (uint32_t)UM_BKE;
       if (ctx->um_ta_ptr != A32) {
-        ctx->um_ta = make_tmap_f32(ctx, A32, 2 * (uint64_t)s.npad, (uint64_t)s.npad, UM_BK, UM_BM);
+        ctx->um_ta = make_tmap_f32(ctx, A32, 2 * (uint64_t)s.npad, (uint64_t)s.npad, bk, UM_BM);
         ctx->um_ta_ptr = A32;
       }
       if (ctx->um_tb_ptr[group] != B32 || ctx->um_tb_ncol[group] != g.ncol) {
-        ctx->um_tb[group] = make_tmap_f32(ctx, B32, (uint64_t)s.npad, 2 * (uint64_t)g.ncol, UM_BK, (uint32_t)um_bn());
+        ctx->um_tb[group] = make_tmap_f32(ctx, B32, (uint64_t)s.npad, 2 * (uint64_t)g.ncol, bk, (uint32_t)um_bn());
         ctx->um_tb_ptr[group] = B32;
         ctx->um_tb_ncol[group] = g.ncol;
       }
-      const int Kd = (int)std::min<int64_t>(roundup(s.n, UM_BK), s.npad);  // zero rows skipped
+      const int Kd = (int)std::min<int64_t>(roundup(s.n, 32), s.npad);  // zero rows skipped (multiple of both BKs)
       K1EpiArgs ep{a, s.btl, s.F, s.g0, (int)s.npad, two_np, (int)s.npairs, (int)s.n};
       const int cpa = (int)(s.k * s.k), epi = fuse_um ? (int)s.k : 0;
       if (um_bn() == 128)
-        launch_umma<128, 3>(ctx, epi, ctx->um_ta, ctx->um_tb[group], U32, (int)s.npad, Nc, Kd, a.nactive, cpa, ep, st,
+        launch_umma<128, 3, 32>(ctx, epi, ctx->um_ta, ctx->um_tb[group], U32, (int)s.npad, Nc, Kd, a.nactive, cpa, ep, st,
                             g.umctr + 2 * group);
       else
-        launch_umma<UM_BN, UM_STAGES>(ctx, epi, ctx->um_ta, ctx->um_tb[group], U32, (int)s.npad, Nc, Kd, a.nactive, cpa,
+        launch_umma<UM_BN, UM_STAGES, UM_BKE>(ctx, epi, ctx->um_ta, ctx->um_tb[group], U32, (int)s.npad, Nc, Kd, a.nactive, cpa,
                                       ep, st, g.umctr + 2 * group);
     } else {
       cublasHandle_t hb = ctx->cublas_eng[group];
@@ -1360,8 +1366,8 @@ static int setup_core(int64_t n, int64_t k, const double* A0, const double* Bl, 
     set_smem_attrs<G_BM, G_BN, G_WM, G_WN, G_ST, G_BK>(ctx);
     set_smem_attrs<S_BM, S_BN, S_WM, S_WN, S_ST, S_BK>(ctx);
     set_smem_attrs<V_BM, V_BN, V_WM, V_WN, V_ST, V_BK>(ctx);
-    set_umma_attrs<UM_BN, UM_STAGES>(ctx);
-    set_umma_attrs<128, 3>(ctx);
+    set_umma_attrs<UM_BN, UM_STAGES, UM_BKE>(ctx);
+    set_umma_attrs<128, 3, 32>(ctx);
     cudaStream_t st = ctx->stream;
     CK(cudaEventRecord(ctx->ev0, st));
     Seed& s = ctx->seed;

@@ -27,17 +27,23 @@ namespace lyap {
 constexpr int UM_BM = 128, UM_BK = 32;
 constexpr int UM_A_BYTES = UM_BM * UM_BK * 4;  // one A plane per stage: 16 KB
 // BN: GEMM columns per CTA (one tcgen05.mma N), STAGES: TMA pipeline depth
-template <int BN, int STAGES>
+template <int BN, int STAGES, int BK = UM_BK>
 struct UmCfg {
-  static constexpr int B_BYTES = BN * UM_BK * 4;                       // one B plane per stage
-  static constexpr int STAGE_BYTES = 2 * UM_A_BYTES + 2 * B_BYTES;
+  static constexpr int A_BYTES = UM_BM * BK * 4;                       // one A plane per stage
+  static constexpr int B_BYTES = BN * BK * 4;                          // one B plane per stage
+  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+  // K-major rows of BK fp32 = 128 B (SWIZZLE_128B) or 64 B (SWIZZLE_64B); 8-row atoms
+  static constexpr uint32_t LAYOUT = BK == 32 ? 2u : 4u, SBO = 8 * BK * 4;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;       // + alignment slack + barriers
   static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
   // instruction descriptor: D fp32, A/B tf32, both K-major, M = 128, N = BN
   static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                                     ((uint32_t)(UM_BM >> 4) << 24);
 };
-constexpr int UM_BN = 256, UM_STAGES = 2;  // production configuration (tools/microbench/umma_tf32x3.cu)
+// production configuration of the persistent kernel: 128 x 256 tiles, 16-wide k-blocks (64-byte swizzle),
+// 4 stages (tools/microbench/umma_tf32x3.cu: 740 TFLOP/s of TF32 work at the c5 shape, vs 663 for
+// 32-wide k-blocks in 2 stages and 733 for three cuBLAS TF32 GEMMs)
+constexpr int UM_BN = 256, UM_STAGES = 4, UM_BKE = 16;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -66,16 +72,18 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
       : "memory");
 }
-// UMMA shared-memory matrix descriptor, K-major, 128-byte swizzle: rows of 128 B, 8-row atoms 1024 B apart
-__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+// UMMA shared-memory matrix descriptor, K-major, swizzled: 8-row atoms SBO bytes apart
+template <uint32_t LAYOUT = 2, uint32_t SBO = 1024>
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);        // start address
   d |= (uint64_t)1 << 16;                        // leading byte offset (unused for swizzled K-major)
-  d |= (uint64_t)(1024 >> 4) << 32;              // stride byte offset: next 8-row atom
+  d |= (uint64_t)(SBO >> 4) << 32;               // stride byte offset: next 8-row atom
   d |= (uint64_t)1 << 46;                        // descriptor version (sm_100)
-  d |= (uint64_t)2 << 61;                        // layout: SWIZZLE_128B
+  d |= (uint64_t)LAYOUT << 61;                   // layout: 2 = SWIZZLE_128B, 4 = SWIZZLE_64B
   return d;
 }
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) { return umma_desc<2, 1024>(saddr); }
 template <uint32_t IDESC>
 __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t acc) {
   asm volatile(
@@ -192,6 +200,36 @@ __global__ void __launch_bounds__(128, 1)
 }
 
 
+// Per-thread coordinate data of the fused K1 epilogue, loaded once per tile (the same for every slot):
+// B~l_j (K complex, or real) and the T_d block F_j (K x K complex, or real) of coordinate m.
+// pair: m is the Re row of a conjugate pair (m + 1 its Im row, handled by this thread); active = the
+// thread writes (an Im-row thread of a pair does not); pad: m >= n (zero rows).
+template <int K>
+struct EpiCoord {
+  double blr[K], bli[K], fr[K][K], fi[K][K];
+  bool pair, active, pad;
+  __device__ __forceinline__ void load(const K1EpiArgs& ep, int m) {
+    pair = m < ep.two_np;
+    pad = m >= ep.n;
+    active = pad || !pair || !(m & 1);
+    if (!active || pad) return;
+    const int rep = pair ? (m >> 1) : (m - ep.two_np + ep.npairs);
+#pragma unroll
+    for (int t = 0; t < K; ++t) {
+      blr[t] = ep.btl[(int64_t)m * K + t];
+      bli[t] = pair ? ep.btl[(int64_t)(m + 1) * K + t] : 0.0;
+    }
+#pragma unroll
+    for (int s = 0; s < K; ++s)
+#pragma unroll
+      for (int t = 0; t < K; ++t) {
+        const double* f = ep.F + (((int64_t)rep * K + s) * K + t) * 2;
+        fr[s][t] = f[0];
+        fi[s][t] = f[1];
+      }
+  }
+};
+
 // ------------------------------------------------------------------------------------------------
 // Persistent, warp-specialised form (the engine's kernel): grid = one CTA per SM; tiles (M-tile fastest,
 // only the tiles that hold active columns) are claimed dynamically from a global counter (tctr[0]; the
@@ -208,13 +246,13 @@ __global__ void __launch_bounds__(128, 1)
 // (k1_out_element, the same code as the DMMA path's fused epilogue) and writes C(v)x straight into the
 // slot's Krylov basis; the Im row of a conjugate pair comes from the neighbouring lane (shfl).  VERIFY
 // positions [0, nver) are skipped (their exact FP64 apply comes from the DMMA GEMM).  EPI = 0: U32t.
-template <int BN, int STAGES, int EPI>
+template <int BN, int STAGES, int EPI, int BK = UM_BK>
 __global__ void __launch_bounds__(192, 1)
     k1_umma_persistent(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                        float* __restrict__ U32t, int npad, int ncol, int Kd, const int* __restrict__ nactive, int cpa,
                        const K1EpiArgs ep, int* __restrict__ tctr) {
-  using Cfg = UmCfg<BN, STAGES>;
-  constexpr int SB = Cfg::STAGE_BYTES, BB = Cfg::B_BYTES, TCOLS = 2 * BN <= 256 ? 256 : 512;
+  using Cfg = UmCfg<BN, STAGES, BK>;
+  constexpr int SB = Cfg::STAGE_BYTES, BB = Cfg::B_BYTES, AB = Cfg::A_BYTES, TCOLS = 2 * BN <= 256 ? 256 : 512;
   extern __shared__ __align__(1024) uint8_t um_smem[];
   const uint32_t base = (smem_u32(um_smem) + 1023) & ~1023u;
   uint8_t* gbase = um_smem + (base - smem_u32(um_smem));
@@ -257,7 +295,7 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  const int KB = Kd / UM_BK;
+  const int KB = Kd / BK;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -281,11 +319,11 @@ __global__ void __launch_bounds__(192, 1)
           mbar_wait(empty0 + 8 * s, ((it / STAGES) & 1) ^ 1);
           const uint32_t st = base + s * SB, fb = full0 + 8 * s;
           mbar_expect_tx(fb, SB);
-          const int k = kb * UM_BK;
+          const int k = kb * BK;
           tma_load_2d(st, &tmA, fb, k, m0);
-          tma_load_2d(st + UM_A_BYTES, &tmA, fb, npad + k, m0);
-          tma_load_2d(st + 2 * UM_A_BYTES, &tmB, fb, k, n0);
-          tma_load_2d(st + 2 * UM_A_BYTES + BB, &tmB, fb, k, ncol + n0);
+          tma_load_2d(st + AB, &tmA, fb, npad + k, m0);
+          tma_load_2d(st + 2 * AB, &tmB, fb, k, n0);
+          tma_load_2d(st + 2 * AB + BB, &tmB, fb, k, ncol + n0);
         }
       }
     }
@@ -305,13 +343,14 @@ __global__ void __launch_bounds__(192, 1)
           const int s = it % STAGES;
           mbar_wait(full0 + 8 * s, (it / STAGES) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t ah = base + s * SB, al = ah + UM_A_BYTES, bl = ah + 2 * UM_A_BYTES, bh = bl + BB;
+          const uint32_t ah = base + s * SB, al = ah + AB, bl = ah + 2 * AB, bh = bl + BB;
+          constexpr uint32_t LY = Cfg::LAYOUT, SO = Cfg::SBO;
 #pragma unroll
-          for (int j = 0; j < UM_BK / 8; ++j) {
-            const uint32_t o = 32 * j;
-            umma_tf32<Cfg::IDESC>(td, umma_desc_sw128(ah + o), umma_desc_sw128(bl + o), (kb > 0 || j > 0) ? 1u : 0u);
-            umma_tf32<Cfg::IDESC>(td, umma_desc_sw128(al + o), umma_desc_sw128(bh + o), 1u);
-            umma_tf32<Cfg::IDESC>(td, umma_desc_sw128(ah + o), umma_desc_sw128(bh + o), 1u);
+          for (int j = 0; j < BK / 8; ++j) {
+            const uint32_t o = 32 * j;  // 8 tf32 = 32 bytes along the swizzled row
+            umma_tf32<Cfg::IDESC>(td, umma_desc<LY, SO>(ah + o), umma_desc<LY, SO>(bl + o), (kb > 0 || j > 0) ? 1u : 0u);
+            umma_tf32<Cfg::IDESC>(td, umma_desc<LY, SO>(al + o), umma_desc<LY, SO>(bh + o), 1u);
+            umma_tf32<Cfg::IDESC>(td, umma_desc<LY, SO>(ah + o), umma_desc<LY, SO>(bh + o), 1u);
           }
           umma_commit(empty0 + 8 * s);
         }
@@ -333,6 +372,8 @@ __global__ void __launch_bounds__(192, 1)
       mbar_wait(tfull0 + 8 * acc, (li >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int m = m0 + 32 * q + lane;
+      EpiCoord<EPI ? EPI : 1> ec;
+      if constexpr (EPI > 0) ec.load(ep, m);
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t r[32];
@@ -350,21 +391,61 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) U32t[(int64_t)(n0 + c0 + j) * npad + m] = __uint_as_float(r[j]);
         } else {
+          // fused K1 epilogue: (T X)_sj = sum_t B~l_jt U[(s,t), j] + sum_t F_j[s,t] X_tj, out = sigma_s X_sj - (T X)_sj
+          // (the k1_epi contraction); row m + 1 (the Im row of a pair) comes from the next lane
           constexpr int KK = EPI * EPI, PP = 32 / KK;
           static_assert(32 % KK == 0, "whole (slot, s, t) groups per 32-column chunk");
 #pragma unroll
           for (int pp = 0; pp < PP; ++pp) {
-            double u[KK], u1[KK];
+            float u1[KK];
 #pragma unroll
-            for (int j = 0; j < KK; ++j) {
-              u[j] = (double)__uint_as_float(r[pp * KK + j]);
-              u1[j] = __shfl_down_sync(0xffffffffu, u[j], 1);  // row m + 1: the Im row of a pair
-            }
+            for (int j = 0; j < KK; ++j) u1[j] = __shfl_down_sync(0xffffffffu, __uint_as_float(r[pp * KK + j]), 1);
             const int pos = (n0 + c0) / KK + pp;
-            if (pos < nver || pos >= nact) continue;  // VERIFY (exact path) or inactive
+            if (pos < nver || pos >= nact || !ec.active) continue;  // VERIFY (exact path), inactive, Im lane
             const int slot = k1_slot(ep.a, pos);
+            if (ep.a.phase[slot] != PH_ITER) continue;
+            double* dst = ep.a.Qb + (int64_t)slot * ep.a.qstride + (int64_t)(ep.a.m[slot] + 1) * ep.a.L;
+            if (ec.pad) {
 #pragma unroll
-            for (int s = 0; s < EPI; ++s) k1_out_element<EPI>(ep, slot, s, m, u + s * EPI, u1 + s * EPI, 0);
+              for (int s = 0; s < EPI; ++s) dst[(int64_t)s * npad + m] = 0.0;
+              continue;
+            }
+            const double* x = ep.a.Xin + (int64_t)slot * ep.a.L;
+            if (ec.pair) {
+              double xr[EPI], xi[EPI];
+#pragma unroll
+              for (int t = 0; t < EPI; ++t) {
+                xr[t] = x[(int64_t)t * npad + m];
+                xi[t] = x[(int64_t)t * npad + m + 1];
+              }
+#pragma unroll
+              for (int s = 0; s < EPI; ++s) {
+                double yr = 0.0, yi = 0.0;
+#pragma unroll
+                for (int t = 0; t < EPI; ++t) {
+                  const double ur = __uint_as_float(r[pp * KK + s * EPI + t]), ui = u1[s * EPI + t];
+                  yr += ec.blr[t] * ur - ec.bli[t] * ui + ec.fr[s][t] * xr[t] - ec.fi[s][t] * xi[t];
+                  yi += ec.blr[t] * ui + ec.bli[t] * ur + ec.fr[s][t] * xi[t] + ec.fi[s][t] * xr[t];
+                }
+                const bool on = ep.a.mask[slot * EPI + s] != 0.0;
+                const double sg = ep.a.sigma[slot * EPI + s];
+                dst[(int64_t)s * npad + m] = on ? sg * xr[s] - yr : xr[s];
+                dst[(int64_t)s * npad + m + 1] = on ? sg * xi[s] - yi : xi[s];
+              }
+            } else {  // real eigenvalue
+              double xr[EPI];
+#pragma unroll
+              for (int t = 0; t < EPI; ++t) xr[t] = x[(int64_t)t * npad + m];
+#pragma unroll
+              for (int s = 0; s < EPI; ++s) {
+                double y = 0.0;
+#pragma unroll
+                for (int t = 0; t < EPI; ++t)
+                  y += ec.blr[t] * (double)__uint_as_float(r[pp * KK + s * EPI + t]) + ec.fr[s][t] * xr[t];
+                const bool on = ep.a.mask[slot * EPI + s] != 0.0;
+                dst[(int64_t)s * npad + m] = on ? ep.a.sigma[slot * EPI + s] * xr[s] - y : xr[s];
+              }
+            }
           }
         }
       }

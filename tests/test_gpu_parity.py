@@ -601,7 +601,10 @@ def test_two_level_preconditioner_configs(name, p):
 
 
 # ----------------------------------------------------------------------------- mixed precision
-@pytest.mark.parametrize("n,k,seed", [(30, 3, 0), (64, 2, 1), (13, 1, 2), (40, 4, 3)])
+@pytest.mark.parametrize("n,k,seed", [(30, 3, 0), (64, 2, 1), (13, 1, 2), (40, 4, 3),
+                                      # npad a multiple of 128: the tcgen05 path (fused epilogue for
+                                      # k = 1, 2, 4; k1_epi for k = 3), real eigenvalues included
+                                      (150, 2, 4), (200, 4, 5), (130, 1, 6), (140, 3, 7)])
 def test_mixed_precision_random(n, k, seed):
     """opts.mixed = 1: Krylov steps with the 3xTF32 T-apply, every cycle restarted from
     the exact FP64 true residual.  The stopping test is the FP64 one, so every v meets tol = 1e-12 and
