@@ -380,7 +380,8 @@ def main():
     # running), the figure ncu reports per launch; roofline.achieved above is the timed-region average
     iso = None
     try:
-        nvec = int(P.info["batch"] + 1) // 2
+        # one slot group's width (mixed precision runs one group over all slots)
+        nvec = int(P.info["batch"]) if P.mixed else int(P.info["batch"] + 1) // 2
         Xt = torch.randn(nvec, W.k, P.info["npad"], dtype=torch.float64, device=dev)
         Xt[:, :, W.n:] = 0
         P.apply_C(Xt)

@@ -75,7 +75,7 @@ struct Engine {
   double *Xin = nullptr, *X = nullptr;            // b x L
   double *rhs = nullptr, *t0s = nullptr;          // qlin: per-slot G0(v) (b x L) and t0(v) (b)
   double* Qb = nullptr;                           // b x (mmax+1) x L  (unnormalised basis)
-  double* Minv = nullptr;                         // b x nrep x k x k x 2
+  float* Minv = nullptr;                          // b x nrep x (2k)^2, FP32 (engine.cuh EngArgs::Minv)
   double *sigma = nullptr, *mask = nullptr;       // b x k
   double *eta = nullptr, *H = nullptr, *cs = nullptr, *sn = nullptr, *e = nullptr, *y = nullptr;
   double *bnorm = nullptr;                        // b

@@ -45,7 +45,11 @@ struct EngArgs {
   int* reg;     // per slot: regime of the current v
   int record;   // lyap_build_recycle: stop every slot after its first cycle (keep its Krylov data)
   double* Hraw; // unrotated Hessenberg columns (b x (mmax+1) x mmax), written when record != 0
-  double *X, *Xin, *Qb, *Minv, *sigma, *mask, *eta, *H, *e, *y, *bnorm, *part, *part3;
+  double *X, *Xin, *Qb, *sigma, *mask, *eta, *H, *e, *y, *bnorm, *part, *part3;
+  // P(v)^{-1} pair blocks, stored in FP32 (an FP32-rounded inverse is still one fixed preconditioner,
+  // applied identically by k_prec and the solution update; FP64 arithmetic throughout): half the bytes
+  // of the largest per-iteration stream of k_prec
+  float* Minv;
   double *part2, *Gq, *cf;  // Gram-row partials, Gram matrix Q^T Q of the basis, projection coefficients
   int *phase, *m, *vidx, *applies, *restarts, *ctrl, *newv, *alist;
   int* qctr;      // shared by all slot groups: [0] next queue position, [1] finished v's
@@ -198,7 +202,7 @@ __device__ __forceinline__ constexpr int pb_stride() { return 4 * K * K; }
 // reps of a slot, so the threads of a warp -- consecutive reps -- read and write coalesced)
 template <int D, int K>
 __device__ __forceinline__ void invert_block(const double* __restrict__ pb, const double* mask, const double* sigma,
-                                             double* __restrict__ out, int64_t ostride) {
+                                             float* __restrict__ out, int64_t ostride) {
   constexpr int RS = 2 * K, PER = D / K;  // row stride; rows per parameter (2 pair, 1 real)
   double M[D][D];
   int perm[D];
@@ -251,11 +255,11 @@ __device__ __forceinline__ void invert_block(const double* __restrict__ pb, cons
 #pragma unroll
   for (int r = 0; r < D; ++r)
 #pragma unroll
-    for (int c = 0; c < D; ++c) out[(int64_t)(r * RS + c) * ostride] = M[r][c];
+    for (int c = 0; c < D; ++c) out[(int64_t)(r * RS + c) * ostride] = (float)M[r][c];
 }
 
 // the Minv block of (slot, rep): element e at minv_of(...)[e * nrep]
-__device__ __forceinline__ const double* minv_of(const double* Minv, int64_t slot, int64_t rep, int64_t nrep, int S) {
+__device__ __forceinline__ const float* minv_of(const float* Minv, int64_t slot, int64_t rep, int64_t nrep, int S) {
   return Minv + slot * nrep * S + rep;
 }
 
@@ -266,7 +270,7 @@ __global__ void __launch_bounds__(128) k_pfactor(EngArgs a) {
   const int64_t rep = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (rep >= a.nrep || !a.newv[slot]) return;
   const bool pair = rep < a.npairs;
-  double* out = a.Minv + (int64_t)slot * a.nrep * pb_stride<K>() + rep;
+  float* out = a.Minv + (int64_t)slot * a.nrep * pb_stride<K>() + rep;
   const double* pb = a.Pb + rep * pb_stride<K>();
   if (pair)
     invert_block<2 * K, K>(pb, a.mask + slot * K, a.sigma + slot * K, out, a.nrep);
@@ -300,7 +304,7 @@ __global__ void __launch_bounds__(128) k_pfactor(EngArgs a) {
 
 // z = P_rep^{-1} r on the rep's folded coordinates: r[2t + b] (pairs) / r[t] (reals)
 template <int K>
-__device__ __forceinline__ void apply_pinv(const double* __restrict__ mi, int64_t st, bool pair,
+__device__ __forceinline__ void apply_pinv(const float* __restrict__ mi, int64_t st, bool pair,
                                            const double (&r)[2 * K], double (&z)[2 * K]) {
   constexpr int RS = 2 * K;
   if (pair) {
@@ -308,7 +312,7 @@ __device__ __forceinline__ void apply_pinv(const double* __restrict__ mi, int64_
     for (int i = 0; i < 2 * K; ++i) {
       double acc = 0.0;
 #pragma unroll
-      for (int j = 0; j < 2 * K; ++j) acc = fma(mi[(i * RS + j) * st], r[j], acc);
+      for (int j = 0; j < 2 * K; ++j) acc = fma((double)mi[(i * RS + j) * st], r[j], acc);
       z[i] = acc;
     }
   } else {
@@ -316,7 +320,7 @@ __device__ __forceinline__ void apply_pinv(const double* __restrict__ mi, int64_
     for (int i = 0; i < K; ++i) {
       double acc = 0.0;
 #pragma unroll
-      for (int j = 0; j < K; ++j) acc = fma(mi[(i * RS + j) * st], r[j], acc);
+      for (int j = 0; j < K; ++j) acc = fma((double)mi[(i * RS + j) * st], r[j], acc);
       z[i] = acc;
     }
   }

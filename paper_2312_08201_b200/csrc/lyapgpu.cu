@@ -325,7 +325,7 @@ void ensure_engine(lyap_ctx* ctx, int b, int mmax) {
   g.Xin = dalloc<double>(ctx, (size_t)b * g.L);
   g.X = dalloc<double>(ctx, (size_t)b * g.L);
   g.Qb = dalloc<double>(ctx, (size_t)b * (mmax + 1) * g.L);
-  g.Minv = dalloc<double>(ctx, (size_t)b * s.nrep * s.k * s.k * 4);
+  g.Minv = dalloc<float>(ctx, (size_t)b * s.nrep * s.k * s.k * 4);
   g.sigma = dalloc<double>(ctx, (size_t)b * s.k);
   g.mask = dalloc<double>(ctx, (size_t)b * s.k);
   g.eta = dalloc<double>(ctx, (size_t)b * (mmax + 1));

@@ -200,6 +200,17 @@ __global__ void __launch_bounds__(128, 1)
 }
 
 
+// tile index -> (M tile, N tile): grouped rasterisation, UM_GM row tiles share each sweep over the active
+// column tiles, so the A panels in flight (UM_GM x 128 rows of [Lf_hi | Lf_lo], 64 MB at c5) stay in L2
+// while B streams once per group (M-tile-fastest order re-read all of A, 134 MB, per wave of tiles)
+constexpr int UM_GM = 16;
+__device__ __forceinline__ void um_tile(int t, int MT, int ntn, int& mt, int& nt) {
+  const int gm = t / (UM_GM * ntn), r = t - gm * UM_GM * ntn;
+  const int rows = min(UM_GM, MT - gm * UM_GM);
+  mt = gm * UM_GM + r % rows;
+  nt = r / rows;
+}
+
 // Per-thread coordinate data of the fused K1 epilogue, loaded once per tile (the same for every slot):
 // B~l_j (K complex, or real) and the T_d block F_j (K x K complex, or real) of coordinate m.
 // pair: m is the Re row of a conjugate pair (m + 1 its Im row, handled by this thread); active = the
@@ -267,7 +278,8 @@ __global__ void __launch_bounds__(192, 1)
   const int ncols_act = nactive ? min(ncol, (*nactive) * cpa) : ncol;
   // EPI: column tiles made only of VERIFY positions (exact path) are skipped
   const int nt0 = EPI ? ((*ep.a.nver) * cpa) / BN : 0;
-  const int ntiles = max(0, (ncols_act + BN - 1) / BN - nt0) * MT;
+  const int ntn = max(0, (ncols_act + BN - 1) / BN - nt0);  // active column tiles
+  const int ntiles = ntn * MT;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full0 + 8 * s, 1);
@@ -313,7 +325,9 @@ __global__ void __launch_bounds__(192, 1)
           }
           break;
         }
-        const int m0 = (t % MT) * UM_BM, n0 = (t / MT + nt0) * BN;
+        int mt, nt;
+        um_tile(t, MT, ntn, mt, nt);
+        const int m0 = mt * UM_BM, n0 = (nt + nt0) * BN;
         for (int kb = 0; kb < KB; ++kb, ++it) {
           const int s = it % STAGES;
           mbar_wait(empty0 + 8 * s, ((it / STAGES) & 1) ^ 1);
@@ -367,7 +381,9 @@ __global__ void __launch_bounds__(192, 1)
       const int t = tile_ring[li & 3];
       mbar_arrive(rempty0 + 8 * (li & 3));
       if (t >= ntiles) break;
-      const int m0 = (t % MT) * UM_BM, n0 = (t / MT + nt0) * BN;
+      int mt, nt;
+      um_tile(t, MT, ntn, mt, nt);
+      const int m0 = mt * UM_BM, n0 = (nt + nt0) * BN;
       const int acc = li & 1;
       mbar_wait(tfull0 + 8 * acc, (li >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
