@@ -227,6 +227,13 @@ int lyap_build_recycle(lyap_ctx* ctx, int32_t nseeds, const double* seeds, int32
 int lyap_apply_C(lyap_ctx* ctx, int64_t nvec, const double* X, const double* sigma, double* Y,
                  void* cuda_stream);
 
+/* As lyap_apply_C, with the dense Cauchy part of T (eqs. (N2M1)/(N1M2)) applied in
+ * 3xTF32 on the tcgen05 tensor cores -- the operator of the mixed-precision Krylov steps (DESIGN.md
+ * §2.8); T_d and sigma o X stay FP64.  Relative error ~1e-5 of the Cauchy sums (not an exact apply).
+ * Requires mixed precision on for ctx (opts.mixed = 1, or auto with n > 1536): else LYAP_EINVAL. */
+int lyap_apply_C_mixed(lyap_ctx* ctx, int64_t nvec, const double* X, const double* sigma, double* Y,
+                       void* cuda_stream);
+
 /* Host copies of the folded seed state, for tests (each pointer nullable; sizes from lyap_info):
  *   lam: n x 2 (re, im) eigenvalue per folded coordinate (pair p: coords 2p, 2p+1 both hold the
  *        eigenvalue with positive imaginary part);  bhr, btl: n x k folded  B^r = S^T Br and

@@ -240,8 +240,9 @@ class Problem:
         seeds = _f64(seeds).reshape(U.shape[0], self.k)
         self._check(lib.lyap_set_recycle(self._ctx, U.shape[0], U.shape[1], U.ctypes.data, seeds.ctypes.data))
 
-    def apply_C(self, X, sigma=None, stream=None):
-        """K1 alone: Y = sigma o X - T X for folded vectors X (CUDA tensor, (nvec, k, npad))."""
+    def apply_C(self, X, sigma=None, stream=None, mixed=False):
+        """K1 alone: Y = sigma o X - T X for folded vectors X (CUDA tensor, (nvec, k, npad)).
+        mixed=True: the 3xTF32 tcgen05 operator of the mixed-precision Krylov steps (lyap_apply_C_mixed)."""
         import torch
         X = X.to(torch.float64).contiguous()
         Y = torch.empty_like(X)
@@ -250,8 +251,8 @@ class Problem:
             sigma = sigma.to(torch.float64).contiguous()
             sp = sigma.data_ptr()
         s = stream if stream is not None else torch.cuda.current_stream(X.device)
-        self._check(lib.lyap_apply_C(self._ctx, X.shape[0], X.data_ptr(), sp, Y.data_ptr(),
-                                     C.c_void_p(s.cuda_stream)))
+        fn = lib.lyap_apply_C_mixed if mixed else lib.lyap_apply_C
+        self._check(fn(self._ctx, X.shape[0], X.data_ptr(), sp, Y.data_ptr(), C.c_void_p(s.cuda_stream)))
         return Y
 
     def export_state(self) -> dict:

@@ -19,7 +19,7 @@ LYAP_KMAX = 8
 EXPORTED = ("lyap_default_opts", "lyap_setup", "lyap_trace_batch", "lyap_trace_batch_ex", "lyap_trace_batch_x",
             "lyap_stable_batch", "lyap_setup_qlin", "lyap_ek_trace_batch_ex",
             "lyap_get_info",
-            "lyap_get_stats", "lyap_reset_stats", "lyap_apply_C", "lyap_export_state", "lyap_destroy",
+            "lyap_get_stats", "lyap_reset_stats", "lyap_apply_C", "lyap_apply_C_mixed", "lyap_export_state", "lyap_destroy",
             "lyap_last_error", "lyap_solution", "lyap_setup_like", "lyap_set_recycle",
             "lyap_build_recycle", "lyap_ek_setup", "lyap_ek_trace_batch", "lyap_ek_destroy", "lyap_ek_last_error")
 
@@ -79,6 +79,8 @@ def _load():
     lib.lyap_reset_stats.restype = C.c_int
     lib.lyap_apply_C.argtypes = [P, C.c_int64, P, P, P, P]
     lib.lyap_apply_C.restype = C.c_int
+    lib.lyap_apply_C_mixed.argtypes = [P, C.c_int64, P, P, P, P]
+    lib.lyap_apply_C_mixed.restype = C.c_int
     lib.lyap_export_state.argtypes = [P, P, P, P, P, P, P]
     lib.lyap_export_state.restype = C.c_int
     lib.lyap_setup_like.argtypes = [P, C.c_int64, dp, dp, C.POINTER(Opts), C.POINTER(P)]

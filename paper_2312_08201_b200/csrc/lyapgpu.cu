@@ -462,7 +462,8 @@ void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, cudaEvent_t evb 
   const bool fuse = k1_fused(s.k, s.n, mp);
   // mixed precision with the tcgen05 kernel and k = 1, 2, 4: both GEMMs carry the K1 epilogue (the
   // DMMA one for the VERIFY positions, the tcgen05 one for the ITER positions), k1_epi is not launched
-  const bool fuse_mp = mp == 1 && mp_umma() && s.npad % UM_BM == 0 && (s.k == 1 || s.k == 2 || s.k == 4);
+  const bool fuse_mp =
+      mp == 1 && a.mode == 1 && mp_umma() && s.npad % UM_BM == 0 && (s.k == 1 || s.k == 2 || s.k == 4);
   static const int fmask = [] {  // LYAP_MP_FUSE (diagnostics): bit 0 tcgen05 epilogue, bit 1 DMMA epilogue
     const char* ev = std::getenv("LYAP_MP_FUSE");
     return ev ? std::atoi(ev) : 3;
@@ -536,6 +537,11 @@ void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, cudaEvent_t evb 
         launch_umma<UM_BN, UM_STAGES, UM_BKE>(ctx, epi, ctx->um_ta, ctx->um_tb[group], U32, (int)s.npad, Nc, Kd, a.nactive, cpa,
                                       ep, st, g.umctr + 2 * group);
     } else {
+      if (!ctx->cublas_eng[group]) {  // (the engine creates it; a standalone apply may come first)
+        CKB(cublasCreate(&ctx->cublas_eng[group]));
+        ctx->cublas_ws[group] = dalloc<double>(ctx, (32u << 20) / 8, false);
+        CKB(cublasSetWorkspace(ctx->cublas_eng[group], ctx->cublas_ws[group], 32u << 20));
+      }
       cublasHandle_t hb = ctx->cublas_eng[group];
       CKB(cublasSetStream(hb, st));
       const int Kd = (int)std::min<int64_t>(roundup(s.n, 16), s.npad);  // zero rows skipped
@@ -2296,9 +2302,14 @@ static int build_recycle_impl(lyap_ctx* ctx, int32_t nseeds, const double* seeds
   return rc;
 }
 
-int lyap_apply_C(lyap_ctx* ctx, int64_t nvec, const double* X, const double* sigma, double* Y, void* cuda_stream) {
+static int apply_C_impl(lyap_ctx* ctx, int64_t nvec, const double* X, const double* sigma, double* Y, void* cuda_stream,
+                        bool mixed) {
   if (!ctx || nvec < 0 || (nvec > 0 && (!X || !Y))) {
     set_err(ctx, "lyap_apply_C: invalid arguments");
+    return LYAP_EINVAL;
+  }
+  if (mixed && mp_mode(ctx) != 1) {
+    set_err(ctx, "lyap_apply_C_mixed: mixed precision is off for this context (opts.mixed)");
     return LYAP_EINVAL;
   }
   try {
@@ -2306,8 +2317,14 @@ int lyap_apply_C(lyap_ctx* ctx, int64_t nvec, const double* X, const double* sig
     cudaStream_t st = (cudaStream_t)cuda_stream;
     const int b = auto_batch(ctx, std::max<int64_t>(nvec, 1));
     ensure_engine(ctx, std::max(b, ctx->eng.b), ctx->eng.mmax > 0 ? ctx->eng.mmax : auto_mmax(ctx));
+    if (mixed) ensure_lf32(ctx, 1);
     const Engine& g = ctx->eng;
     const int64_t cap = g.ncol / (ctx->seed.k * ctx->seed.k);  // vectors per K1 launch (group 0 buffers)
+    int* zero = nullptr;
+    if (mixed) {  // no VERIFY positions: every vector takes the 3xTF32 product
+      zero = dalloc<int>(ctx, 1);
+      if (!ctx->eng.umctr) throw Fail{LYAP_ECUDA};
+    }
     for (int64_t v0 = 0; v0 < nvec; v0 += cap) {
       const int nb = (int)std::min<int64_t>(cap, nvec - v0);
       K1Args a{};
@@ -2319,16 +2336,30 @@ int lyap_apply_C(lyap_ctx* ctx, int64_t nvec, const double* X, const double* sig
       a.Yout = Y + v0 * g.L;
       a.nactive = nullptr;
       a.alist = nullptr;
-      launch_k1(ctx, a, st);
+      a.nver = zero;
+      launch_k1(ctx, a, st, nullptr, nullptr, 0, 0, mixed ? 1 : 0);
       ctx->stats.k1_launches++;
       ctx->stats.k1_vectors += nb;
-      ctx->stats.k1_exact_vectors += nb;
+      if (!mixed) ctx->stats.k1_exact_vectors += nb;
       ctx->stats.k1_flops += 2.0 * (double)ctx->seed.n * ctx->seed.n * ctx->seed.k * ctx->seed.k * nb;
+    }
+    if (zero) {
+      CK(cudaStreamSynchronize(st));
+      dfree(zero);
     }
   } catch (Fail f) {
     return f.code;
   }
   return LYAP_OK;
+}
+
+int lyap_apply_C(lyap_ctx* ctx, int64_t nvec, const double* X, const double* sigma, double* Y, void* cuda_stream) {
+  return apply_C_impl(ctx, nvec, X, sigma, Y, cuda_stream, false);
+}
+
+int lyap_apply_C_mixed(lyap_ctx* ctx, int64_t nvec, const double* X, const double* sigma, double* Y,
+                       void* cuda_stream) {
+  return apply_C_impl(ctx, nvec, X, sigma, Y, cuda_stream, true);
 }
 
 int lyap_get_info(const lyap_ctx* ctx, lyap_info* info) {

@@ -63,7 +63,8 @@ def _unfold(X, npairs, n):
     return G
 
 
-@pytest.mark.parametrize("n,k,seed", [(7, 1, 0), (16, 2, 1), (33, 3, 2), (40, 4, 3), (130, 2, 4)])
+@pytest.mark.parametrize("n,k,seed", [(7, 1, 0), (16, 2, 1), (33, 3, 2), (40, 4, 3), (130, 2, 4),
+                                      (1600, 2, 5)])  # n > 1536: the 128x128x32 large-tile DMMA configuration
 def test_k1_apply_against_paper_blocks(n, k, seed):
     """K1 (folded DMMA GEMM + prologue + epilogue) against the complex operator built entrywise from
     eqs. (N1M1), (N2M1), (N1M2) with the same seed factors."""
@@ -643,3 +644,41 @@ def test_mixed_precision_configs(name):
     assert rel_err(tau1, tau0).max() <= 1e-10
     P0.close()
     P1.close()
+
+
+@pytest.mark.parametrize("n,k,seed", [(200, 4, 0), (256, 2, 1), (150, 3, 2), (1700, 4, 3)])
+def test_k1_mixed_apply_against_paper_blocks(n, k, seed):
+    """The mixed-precision operator (lyap_apply_C_mixed: the Cauchy part on the tcgen05 3xTF32 GEMM,
+    T_d and sigma o X in FP64) against the same entrywise operator of eqs. (N1M1)/(N2M1)/(N1M2):
+    within the 3xTF32 accuracy (1e-4 of the largest entry), and visibly NOT exact -- the FP64
+    apply_C of the same vectors is within 1e-12 (the refinement's residual check needs that one)."""
+    import torch
+    rng = np.random.default_rng(40 + seed)
+    A0, Bl, Br, Q, E = workloads.random_stable(n, k, rng)
+    P = _problem(A0, Bl, Br, Q, E, mixed=1)
+    st = P.export_state()
+    npairs, npad = st["n_pairs"], st["npad"]
+    lam, br, bl = _complex_factors(st, n)
+    L = 1.0 / (lam[:, None] + lam[None, :])
+    F = np.einsum("ij,is,it->jst", L, br, bl)
+    nvec = 7
+    sig = rng.uniform(-2, 3, (nvec, k))
+    Gs = [_unfold(_fold(rng.standard_normal((k, n)) + 1j * rng.standard_normal((k, n)), npairs, npad), npairs, n)
+          for _ in range(nvec)]
+    Xt = torch.tensor(np.stack([_fold(G, npairs, npad) for G in Gs]), device="cuda")
+    St = torch.tensor(sig, device="cuda")
+    Ym = P.apply_C(Xt, St, mixed=True).cpu().numpy()
+    Y64 = P.apply_C(Xt, St).cpu().numpy()
+    worst = 0.0
+    for v in range(nvec):
+        G = Gs[v]
+        TG = np.einsum("jst,tj->sj", F, G) + np.einsum("jt,ij,is,ti->sj", bl, L, br, G)
+        expect = _fold(sig[v][:, None] * G - TG, npairs, npad)
+        scale = np.abs(expect).max()
+        np.testing.assert_allclose(Y64[v], expect, rtol=0, atol=1e-12 * scale)
+        err = np.abs(Ym[v] - expect).max() / scale
+        worst = max(worst, err)
+        assert err <= 1e-4, err
+        assert np.all(Ym[v][:, n:] == 0.0)
+    assert worst > 1e-12  # the inexact operator really is the float one
+    P.close()
