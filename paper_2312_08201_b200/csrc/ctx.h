@@ -74,7 +74,8 @@ struct Engine {
   int* umctr = nullptr;                           // tcgen05 GEMM tile counters (2 per slot group)
   double *Xin = nullptr, *X = nullptr;            // b x L
   double *rhs = nullptr, *t0s = nullptr;          // qlin: per-slot G0(v) (b x L) and t0(v) (b)
-  double* Qb = nullptr;                           // b x (mmax+1) x L  (unnormalised basis)
+  double* Qb = nullptr;                           // b x (mmax+1) x L  (unnormalised basis), FP64 engine
+  float* Qf = nullptr;                            // the same in FP32 (mixed-precision engine; Qb null)
   float* Minv = nullptr;                          // b x nrep x (2k)^2, FP32 (engine.cuh EngArgs::Minv)
   double *sigma = nullptr, *mask = nullptr;       // b x k
   double *eta = nullptr, *H = nullptr, *cs = nullptr, *sn = nullptr, *e = nullptr, *y = nullptr;

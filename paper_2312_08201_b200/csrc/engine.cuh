@@ -46,6 +46,9 @@ struct EngArgs {
   int record;   // lyap_build_recycle: stop every slot after its first cycle (keep its Krylov data)
   double* Hraw; // unrotated Hessenberg columns (b x (mmax+1) x mmax), written when record != 0
   double *X, *Xin, *Qb, *sigma, *mask, *eta, *H, *e, *y, *bnorm, *part, *part3;
+  // mixed precision: the Krylov basis is stored in FP32 (Qf; Qb null) -- a cycle only has to reduce the
+  // residual by mixed_eta, and every cycle starts from the exact FP64 residual
+  float* Qf;
   // P(v)^{-1} pair blocks, stored in FP32 (an FP32-rounded inverse is still one fixed preconditioner,
   // applied identically by k_prec and the solution update; FP64 arithmetic throughout): half the bytes
   // of the largest per-iteration stream of k_prec
@@ -73,6 +76,14 @@ struct EngArgs {
 };
 
 __device__ __forceinline__ int64_t rep_coord(int64_t rep, int64_t npairs) { return rep < npairs ? 2 * rep : rep + npairs; }
+
+// the basis in its storage type (QT = double: Qb; QT = float: Qf)
+template <typename QT>
+__device__ __forceinline__ QT* qbase(const EngArgs& a);
+template <>
+__device__ __forceinline__ double* qbase<double>(const EngArgs& a) { return a.Qb; }
+template <>
+__device__ __forceinline__ float* qbase<float>(const EngArgs& a) { return a.Qf; }
 
 // ---------------------------------------------------------------- phase advance + v queue
 // One block (b <= 1024 threads): XUPD -> VERIFY; FREE slots take the next v's in slot order.
@@ -327,16 +338,16 @@ __device__ __forceinline__ void apply_pinv(const float* __restrict__ mi, int64_t
 }
 
 // gather / scatter of a rep's folded coordinates of a k x npad vector (scaled on the way in)
-template <int K>
-__device__ __forceinline__ void rep_load(const double* __restrict__ x, int64_t npad, int64_t c, bool pair, double sc,
+template <int K, typename T>
+__device__ __forceinline__ void rep_load(const T* __restrict__ x, int64_t npad, int64_t c, bool pair, double sc,
                                          double (&r)[2 * K]) {
 #pragma unroll
   for (int t = 0; t < K; ++t) {
     if (pair) {
-      r[2 * t] = sc * x[t * npad + c];
-      r[2 * t + 1] = sc * x[t * npad + c + 1];
+      r[2 * t] = sc * (double)x[t * npad + c];
+      r[2 * t + 1] = sc * (double)x[t * npad + c + 1];
     } else {
-      r[t] = sc * x[t * npad + c];
+      r[t] = sc * (double)x[t * npad + c];
     }
   }
 }
@@ -356,7 +367,7 @@ __device__ __forceinline__ void rep_store(double* __restrict__ x, int64_t npad, 
 
 // ---------------------------------------------------------------- apply input (K2 apply)
 // ITER: Xin = P(v)^{-1} (q^_m / eta_m);  VERIFY: Xin = X.
-template <int K>
+template <int K, typename QT = double>
 __global__ void __launch_bounds__(128) k_prec(EngArgs a) {
   const int slot = blockIdx.y;
   const int64_t rep = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -378,7 +389,7 @@ __global__ void __launch_bounds__(128) k_prec(EngArgs a) {
   }
   const int m = a.m[slot];
   const double sc = 1.0 / a.eta[(int64_t)slot * (a.mmax + 1) + m];
-  const double* q = a.Qb + ((int64_t)slot * (a.mmax + 1) + m) * a.L;
+  const QT* q = qbase<QT>(a) + ((int64_t)slot * (a.mmax + 1) + m) * a.L;
   double r[2 * K], z[2 * K];
   rep_load<K>(q, a.npad, c, pair, sc, r);
   if (a.pc > 0) {
@@ -679,6 +690,7 @@ __global__ void __launch_bounds__(256) k_uapply(EngArgs a) {
 #define LYAP_DOT_IG 64
 #endif
 constexpr int DOT_IG = LYAP_DOT_IG;  // basis vectors per k_dots block (grid.z splits long cycles)
+template <typename QT = double>
 __global__ void __launch_bounds__(256) k_dots(EngArgs a) {
   __shared__ double ws[RED_CE];
   __shared__ double qm[RED_CE];
@@ -689,7 +701,7 @@ __global__ void __launch_bounds__(256) k_dots(EngArgs a) {
   const int64_t qs = (int64_t)(a.mmax + 1) * a.L;
   if (ph == PH_VERIFY || ph == PH_START) {
     if (blockIdx.z != 0) return;
-    double* R = a.Qb + slot * qs;
+    QT* R = qbase<QT>(a) + slot * qs;
     const double* X = a.X + (int64_t)slot * a.L;
     const bool start = ph == PH_START;  // g = 0: R = rhs, written here as q^_0
     double s0 = 0.0, s1 = 0.0, s2 = 0.0;
@@ -701,7 +713,7 @@ __global__ void __launch_bounds__(256) k_dots(EngArgs a) {
         double r;
         if (start) {
           r = rh;
-          R[e] = rh;
+          R[e] = (QT)rh;
         } else {
           r = R[e];
           s2 += a.hf[e] * X[e];
@@ -726,8 +738,8 @@ __global__ void __launch_bounds__(256) k_dots(EngArgs a) {
   const int i0 = blockIdx.z * DOT_IG;  // this block's basis vectors: [i0, min(m, i0 + DOT_IG - 1)]
   if (i0 > m) return;
   const int i1 = min(m, i0 + DOT_IG - 1);
-  const double* w = a.Qb + slot * qs + (int64_t)(m + 1) * a.L;
-  const double* qlast = a.Qb + slot * qs + (int64_t)m * a.L;
+  const QT* w = qbase<QT>(a) + slot * qs + (int64_t)(m + 1) * a.L;
+  const QT* qlast = qbase<QT>(a) + slot * qs + (int64_t)m * a.L;
   for (int i = threadIdx.x; i < RED_CE; i += blockDim.x) {
     const int64_t e = e0 + i;
     ws[i] = e < a.L ? w[e] : 0.0;
@@ -737,7 +749,7 @@ __global__ void __launch_bounds__(256) k_dots(EngArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int lim = (int)((a.L - e0) < RED_CE ? (a.L - e0) : RED_CE);
   for (int i = i0 + warp; i <= i1; i += 8) {
-    const double* q = a.Qb + slot * qs + (int64_t)i * a.L + e0;
+    const QT* q = qbase<QT>(a) + slot * qs + (int64_t)i * a.L + e0;
     double d0 = 0.0, d1 = 0.0, g0 = 0.0, g1 = 0.0;
     int e = lane;
     for (; e + 224 < lim; e += 256) {  // 8 independent loads per lane per round
@@ -827,6 +839,7 @@ __global__ void __launch_bounds__(256) k_gram(EngArgs a) {
 #ifndef LYAP_UPD_UNROLL
 #define LYAP_UPD_UNROLL 8
 #endif
+template <typename QT = double>
 __global__ void __launch_bounds__(256) k_upd(EngArgs a) {
   extern __shared__ double cfs[];  // mmax + 1
   __shared__ double red[8];
@@ -836,8 +849,8 @@ __global__ void __launch_bounds__(256) k_upd(EngArgs a) {
   const int64_t qs = (int64_t)(a.mmax + 1) * a.L;
   for (int i = threadIdx.x; i <= m; i += blockDim.x) cfs[i] = a.cf[(int64_t)slot * (a.mmax + 1) + i];
   __syncthreads();
-  double* w = a.Qb + slot * qs + (int64_t)(m + 1) * a.L;
-  const double* Q = a.Qb + slot * qs;
+  QT* w = qbase<QT>(a) + slot * qs + (int64_t)(m + 1) * a.L;
+  const QT* Q = qbase<QT>(a) + slot * qs;
   const int64_t e0 = (int64_t)chunk * RED_CE;
   // each thread owns 4 elements of the chunk; the basis loop issues 4 independent loads per vector
   constexpr int EPT = RED_CE / 256;
@@ -858,9 +871,9 @@ __global__ void __launch_bounds__(256) k_upd(EngArgs a) {
     double v[UU][EPT];
 #pragma unroll
     for (int u = 0; u < UU; ++u) {
-      const double* q = Q + (int64_t)(i + u) * a.L;
+      const QT* q = Q + (int64_t)(i + u) * a.L;
 #pragma unroll
-      for (int r = 0; r < EPT; ++r) v[u][r] = ok[r] ? q[eo[r]] : 0.0;
+      for (int r = 0; r < EPT; ++r) v[u][r] = ok[r] ? (double)q[eo[r]] : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < UU; ++u) {
@@ -871,18 +884,18 @@ __global__ void __launch_bounds__(256) k_upd(EngArgs a) {
   }
   for (; i <= m; ++i) {
     const double c = cfs[i];
-    const double* q = Q + (int64_t)i * a.L;
+    const QT* q = Q + (int64_t)i * a.L;
 #pragma unroll
     for (int r = 0; r < EPT; ++r)
-      if (ok[r]) acc[r] = fma(c, q[eo[r]], acc[r]);
+      if (ok[r]) acc[r] = fma(c, (double)q[eo[r]], acc[r]);
   }
   double nrm = 0.0;
 #pragma unroll
   for (int r = 0; r < EPT; ++r)
     if (ok[r]) {
-      const double v = w[eo[r]] - acc[r];
+      const QT v = (QT)((double)w[eo[r]] - acc[r]);
       w[eo[r]] = v;
-      nrm += v * v;
+      nrm += (double)v * (double)v;  // the norm of the vector as stored
     }
   nrm = block_sum(nrm, red);
   if (threadIdx.x == 0) a.part3[((int64_t)slot * a.nchunk + chunk) * 3] = nrm;
@@ -1073,7 +1086,7 @@ __global__ void __launch_bounds__(256) k_gout(EngArgs a) {
 // at an even coordinate), forms the basis combination there (64 elements x 4 slices of the basis
 // index, reduced in shared memory), then applies the k x k P^{-1} block of every representative in
 // the window.
-template <int K>
+template <int K, typename QT = double>
 __global__ void __launch_bounds__(256) k_xcomb(EngArgs a) {
   __shared__ double ys[1024];
   __shared__ double red[4][64];
@@ -1085,7 +1098,10 @@ __global__ void __launch_bounds__(256) k_xcomb(EngArgs a) {
   const double* ysl = a.y + (int64_t)slot * a.mmax;
   for (int i = threadIdx.x; i < m1; i += blockDim.x) ys[i] = i < su ? 0.0 : ysl[i];
   __syncthreads();
-  const double* Q = (a.pc > 0 ? a.Zb : a.Qb) + (int64_t)slot * (a.mmax + 1) * a.L;  // two-level: Z_j = P^{-1} q_j
+  const QT* Qb0 = qbase<QT>(a);
+  if constexpr (sizeof(QT) == 8)
+    if (a.pc > 0) Qb0 = (const QT*)a.Zb;  // two-level: Z_j = P^{-1} q_j (FP64 basis only)
+  const QT* Q = Qb0 + (int64_t)slot * (a.mmax + 1) * a.L;
   double* X = a.X + (int64_t)slot * a.L;
   const int el = threadIdx.x & 63, sl = threadIdx.x >> 6;
   for (int64_t c0 = (int64_t)blockIdx.x * 64; c0 < a.npad; c0 += (int64_t)gridDim.x * 64) {
@@ -1097,12 +1113,12 @@ __global__ void __launch_bounds__(256) k_xcomb(EngArgs a) {
       if (c < a.npad) {
         int i = sl;
         for (; i + 12 < m1; i += 16) {  // 4 independent basis loads per step
-          s0 = fma(ys[i], Q[(int64_t)i * a.L + e], s0);
-          s1 = fma(ys[i + 4], Q[(int64_t)(i + 4) * a.L + e], s1);
-          s2 = fma(ys[i + 8], Q[(int64_t)(i + 8) * a.L + e], s2);
-          s3 = fma(ys[i + 12], Q[(int64_t)(i + 12) * a.L + e], s3);
+          s0 = fma(ys[i], (double)Q[(int64_t)i * a.L + e], s0);
+          s1 = fma(ys[i + 4], (double)Q[(int64_t)(i + 4) * a.L + e], s1);
+          s2 = fma(ys[i + 8], (double)Q[(int64_t)(i + 8) * a.L + e], s2);
+          s3 = fma(ys[i + 12], (double)Q[(int64_t)(i + 12) * a.L + e], s3);
         }
-        for (; i < m1; i += 4) s0 = fma(ys[i], Q[(int64_t)i * a.L + e], s0);
+        for (; i < m1; i += 4) s0 = fma(ys[i], (double)Q[(int64_t)i * a.L + e], s0);
       }
       red[sl][el] = (s0 + s2) + (s1 + s3);
       __syncthreads();

@@ -35,6 +35,7 @@ struct K1Args {
   const int* phase;    // engine: slot phases
   const int* m;        // engine: current Krylov index per slot
   double* Qb;          // engine: basis (nslot x (mmax+1) x L)
+  float* Qf;           // engine, mixed precision: the basis in FP32 (then Qb is null)
   int64_t qstride;     // (mmax+1) * L
   double* Yout;        // apply mode output (nslot x L)
   const int* nactive;  // engine: number of active slots (null: all nslot vectors are active)
@@ -164,6 +165,18 @@ struct DgemmCfg {
 // col = v * blk + c is written to C[(v * no + r) * no + c] for r, c < no (the unpadded order).
 struct DgemmOut {
   int blk, nblk, no;
+};
+
+// destination of a K1 output row: FP64 (d) or, for the FP32 basis of the mixed-precision engine, f
+struct K1Dst {
+  double* d;
+  float* f;
+  __device__ __forceinline__ void put(int64_t i, double v) const {
+    if (f)
+      f[i] = (float)v;
+    else
+      d[i] = v;
+  }
 };
 
 template <int K>
@@ -315,27 +328,29 @@ __device__ __forceinline__ void k1_out_element(const K1EpiArgs& ep, int slot, in
   const int npad = ep.npad;
   const double* gsrc = a.rhs ? a.rhs + (int64_t)slot * a.L : ep.g0;
   const double* x = a.Xin + (int64_t)slot * a.L;
-  double* dst;
+  K1Dst dst;
   bool verify = false;
   double msk = 1.0, sig;
   if (a.mode == 0) {
-    dst = a.Yout + (int64_t)slot * a.L + (int64_t)s * npad;
+    dst = K1Dst{a.Yout + (int64_t)slot * a.L + (int64_t)s * npad, nullptr};
     sig = a.sigma ? a.sigma[slot * K + s] : 0.0;
   } else {
     const int ph = a.phase[slot];
+    int64_t off;
     if (ph == PH_ITER) {
-      dst = a.Qb + (int64_t)slot * a.qstride + (int64_t)(a.m[slot] + 1) * a.L + (int64_t)s * npad;
+      off = (int64_t)slot * a.qstride + (int64_t)(a.m[slot] + 1) * a.L + (int64_t)s * npad;
     } else if (ph == PH_VERIFY) {
-      dst = a.Qb + (int64_t)slot * a.qstride + (int64_t)s * npad;
+      off = (int64_t)slot * a.qstride + (int64_t)s * npad;
       verify = true;
     } else {
       return;
     }
+    dst = a.Qf ? K1Dst{nullptr, a.Qf + off} : K1Dst{a.Qb + off, nullptr};
     sig = a.sigma[slot * K + s];
     msk = a.mask[slot * K + s];
   }
   if (c >= ep.n) {  // zero padding stays zero
-    dst[c] = 0.0;
+    dst.put(c, 0.0);
     return;
   }
   if (c < ep.two_np) {
@@ -353,8 +368,8 @@ __device__ __forceinline__ void k1_out_element(const K1EpiArgs& ep, int slot, in
     const cplx xv = mk(x[(int64_t)s * npad + c], x[(int64_t)s * npad + c + 1]);
     cplx o = (msk != 0.0) ? (sig * xv - y) : xv;
     if (verify) o = mk(msk * gsrc[(int64_t)s * npad + c], msk * gsrc[(int64_t)s * npad + c + 1]) - o;
-    dst[c] = o.re;
-    dst[c + 1] = o.im;
+    dst.put(c, o.re);
+    dst.put(c + 1, o.im);
   } else {
     const int rep = c - ep.two_np + ep.npairs;
     double y = 0.0;
@@ -366,7 +381,7 @@ __device__ __forceinline__ void k1_out_element(const K1EpiArgs& ep, int slot, in
     const double xv = x[(int64_t)s * npad + c];
     double o = (msk != 0.0) ? (sig * xv - y) : xv;
     if (verify) o = msk * gsrc[(int64_t)s * npad + c] - o;
-    dst[c] = o;
+    dst.put(c, o);
   }
 }
 
@@ -413,27 +428,29 @@ __global__ void __launch_bounds__(256) k1_epi(K1Args a, const double* __restrict
     const int slot = k1_slot(a, s0 + sl);
     const double* gsrc = a.rhs ? a.rhs + (int64_t)slot * a.L : g0;
     int c = i0 + r;
-    double* dst;
+    K1Dst dst;
     bool verify = false;
     double msk = 1.0, sig;
     if (a.mode == 0) {
-      dst = a.Yout + (int64_t)slot * a.L + (int64_t)s * npad;
+      dst = K1Dst{a.Yout + (int64_t)slot * a.L + (int64_t)s * npad, nullptr};
       sig = a.sigma ? a.sigma[slot * K + s] : 0.0;
     } else {
       int ph = a.phase[slot];
+      int64_t off;
       if (ph == PH_ITER) {
-        dst = a.Qb + (int64_t)slot * a.qstride + (int64_t)(a.m[slot] + 1) * a.L + (int64_t)s * npad;
+        off = (int64_t)slot * a.qstride + (int64_t)(a.m[slot] + 1) * a.L + (int64_t)s * npad;
       } else if (ph == PH_VERIFY) {
-        dst = a.Qb + (int64_t)slot * a.qstride + (int64_t)s * npad;
+        off = (int64_t)slot * a.qstride + (int64_t)s * npad;
         verify = true;
       } else {
         continue;
       }
+      dst = a.Qf ? K1Dst{nullptr, a.Qf + off} : K1Dst{a.Qb + off, nullptr};
       sig = a.sigma[slot * K + s];
       msk = a.mask[slot * K + s];
     }
     if (c >= n) {  // zero padding stays zero
-      dst[c] = 0.0;
+      dst.put(c, 0.0);
       continue;
     }
     const int colb = sl * K * K + s * K;
@@ -454,8 +471,8 @@ __global__ void __launch_bounds__(256) k1_epi(K1Args a, const double* __restrict
       if (verify) {
         o = mk(msk * gsrc[(int64_t)s * npad + c], msk * gsrc[(int64_t)s * npad + c + 1]) - o;
       }
-      dst[c] = o.re;
-      dst[c + 1] = o.im;
+      dst.put(c, o.re);
+      dst.put(c + 1, o.im);
     } else {
       const int rep = c - two_np + npairs;
       double y = 0.0;
@@ -467,7 +484,7 @@ __global__ void __launch_bounds__(256) k1_epi(K1Args a, const double* __restrict
       double xv = xs[sl][s][r];
       double o = (msk != 0.0) ? (sig * xv - y) : xv;
       if (verify) o = msk * gsrc[(int64_t)s * npad + c] - o;
-      dst[c] = o;
+      dst.put(c, o);
     }
   }
 }

@@ -135,7 +135,7 @@ void upload_seeds(lyap_ctx* ctx) {
 
 // ------------------------------------------------------------------ engine allocation
 void free_engine(Engine& g, bool keep_order = true) {
-  void* ps[] = {g.Bop, g.U, g.Bop32, g.U32, g.umctr, g.Xin, g.X, g.Qb, g.Minv, g.sigma, g.mask, g.eta, g.H, g.e, g.y,
+  void* ps[] = {g.Bop, g.U, g.Bop32, g.U32, g.umctr, g.Xin, g.X, g.Qb, g.Qf, g.Minv, g.sigma, g.mask, g.eta, g.H, g.e, g.y,
                 g.bnorm, g.part, g.part3, g.phase, g.m, g.vidx, g.applies, g.restarts, g.ctrl,
                 g.part2, g.Gq, g.cf, g.Hraw, g.rhs, g.t0s, g.Zb, g.Rbuf, g.Yz, g.Cc, g.Wc, g.Einv};
   for (void* p : ps) dfree(p);
@@ -299,7 +299,7 @@ void ensure_engine(lyap_ctx* ctx, int b, int mmax) {
   const Seed& s = ctx->seed;
   const int pc = ctx->coarse.p;
   const int mp = mp_mode(ctx);
-  if (g.Qb && g.mmax == mmax && g.bcap >= b && g.pc == pc && g.mp == mp) {
+  if ((g.Qb || g.Qf) && g.mmax == mmax && g.bcap >= b && g.pc == pc && g.mp == mp) {
     configure_run(s, g, b);
     return;
   }
@@ -324,7 +324,10 @@ void ensure_engine(lyap_ctx* ctx, int b, int mmax) {
   }
   g.Xin = dalloc<double>(ctx, (size_t)b * g.L);
   g.X = dalloc<double>(ctx, (size_t)b * g.L);
-  g.Qb = dalloc<double>(ctx, (size_t)b * (mmax + 1) * g.L);
+  if (mp)  // mixed precision: FP32 Krylov basis
+    g.Qf = dalloc<float>(ctx, (size_t)b * (mmax + 1) * g.L);
+  else
+    g.Qb = dalloc<double>(ctx, (size_t)b * (mmax + 1) * g.L);
   g.Minv = dalloc<float>(ctx, (size_t)b * s.nrep * s.k * s.k * 4);
   g.sigma = dalloc<double>(ctx, (size_t)b * s.k);
   g.mask = dalloc<double>(ctx, (size_t)b * s.k);
@@ -654,7 +657,7 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   a.gout = gout;
   a.x0 = x0;
   a.record = record;
-  a.s_rec = ctx->nreg > 0 ? ctx->s_rec : 0;
+  a.s_rec = (ctx->nreg > 0 && !mp) ? ctx->s_rec : 0;  // recycle spaces: FP64 engine only
   a.Ureg = ctx->Ureg;
   a.sreg = ctx->sreg;
   a.TUreg = ctx->TUreg;
@@ -676,7 +679,8 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
     const int64_t ld = mmax + 1;
     x.X = g.X + s0 * g.L;
     x.Xin = g.Xin + s0 * g.L;
-    x.Qb = g.Qb + s0 * ld * g.L;
+    x.Qb = g.Qb ? g.Qb + s0 * ld * g.L : nullptr;
+    x.Qf = g.Qf ? g.Qf + s0 * ld * g.L : nullptr;
     x.Minv = g.Minv + s0 * s.nrep * s.k * s.k * 4;
     x.sigma = g.sigma + s0 * s.k;
     x.mask = g.mask + s0 * s.k;
@@ -726,6 +730,7 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
     k1.phase = x.phase;
     k1.m = x.m;
     k1.Qb = x.Qb;
+    k1.Qf = x.Qf;
     k1.qstride = ld * g.L;
     k1.nactive = x.ctrl + 2;
     k1.alist = x.alist;
@@ -749,7 +754,10 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   const size_t gram_smem = sizeof(double) * (size_t)(mmax + 1);
   if (gram_smem > 48 * 1024) CK(cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_smem));
   if (ctrl_smem > 48 * 1024) CK(cudaFuncSetAttribute(k_ctrl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctrl_smem));
-  if (upd_smem > 48 * 1024) CK(cudaFuncSetAttribute(k_upd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem));
+  if (upd_smem > 48 * 1024) {
+    CK(cudaFuncSetAttribute(k_upd<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem));
+    CK(cudaFuncSetAttribute(k_upd<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem));
+  }
   const int64_t per_v = (int64_t)(ctx->opts.max_restarts + 1) * (mmax + 2);
   const int64_t max_iter = ((nv + bg0 - 1) / bg0) * per_v + 64;
   const int poll = 8;
@@ -793,18 +801,29 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
       LAUNCHED();
       CKB(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, 2 * Li, bg, p, &one, x.Zc, 2 * Li, x.Wc, p, &zero, x.Yz, 2 * Li));
     }
-    K_DISPATCH(s.k, (k_prec<KK><<<grep, 128, 0, sg>>>(x)));
+    if (g.Qf) {
+      K_DISPATCH(s.k, (k_prec<KK, float><<<grep, 128, 0, sg>>>(x)));
+    } else {
+      K_DISPATCH(s.k, (k_prec<KK><<<grep, 128, 0, sg>>>(x)));
+    }
     LAUNCHED();
     if (x.s_rec > 0) {
       k_uapply<<<dim3((unsigned)std::min<int64_t>((g.L + 255) / 256, 64), (unsigned)bg), 256, 0, sg>>>(x);
       LAUNCHED();
     }
     launch_k1(ctx, gk[gi], sg, evb, eve, evflags, gi, mp);
-    k_dots<<<dim3((unsigned)g.nchunk, (unsigned)bg, (unsigned)((mmax + DOT_IG) / DOT_IG)), 256, 0, sg>>>(x);
+    const dim3 gdot((unsigned)g.nchunk, (unsigned)bg, (unsigned)((mmax + DOT_IG) / DOT_IG));
+    if (g.Qf)
+      k_dots<float><<<gdot, 256, 0, sg>>>(x);
+    else
+      k_dots<<<gdot, 256, 0, sg>>>(x);
     LAUNCHED();
     k_gram<<<bg, 256, gram_smem, sg>>>(x);
     LAUNCHED();
-    k_upd<<<gred, 256, upd_smem, sg>>>(x);
+    if (g.Qf)
+      k_upd<float><<<gred, 256, upd_smem, sg>>>(x);
+    else
+      k_upd<<<gred, 256, upd_smem, sg>>>(x);
     LAUNCHED();
     k_ctrl<<<(bg + 3) / 4, 128, ctrl_smem, sg>>>(x);
     LAUNCHED();
@@ -812,7 +831,11 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
       k_gout<<<dim3((unsigned)std::min<int64_t>((g.L + 255) / 256, 64), (unsigned)bg), 256, 0, sg>>>(x);
       LAUNCHED();
     }
-    K_DISPATCH(s.k, (k_xcomb<KK><<<gxc, 256, 0, sg>>>(x)));
+    if (g.Qf) {
+      K_DISPATCH(s.k, (k_xcomb<KK, float><<<gxc, 256, 0, sg>>>(x)));
+    } else {
+      K_DISPATCH(s.k, (k_xcomb<KK><<<gxc, 256, 0, sg>>>(x)));
+    }
     LAUNCHED();
     return ctx->stats.kernel_launches - l0;
   };
@@ -1077,7 +1100,8 @@ int coarse_size(const lyap_ctx* ctx) {
   const Seed& s = ctx->seed;
   // auto: 32 when n k >= 2000 -- except under mixed precision, where the coarse products cost what they
   // save (c5 2280 with / 2315 v/s without)
-  int p = ctx->opts.coarse < 0 ? ((s.n * s.k >= 2000 && !mp_mode(ctx)) ? 32 : 0) : ctx->opts.coarse;
+  if (mp_mode(ctx)) return 0;  // the coarse space is an FP64-engine option (the FP32 basis has no Zb)
+  int p = ctx->opts.coarse < 0 ? (s.n * s.k >= 2000 ? 32 : 0) : ctx->opts.coarse;
   p = std::min<int>(p, 256);
   p = std::min<int64_t>(p, (s.n * s.k) / 2);
   return p < 8 ? 0 : p / 8 * 8;
@@ -1726,7 +1750,7 @@ static int trace_batch_impl(lyap_ctx* ctx, int64_t nv, const double* V, double* 
     const int s_auto = ctx->opts.recycle < 0 ? 0 : ctx->opts.recycle;
     Seed& sd = ctx->seed;
     ensure_dwork(ctx);
-    if (s_auto > 0 && !ctx->recycle_manual) {
+    if (s_auto > 0 && !ctx->recycle_manual && !mp_mode(ctx)) {
       // automatic recycle spaces from the corners of the batch's bounding box: the 2k box bounds are
       // the only host read of the call before the engine runs
       k_box<<<(unsigned)k, 256, 0, st>>>(dV, (int)nv, (int)k, sd.dwork + 8);
@@ -2004,6 +2028,10 @@ int lyap_solution(lyap_ctx* ctx, int64_t nv, const double* V, double* X, double*
 }
 
 int lyap_set_recycle(lyap_ctx* ctx, int32_t nreg, int32_t s, const double* U, const double* seeds) {
+  if (ctx && nreg > 0 && mp_mode(ctx)) {
+    set_err(ctx, "lyap_set_recycle: recycle spaces need the FP64 engine (opts.mixed = 0)");
+    return LYAP_EINVAL;
+  }
   if (ctx) ctx->recycle_manual = nreg > 0;  // user-managed spaces: no automatic rebuild
   if (!ctx || nreg < 0 || (nreg > 0 && (s < 1 || !U || !seeds))) {
     set_err(ctx, "lyap_set_recycle: invalid arguments");
@@ -2051,6 +2079,10 @@ int lyap_set_recycle(lyap_ctx* ctx, int32_t nreg, int32_t s, const double* U, co
 static int build_recycle_impl(lyap_ctx* ctx, int32_t nseeds, const double* seeds, int32_t s);
 
 int lyap_build_recycle(lyap_ctx* ctx, int32_t nseeds, const double* seeds, int32_t s) {
+  if (ctx && mp_mode(ctx)) {
+    set_err(ctx, "lyap_build_recycle: recycle spaces need the FP64 engine (opts.mixed = 0)");
+    return LYAP_EINVAL;
+  }
   if (!ctx || nseeds < 1 || !seeds || s < 1) {
     set_err(ctx, "lyap_build_recycle: invalid arguments");
     return LYAP_EINVAL;

@@ -420,10 +420,11 @@ __global__ void __launch_bounds__(192, 1)
             if (pos < nver || pos >= nact || !ec.active) continue;  // VERIFY (exact path), inactive, Im lane
             const int slot = k1_slot(ep.a, pos);
             if (ep.a.phase[slot] != PH_ITER) continue;
-            double* dst = ep.a.Qb + (int64_t)slot * ep.a.qstride + (int64_t)(ep.a.m[slot] + 1) * ep.a.L;
+            const int64_t off = (int64_t)slot * ep.a.qstride + (int64_t)(ep.a.m[slot] + 1) * ep.a.L;
+            const K1Dst dst = ep.a.Qf ? K1Dst{nullptr, ep.a.Qf + off} : K1Dst{ep.a.Qb + off, nullptr};
             if (ec.pad) {
 #pragma unroll
-              for (int s = 0; s < EPI; ++s) dst[(int64_t)s * npad + m] = 0.0;
+              for (int s = 0; s < EPI; ++s) dst.put((int64_t)s * npad + m, 0.0);
               continue;
             }
             const double* x = ep.a.Xin + (int64_t)slot * ep.a.L;
@@ -445,8 +446,8 @@ __global__ void __launch_bounds__(192, 1)
                 }
                 const bool on = ep.a.mask[slot * EPI + s] != 0.0;
                 const double sg = ep.a.sigma[slot * EPI + s];
-                dst[(int64_t)s * npad + m] = on ? sg * xr[s] - yr : xr[s];
-                dst[(int64_t)s * npad + m + 1] = on ? sg * xi[s] - yi : xi[s];
+                dst.put((int64_t)s * npad + m, on ? sg * xr[s] - yr : xr[s]);
+                dst.put((int64_t)s * npad + m + 1, on ? sg * xi[s] - yi : xi[s]);
               }
             } else {  // real eigenvalue
               double xr[EPI];
@@ -459,7 +460,7 @@ __global__ void __launch_bounds__(192, 1)
                 for (int t = 0; t < EPI; ++t)
                   y += ec.blr[t] * (double)__uint_as_float(r[pp * KK + s * EPI + t]) + ec.fr[s][t] * xr[t];
                 const bool on = ep.a.mask[slot * EPI + s] != 0.0;
-                dst[(int64_t)s * npad + m] = on ? ep.a.sigma[slot * EPI + s] * xr[s] - y : xr[s];
+                dst.put((int64_t)s * npad + m, on ? ep.a.sigma[slot * EPI + s] * xr[s] - y : xr[s]);
               }
             }
           }
