@@ -15,7 +15,7 @@ timeout 600 python bench.py --config c5 --mixed 0 --steps 2 --warmup 3 --no-cpu-
 for r in 2 4 8; do timeout 600 python bench.py --emulate-rank 0/$r --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/${P}_emu_$r.log 2>&1; done
 timeout 900 python tools/ek_demo.py c3 c5 > gpurun_out/${P}_ek_demo.log 2>&1
 timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/${P}_reference.log 2>&1
-(cd tools/microbench && timeout 120 ./umma_tf32x3 4096 4736 4000) > gpurun_out/${P}_umma_micro.log 2>&1
+(cd tools/microbench && timeout 120 ./umma_tf32x3 4096 4736 4000 && timeout 120 ./umma_tf32x3 4096 4864 4000) > gpurun_out/${P}_umma_micro.log 2>&1
 timeout 1500 ncu --profile-from-start off --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
    --clock-control none -c 4000 --csv --log-file gpurun_out/${P}_launches_c5.csv \
    python tools/profile_step.py c5 > gpurun_out/${P}_ncu1.log 2>&1
