@@ -692,7 +692,7 @@ __global__ void __launch_bounds__(256) k_uapply(EngArgs a) {
 constexpr int DOT_IG = LYAP_DOT_IG;  // basis vectors per k_dots block (grid.z splits long cycles)
 template <typename QT = double>
 __global__ void __launch_bounds__(256) k_dots(EngArgs a) {
-  __shared__ double ws[RED_CE];
+  __shared__ __align__(16) double ws[RED_CE];
   __shared__ double qm[RED_CE];
   __shared__ double red[8];
   const int slot = blockIdx.y, chunk = blockIdx.x;
@@ -740,14 +740,58 @@ __global__ void __launch_bounds__(256) k_dots(EngArgs a) {
   const int i1 = min(m, i0 + DOT_IG - 1);
   const QT* w = qbase<QT>(a) + slot * qs + (int64_t)(m + 1) * a.L;
   const QT* qlast = qbase<QT>(a) + slot * qs + (int64_t)m * a.L;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lim = (int)((a.L - e0) < RED_CE ? (a.L - e0) : RED_CE);
+  if constexpr (sizeof(QT) == 4) {
+    // FP32 basis: 16-byte loads; w and q_m staged as float4 in shared memory (conflict-free), the products
+    // and sums in FP64.  lim is a multiple of 4 (L and the chunk start are).
+    float4* ws4 = reinterpret_cast<float4*>(ws);  // RED_CE floats of w, then RED_CE of q_m
+    float4* qm4 = ws4 + RED_CE / 4;
+    for (int i = threadIdx.x; i < RED_CE / 4; i += blockDim.x) {
+      const bool in = 4 * i < lim;
+      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+      ws4[i] = in ? reinterpret_cast<const float4*>(w + e0)[i] : z;
+      qm4[i] = in ? reinterpret_cast<const float4*>(qlast + e0)[i] : z;
+    }
+    __syncthreads();
+    const int lim4 = lim / 4;
+    for (int i = i0 + warp; i <= i1; i += 8) {
+      const float4* q = reinterpret_cast<const float4*>(qbase<QT>(a) + slot * qs + (int64_t)i * a.L + e0);
+      double d0 = 0.0, d1 = 0.0, g0 = 0.0, g1 = 0.0;
+      float4 x[RED_CE / 128];
+#pragma unroll
+      for (int u = 0; u < RED_CE / 128; ++u) {
+        const int j = lane + 32 * u;
+        x[u] = j < lim4 ? q[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < RED_CE / 128; ++u) {
+        const int j = lane + 32 * u;
+        const float4 wv = ws4[j], qv = qm4[j];
+        d0 = fma((double)x[u].x, (double)wv.x, d0);
+        d1 = fma((double)x[u].y, (double)wv.y, d1);
+        d0 = fma((double)x[u].z, (double)wv.z, d0);
+        d1 = fma((double)x[u].w, (double)wv.w, d1);
+        g0 = fma((double)x[u].x, (double)qv.x, g0);
+        g1 = fma((double)x[u].y, (double)qv.y, g1);
+        g0 = fma((double)x[u].z, (double)qv.z, g0);
+        g1 = fma((double)x[u].w, (double)qv.w, g1);
+      }
+      const double d = warp_sum(d0 + d1);
+      const double g = warp_sum(g0 + g1);
+      if (lane == 0) {
+        a.part[((int64_t)slot * (a.mmax + 2) + i) * a.nchunk + chunk] = d;
+        if (i < m) a.part2[((int64_t)slot * (a.mmax + 2) + i) * a.nchunk + chunk] = g;
+      }
+    }
+    return;
+  }
   for (int i = threadIdx.x; i < RED_CE; i += blockDim.x) {
     const int64_t e = e0 + i;
     ws[i] = e < a.L ? w[e] : 0.0;
     qm[i] = e < a.L ? qlast[e] : 0.0;
   }
   __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int lim = (int)((a.L - e0) < RED_CE ? (a.L - e0) : RED_CE);
   for (int i = i0 + warp; i <= i1; i += 8) {
     const QT* q = qbase<QT>(a) + slot * qs + (int64_t)i * a.L + e0;
     double d0 = 0.0, d1 = 0.0, g0 = 0.0, g1 = 0.0;
@@ -852,6 +896,51 @@ __global__ void __launch_bounds__(256) k_upd(EngArgs a) {
   QT* w = qbase<QT>(a) + slot * qs + (int64_t)(m + 1) * a.L;
   const QT* Q = qbase<QT>(a) + slot * qs;
   const int64_t e0 = (int64_t)chunk * RED_CE;
+  if constexpr (sizeof(QT) == 4) {
+    // FP32 basis: each thread owns 4 consecutive elements (one 16-byte load per basis vector)
+    static_assert(RED_CE == 4 * 256, "k_upd<float>: one float4 per thread and chunk");
+    const int64_t eb = e0 + 4 * threadIdx.x;
+    const bool okv = eb < a.L;  // L and e0 are multiples of 4
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    constexpr int UU = LYAP_UPD_UNROLL;
+    int i = 0;
+    if (okv) {
+      for (; i + UU <= m + 1; i += UU) {
+        float4 v[UU];
+#pragma unroll
+        for (int u = 0; u < UU; ++u) v[u] = *reinterpret_cast<const float4*>(Q + (int64_t)(i + u) * a.L + eb);
+#pragma unroll
+        for (int u = 0; u < UU; ++u) {
+          const double c = cfs[i + u];
+          acc[0] = fma(c, (double)v[u].x, acc[0]);
+          acc[1] = fma(c, (double)v[u].y, acc[1]);
+          acc[2] = fma(c, (double)v[u].z, acc[2]);
+          acc[3] = fma(c, (double)v[u].w, acc[3]);
+        }
+      }
+      for (; i <= m; ++i) {
+        const double c = cfs[i];
+        const float4 v = *reinterpret_cast<const float4*>(Q + (int64_t)i * a.L + eb);
+        acc[0] = fma(c, (double)v.x, acc[0]);
+        acc[1] = fma(c, (double)v.y, acc[1]);
+        acc[2] = fma(c, (double)v.z, acc[2]);
+        acc[3] = fma(c, (double)v.w, acc[3]);
+      }
+    }
+    double nrm = 0.0;
+    if (okv) {
+      float4 wv = *reinterpret_cast<const float4*>(w + eb);
+      wv.x = (float)((double)wv.x - acc[0]);
+      wv.y = (float)((double)wv.y - acc[1]);
+      wv.z = (float)((double)wv.z - acc[2]);
+      wv.w = (float)((double)wv.w - acc[3]);
+      *reinterpret_cast<float4*>(w + eb) = wv;
+      nrm = (double)wv.x * wv.x + (double)wv.y * wv.y + (double)wv.z * wv.z + (double)wv.w * wv.w;
+    }
+    nrm = block_sum(nrm, red);
+    if (threadIdx.x == 0) a.part3[((int64_t)slot * a.nchunk + chunk) * 3] = nrm;
+    return;
+  }
   // each thread owns 4 elements of the chunk; the basis loop issues 4 independent loads per vector
   constexpr int EPT = RED_CE / 256;
   double acc[EPT];

@@ -32,7 +32,13 @@ static float tf32_host(float f) {
   return r;
 }
 
+static CUtensorMap tmap_sw(const float* p, uint64_t inner, uint64_t outer, uint32_t bi, uint32_t bo,
+                           CUtensorMapSwizzle sw);
 static CUtensorMap tmap(const float* p, uint64_t inner, uint64_t outer, uint32_t bi, uint32_t bo) {
+  return tmap_sw(p, inner, outer, bi, bo, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+static CUtensorMap tmap_sw(const float* p, uint64_t inner, uint64_t outer, uint32_t bi, uint32_t bo,
+                           CUtensorMapSwizzle sw) {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
     cudaDriverEntryPointQueryResult q;
@@ -46,7 +52,7 @@ static CUtensorMap tmap(const float* p, uint64_t inner, uint64_t outer, uint32_t
   cuuint32_t box[2] = {bi, bo};
   cuuint32_t es[2] = {1, 1};
   CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)p, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     printf("cuTensorMapEncodeTiled failed %d\n", (int)r);
     exit(1);
@@ -133,9 +139,11 @@ int main(int argc, char** argv) {
   variant(lyap::k1_umma_tf32x3<192, 2>, 192, lyap::UmCfg<192, 2>::SMEM, "192x2");
   variant(lyap::k1_umma_tf32x3<64, 4>, 64, lyap::UmCfg<64, 4>::SMEM, "64x4");
   variant(lyap::k1_umma_tf32x3<256, 2>, 256, lyap::UmCfg<256, 2>::SMEM, "256x2");
-  auto pvariant = [&](auto kern, int BN, int smem, const char* name) {
+  auto pvariant = [&](auto kern, int BN, int smem, const char* name, int BK = 32) {
     if (ncol % BN) return;
-    CUtensorMap tb = tmap(dB, npad, 2 * (uint64_t)ncol, lyap::UM_BK, BN);
+    const CUtensorMapSwizzle sw = BK == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+    CUtensorMap tb = tmap_sw(dB, npad, 2 * (uint64_t)ncol, BK, BN, sw);
+    CUtensorMap ta = tmap_sw(dA, 2 * (uint64_t)npad, npad, BK, lyap::UM_BM, sw);
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int nsm = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
@@ -172,6 +180,9 @@ int main(int argc, char** argv) {
   };
   pvariant(lyap::k1_umma_persistent<256, 2, 0>, 256, lyap::UmCfg<256, 2>::SMEM, "256x2");
   pvariant(lyap::k1_umma_persistent<128, 3, 0>, 128, lyap::UmCfg<128, 3>::SMEM, "128x3");
+  pvariant(lyap::k1_umma_persistent<256, 4, 0, 16>, 256, lyap::UmCfg<256, 4, 16>::SMEM, "256x4 bk16", 16);
+  pvariant(lyap::k1_umma_persistent<128, 6, 0, 16>, 128, lyap::UmCfg<128, 6, 16>::SMEM, "128x6 bk16", 16);
+  pvariant(lyap::k1_umma_persistent<256, 3, 0, 16>, 256, lyap::UmCfg<256, 3, 16>::SMEM, "256x3 bk16", 16);
   // cuBLAS: three TF32 GEMMs (column-major C (npad x ncol, ld npad) = A^T(op T) * Bt)
   cublasHandle_t h;
   cublasCreate(&h);
