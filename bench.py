@@ -34,6 +34,16 @@ FP64_PEAK_TFLOPS = 37.0   # measured: DMMA m8n8k4 burst, profiles/r01_fp64_peaks
 TF32_PER_BF16 = 1.1 / 2.25  # B200_PROFILING.md nominal dense tf32 / bf16 tensor peaks
 
 
+def bf16_peak():
+    """FP16/BF16 dense tensor peak: MEASURED_PEAKS.json bf16 burst (fp16 runs at the bf16 rate)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            bf16 = float(json.load(f)["bf16_tflops"])
+        return bf16, f"MEASURED_PEAKS.json bf16_tflops {bf16:.1f} (burst; dense fp16 = bf16 rate)"
+    except (OSError, KeyError, ValueError):
+        return 2250.0, "B200_PROFILING.md nominal dense bf16/fp16 2.25 PFLOP/s (MEASURED_PEAKS.json absent)"
+
+
 def tf32_peak():
     """TF32 dense tensor peak: MEASURED_PEAKS.json bf16 burst x the guide's nominal tf32/bf16 ratio."""
     try:
@@ -361,15 +371,21 @@ def main():
         # steps; its tensor work = 3 TF32 passes x 2 n^2 k^2 per ITER vector.  The timed region of each
         # launch (CUDA events on the engine stream) spans that kernel, its fused epilogue, and the exact
         # DMMA GEMM of the VERIFY vectors on the side stream (joined).
-        peak, psrc = tf32_peak()
+        mode = P.info["mixed_mode"]
+        if mode == 3:  # 3xFP16 on tcgen05: the FP16 dense peak = the measured bf16 one (same rate)
+            peak, psrc = bf16_peak()
+            dt = "f16 (3xFP16: hi/lo split with power-of-two scales, 3 passes, FP32 accumulation in TMEM)"
+        else:
+            peak, psrc = tf32_peak()
+            dt = "tf32 (3xTF32: hi/lo split, 3 passes, FP32 accumulation in TMEM)"
         it_vec = st["k1_vectors"] - st["k1_exact_vectors"]
         fl = 3.0 * 2.0 * W.n ** 2 * W.k ** 2 * it_vec
         a_tf = fl / (st["k1_ms"] * 1e-3) / 1e12 if st["k1_ms"] > 0 else 0.0
         tfile = os.path.join(ROOT, "profiles", f"umma_traffic_{args.config}.json")
         utraffic = json.load(open(tfile)).get("bytes_per_launch") if os.path.exists(tfile) else None
-        roof = {"bound": "tensor", "dtype": "tf32 (3xTF32: hi/lo split, 3 passes, FP32 accumulation in TMEM)",
+        roof = {"bound": "tensor", "dtype": dt,
                 "achieved": a_tf, "peak": peak, "unit": "TFLOP/s", "frac": a_tf / peak, "traffic": utraffic,
-                "kernel": "k1_umma_persistent (tcgen05.mma kind::tf32, TMA, TMEM; K1 epilogue fused)",
+                "kernel": "k1_umma_persistent (tcgen05.mma, TMA, TMEM; K1 epilogue fused)",
                 "peak_source": psrc, "avg_launch_ms": avg_k1_ms, "launches": st["k1_launches"],
                 "k1_share_of_step": st["k1_ms"] / ms if ms > 0 else None,
                 "work": "3 x 2 n^2 k^2 flops per ITER vector; VERIFY vectors (exact FP64, k1_dgemm on a side "
@@ -420,7 +436,7 @@ def main():
                                                      "recycle_build_ms": recycle_ms,
                                                      "applies_per_v": st["k1_vectors"] / (len(idx) * args.steps),
                                                      "exact_applies_per_v": st["k1_exact_vectors"] / (len(idx) * args.steps),
-                                                     "mixed": P.mixed,
+                                                     "mixed": P.mixed, "mixed_mode": P.info["mixed_mode"],
                                                      "shard_cost_max_over_mean": balance,
                                                      "coarse": P.info["coarse"],
                                                      "coarse_build_ms": P.info["coarse_build_ms"],

@@ -84,8 +84,9 @@ typedef struct {
                           -1 (default) auto: 32 when n k >= 2000, else off; 0 off; > 0 that size
                           (multiple of 8, <= 256).  Recycle spaces are not used together with it. */
   int32_t mixed;       /* mixed-precision iterative refinement: the Krylov steps apply
-                          the dense Cauchy part of T with an FP32-accurate tensor-core GEMM (3xTF32,
-                          operands split hi + lo), every cycle ends once its estimated residual has
+                          the dense Cauchy part of T with an FP32-accurate tensor-core GEMM (3xFP16 with
+                          power-of-two scales, or 3xTF32; operands split hi + lo), every cycle ends once
+                          its estimated residual has
                           dropped by mixed_eta, and every cycle starts from the TRUE residual of the
                           exact FP64 operator (DMMA GEMM), so the stopping test (tol, reading R14)
                           is unchanged.  -1 (default) auto: on when n > 1536 (the large-tile
@@ -107,6 +108,9 @@ typedef struct {
                               sum_t |v_t| wcost[t] (opts.schedule; multi-GPU shard balancing) */
   int32_t coarse;          /* size of the two-level preconditioner's coarse space once built (0: none) */
   double coarse_build_ms;  /* device time of its build (explicit T, randomized SVD, T Z, Gram blocks) */
+  int32_t mixed_mode;      /* the Krylov steps' T-apply: 0 FP64 (DMMA); 3 3xFP16 on tcgen05 (npad a multiple
+                              of 128; the default under mixed precision); 1 3xTF32 (otherwise, or
+                              LYAP_MP_GEMM=tf32x3); 2 a one-plane cuBLAS variant (diagnostics) */
 } lyap_info;
 
 typedef struct {

@@ -37,7 +37,7 @@ class Info(C.Structure):
                 ("t0", C.c_double), ("cond_S", C.c_double), ("min_lam_sum", C.c_double),
                 ("max_abs_lam", C.c_double), ("setup_ms", C.c_double), ("batch", C.c_int32),
                 ("max_dim", C.c_int32), ("wcost", C.c_double * LYAP_KMAX), ("coarse", C.c_int32),
-                ("coarse_build_ms", C.c_double)]
+                ("coarse_build_ms", C.c_double), ("mixed_mode", C.c_int32)]
 
 
 class Stats(C.Structure):

@@ -24,7 +24,9 @@ struct Basis {
   double* Qr = nullptr;    // S_r^{-1} Q S_r^{-T} (nterms matrices for a v-linear Q)
   double* Er = nullptr;    // S_r^T E S_r
   float* Lf32 = nullptr;   // mixed precision: [hi | lo] float planes of Lf (npad x 2 npad), built on first use
-  int lf32_mode = 0;       // split mode Lf32 was built with (1: 3xTF32 hi/lo, 2: one float plane)
+  int lf32_mode = 0;       // split mode Lf32 was built with (1: 3xTF32 hi/lo, 2: one float plane,
+                           // 3: 3xFP16 hi/lo half planes of 2^lf_eA Lf in the same buffer)
+  int lf_eA = 0;
   ~Basis() {
     cudaSetDevice(device);
     for (double* p : {lam, Lf, Sr, Sinv, Qr, Er})
@@ -72,6 +74,8 @@ struct Engine {
   float *Bop32 = nullptr, *U32 = nullptr;         // mixed precision: groups x 2 npad x ncol (lo | hi), groups x npad x ncol
   int mp = 0;                                     // mixed-precision mode the buffers were made for
   int* umctr = nullptr;                           // tcgen05 GEMM tile counters (2 per slot group)
+  float *xmax = nullptr, *bmax = nullptr;         // 3xFP16: per slot x parameter max |X_t|; per s max |B^r_s|
+  float* colscale = nullptr;                      // 3xFP16: per GEMM column unscale factor (groups x ncol)
   double *Xin = nullptr, *X = nullptr;            // b x L
   double *rhs = nullptr, *t0s = nullptr;          // qlin: per-slot G0(v) (b x L) and t0(v) (b)
   double* Qb = nullptr;                           // b x (mmax+1) x L  (unnormalised basis), FP64 engine
@@ -160,6 +164,7 @@ struct lyap_ctx {
   CUtensorMap um_ta{}, um_tb[4]{};
   const void* um_ta_ptr = nullptr;
   const void* um_tb_ptr[4] = {};
+  int um_ta_mode = 0, um_tb_mode[4] = {};
   int64_t um_tb_ncol[4] = {};
   cudaEvent_t mpfork[4] = {}, mpjoin[4] = {};
 };

@@ -10,6 +10,8 @@
 // on the DMMA tensor pipe (mma.sync.m8n8k4.f64), with a prologue kernel that builds the B operand
 // (B^r o X outer products) and an epilogue kernel that contracts over t and adds T_d.
 #pragma once
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 
 namespace lyap {
@@ -45,6 +47,12 @@ struct K1Args {
   // FP64 apply through the DMMA GEMM), positions [*nver, *nactive) ITER slots (apply through the
   // FP32-accurate tensor-core GEMM on the float planes B32 / U32).  nver == null: all FP64.
   const int* nver;
+  // MP = 3 (3xFP16): power-of-two operand scales -- per slot and parameter t the max |X_t| (xmax, from
+  // k_xmax), per s max |B^r_s| (bmax), the exponent of Lf's scale (eA); k1_gen writes each column's
+  // unscale factor 2^-(eA + e_n) to colscale
+  const float *xmax, *bmax;
+  int eA;
+  float* colscale;
 };
 
 // float split of a double for the 3xTF32 GEMM: hi = x rounded to TF32 (10-bit mantissa), lo = x - hi
@@ -87,6 +95,7 @@ template <int K, int MP = 0>
 __global__ void __launch_bounds__(256) k1_gen(K1Args a, const double* __restrict__ bhr, int npad,
                                                int two_np, double* __restrict__ Bop, int64_t ncol,
                                                float* __restrict__ B32 = nullptr) {
+  __half* B16 = reinterpret_cast<__half*>(B32);  // MP = 3: the planes in FP16
   constexpr int TS = K1Tile<K>::TS, NC = K1Tile<K>::NC, TC = K1_TILE_C;
   const int nact = k1_nact(a);
   const int nver = MP ? *a.nver : nact;
@@ -122,10 +131,21 @@ __global__ void __launch_bounds__(256) k1_gen(K1Args a, const double* __restrict
       const double val = k1_bval<K>(xs[sl][t], bs, r, s, i0 + r < two_np);
       const int64_t nn = (int64_t)(s0 + sl) * K * K + col % (K * K);
       if (s0 + sl < nver) Bop[(int64_t)(i0 + r) * ncol + nn] = val;  // FP64 operand of the exact apply
-      const float f = (float)val;
-      const float hi = MP == 1 ? tf32_rn(f) : f;
-      B32[(ncol + nn) * npad + i0 + r] = hi;
-      if (MP == 1) B32[nn * npad + i0 + r] = (float)(val - (double)hi);
+      if constexpr (MP == 3) {
+        // column scale 2^e: the bound max|B^r_s| max|X_t| (x 1.5 for the folded complex product) -> 2^13
+        const float bound = a.bmax[s] * a.xmax[k1_slot(a, s0 + sl) * K + t] * 1.5f;
+        const int e = bound > 0.f ? 13 - (int)ceilf(log2f(bound)) : 0;
+        const double xs_ = ldexp(val, e);
+        const __half hi = __double2half(xs_);
+        B16[(ncol + nn) * npad + i0 + r] = hi;
+        B16[nn * npad + i0 + r] = __double2half(xs_ - (double)__half2float(hi));
+        if (blockIdx.x == 0 && r == 0) a.colscale[nn] = ldexpf(1.f, -(a.eA + e));
+      } else {
+        const float f = (float)val;
+        const float hi = MP == 1 ? tf32_rn(f) : f;
+        B32[(ncol + nn) * npad + i0 + r] = hi;
+        if (MP == 1) B32[nn * npad + i0 + r] = (float)(val - (double)hi);
+      }
     }
   }
 }
@@ -142,6 +162,75 @@ __global__ void k_split_Lf(const double* __restrict__ Lf, int64_t npad, float* _
     const float hi = MP == 1 ? tf32_rn(f) : f;
     Lf32[j * 2 * npad + i] = hi;
     Lf32[j * 2 * npad + npad + i] = MP == 1 ? (float)(x - (double)hi) : 0.f;
+  }
+}
+
+// 3xFP16: Lf16 = [hi | lo] half planes of 2^eA Lf (npad x 2 npad row-major)
+__global__ void k_split_Lf16(const double* __restrict__ Lf, int64_t npad, int eA, __half* __restrict__ Lf16) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < npad * npad;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / npad, i = e % npad;
+    const double x = ldexp(Lf[e], eA);
+    const __half hi = __double2half(x);
+    Lf16[j * 2 * npad + i] = hi;
+    Lf16[j * 2 * npad + npad + i] = __double2half(x - (double)__half2float(hi));
+  }
+}
+// max |x| over cnt doubles into *out (one block; float result, rounded up)
+__global__ void k_absmax(const double* __restrict__ x, int64_t cnt, float* __restrict__ out) {
+  __shared__ double red[32];
+  double m = 0.0;
+  for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) m = fmax(m, fabs(x[i]));
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
+    *out = __double2float_ru(fmax(m, red[0]));
+  }
+}
+// per-parameter max |B^r_s| (complex modulus over a pair's two coordinates): bmax[s], one block per s
+__global__ void k_bmax(const double* __restrict__ bhr, int64_t npad, int k, int two_np, float* __restrict__ bmax) {
+  __shared__ double red[32];
+  const int s = blockIdx.x;
+  double m = 0.0;
+  for (int64_t c = threadIdx.x; c < npad; c += blockDim.x) {
+    const double v = bhr[c * k + s];
+    const double w = (c < two_np) ? bhr[(c ^ 1) * k + s] : 0.0;
+    m = fmax(m, sqrt(v * v + w * w));
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
+    bmax[s] = __double2float_ru(fmax(m, red[0]));
+  }
+}
+// per active position: xmax[slot * K + t] = max_c |Xin[slot][t][c]| (one block per position)
+template <int K>
+__global__ void __launch_bounds__(256) k_xmax(K1Args a, int npad, float* __restrict__ xmax) {
+  __shared__ double red[K][8];
+  const int pos = blockIdx.x;
+  if (pos >= k1_nact(a)) return;
+  const int slot = k1_slot(a, pos);
+  const double* x = a.Xin + (int64_t)slot * a.L;
+  double m[K];
+#pragma unroll
+  for (int t = 0; t < K; ++t) m[t] = 0.0;
+  for (int c = threadIdx.x; c < npad; c += blockDim.x)
+#pragma unroll
+    for (int t = 0; t < K; ++t) m[t] = fmax(m[t], fabs(x[(int64_t)t * npad + c]));
+#pragma unroll
+  for (int t = 0; t < K; ++t) {
+    for (int o = 16; o > 0; o >>= 1) m[t] = fmax(m[t], __shfl_xor_sync(0xffffffffu, m[t], o));
+    if ((threadIdx.x & 31) == 0) red[t][threadIdx.x >> 5] = m[t];
+  }
+  __syncthreads();
+  if (threadIdx.x < K) {
+    double v = 0.0;
+    for (int w = 0; w < 8; ++w) v = fmax(v, red[threadIdx.x][w]);
+    xmax[slot * K + threadIdx.x] = __double2float_ru(v);
   }
 }
 

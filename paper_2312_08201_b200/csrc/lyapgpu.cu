@@ -135,7 +135,7 @@ void upload_seeds(lyap_ctx* ctx) {
 
 // ------------------------------------------------------------------ engine allocation
 void free_engine(Engine& g, bool keep_order = true) {
-  void* ps[] = {g.Bop, g.U, g.Bop32, g.U32, g.umctr, g.Xin, g.X, g.Qb, g.Qf, g.Minv, g.sigma, g.mask, g.eta, g.H, g.e, g.y,
+  void* ps[] = {g.Bop, g.U, g.Bop32, g.U32, g.umctr, g.xmax, g.bmax, g.colscale, g.Xin, g.X, g.Qb, g.Qf, g.Minv, g.sigma, g.mask, g.eta, g.H, g.e, g.y,
                 g.bnorm, g.part, g.part3, g.phase, g.m, g.vidx, g.applies, g.restarts, g.ctrl,
                 g.part2, g.Gq, g.cf, g.Hraw, g.rhs, g.t0s, g.Zb, g.Rbuf, g.Yz, g.Cc, g.Wc, g.Einv};
   for (void* p : ps) dfree(p);
@@ -227,7 +227,10 @@ int mp_mode(const lyap_ctx* ctx) {
   if (!(o > 0 || (o < 0 && ctx->seed.n > SMALL_N))) return 0;
   const char* ev = std::getenv("LYAP_MP_GEMM");
   const bool plane = ev && (!std::strcmp(ev, "bf16x9") || !std::strcmp(ev, "tf32") || !std::strcmp(ev, "fp32"));
-  return plane ? 2 : 1;
+  if (plane) return 2;
+  // 3xFP16 on the tcgen05 kernel (mode 3) needs npad % 128 == 0; LYAP_MP_GEMM=tf32x3 / cublas: 3xTF32
+  const bool f16 = !(ev && (!std::strcmp(ev, "tf32x3") || !std::strcmp(ev, "cublas")));
+  return (f16 && ctx->seed.npad % 128 == 0) ? 3 : 1;
 }
 // the 3xTF32 product runs on the repo's tcgen05 kernel (umma.cuh); LYAP_MP_GEMM=cublas: three cuBLAS
 // TF32 GEMMs instead (measurement alternative)
@@ -243,10 +246,10 @@ int um_bn() {
   }();
   return bn;
 }
-CUtensorMap make_tmap_f32(lyap_ctx* ctx, const float* p, uint64_t inner, uint64_t outer, uint32_t box_inner,
-                          uint32_t box_outer) {
-  // the swizzle spans one box row: 32 fp32 = 128 B, 16 fp32 = 64 B (must match the UMMA descriptors)
-  const CUtensorMapSwizzle sw = box_inner == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+CUtensorMap make_tmap_f32(lyap_ctx* ctx, const void* p, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                          uint32_t box_outer, int eb = 4) {
+  // the swizzle spans one box row: 128 B or 64 B (must match the UMMA descriptors); eb = element bytes
+  const CUtensorMapSwizzle sw = box_inner * eb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -260,10 +263,10 @@ CUtensorMap make_tmap_f32(lyap_ctx* ctx, const float* p, uint64_t inner, uint64_
   }
   CUtensorMap m;
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {inner * 4};
+  cuuint64_t strides[1] = {inner * (uint64_t)eb};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t es[2] = {1, 1};
-  if (encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)p, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+  if (encode(&m, eb == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (void*)p, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
              sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
       CUDA_SUCCESS) {
     set_err(ctx, "cuTensorMapEncodeTiled failed");
@@ -287,10 +290,21 @@ void ensure_lf32(lyap_ctx* ctx, int mode) {
   const int64_t np = ctx->seed.npad;
   B.Lf32 = dalloc<float>(ctx, (size_t)np * 2 * np, false);
   B.lf32_mode = mode;
-  if (mode == 1)
+  if (mode == 3) {  // 3xFP16: one power-of-two scale for all of Lf (max |Lf| -> 2^14)
+    float* dmax = dalloc<float>(ctx, 1);
+    k_absmax<<<1, 1024, 0, ctx->stream>>>(B.Lf, np * np, dmax);
+    LAUNCHED();
+    float hmax = 0.f;
+    CK(cudaMemcpyAsync(&hmax, dmax, sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    dfree(dmax);
+    B.lf_eA = hmax > 0.f ? 14 - (int)std::ceil(std::log2((double)hmax)) : 0;
+    k_split_Lf16<<<1184, 256, 0, ctx->stream>>>(B.Lf, np, B.lf_eA, reinterpret_cast<__half*>(B.Lf32));
+  } else if (mode == 1) {
     k_split_Lf<1><<<1184, 256, 0, ctx->stream>>>(B.Lf, np, B.Lf32);
-  else
+  } else {
     k_split_Lf<2><<<1184, 256, 0, ctx->stream>>>(B.Lf, np, B.Lf32);
+  }
   LAUNCHED();
 }
 
@@ -321,6 +335,13 @@ void ensure_engine(lyap_ctx* ctx, int b, int mmax) {
     g.Bop32 = dalloc<float>(ctx, (size_t)2 * s.npad * colcap);
     g.U32 = dalloc<float>(ctx, (size_t)s.npad * colcap);
     g.umctr = dalloc<int>(ctx, 8);  // tile counters of the persistent tcgen05 GEMM (2 per slot group), zeroed
+    if (mp == 3) {
+      g.xmax = dalloc<float>(ctx, (size_t)b * s.k);
+      g.bmax = dalloc<float>(ctx, s.k);
+      g.colscale = dalloc<float>(ctx, (size_t)colcap);
+      k_bmax<<<(unsigned)s.k, 256, 0, ctx->stream>>>(s.bhr, s.npad, (int)s.k, (int)(2 * s.npairs), g.bmax);
+      LAUNCHED();
+    }
   }
   g.Xin = dalloc<double>(ctx, (size_t)b * g.L);
   g.X = dalloc<double>(ctx, (size_t)b * g.L);
@@ -425,34 +446,39 @@ int num_sms() {
   }
   return n;
 }
-template <int BN, int ST, int BK>
+template <int BN, int ST, int BK, int EB = 4>
 void launch_umma(lyap_ctx* ctx, int epi, const CUtensorMap& ta, const CUtensorMap& tb, float* U32, int npad, int Nc,
-                 int Kd, const int* nactive, int cpa, const K1EpiArgs& ep, cudaStream_t st, int* tctr) {
+                 int Kd, const int* nactive, int cpa, const K1EpiArgs& ep, cudaStream_t st, int* tctr,
+                 const float* colscale = nullptr) {
   const int tiles = (Nc / BN) * (npad / UM_BM);
   const dim3 grid((unsigned)std::max(1, std::min(num_sms(), tiles)));
-  constexpr int SM = UmCfg<BN, ST, BK>::SMEM;
+  constexpr int SM = UmCfg<BN, ST, BK, EB>::SMEM;
   switch (epi) {
     case 1:
-      k1_umma_persistent<BN, ST, 1, BK><<<grid, 192, SM, st>>>(ta, tb, U32, npad, Nc, Kd, nactive, cpa, ep, tctr);
+      k1_umma_persistent<BN, ST, 1, BK, EB><<<grid, 192, SM, st>>>(ta, tb, U32, npad, Nc, Kd, nactive, cpa, ep, tctr,
+                                                                   colscale);
       break;
     case 2:
-      k1_umma_persistent<BN, ST, 2, BK><<<grid, 192, SM, st>>>(ta, tb, U32, npad, Nc, Kd, nactive, cpa, ep, tctr);
+      k1_umma_persistent<BN, ST, 2, BK, EB><<<grid, 192, SM, st>>>(ta, tb, U32, npad, Nc, Kd, nactive, cpa, ep, tctr,
+                                                                   colscale);
       break;
     case 4:
-      k1_umma_persistent<BN, ST, 4, BK><<<grid, 192, SM, st>>>(ta, tb, U32, npad, Nc, Kd, nactive, cpa, ep, tctr);
+      k1_umma_persistent<BN, ST, 4, BK, EB><<<grid, 192, SM, st>>>(ta, tb, U32, npad, Nc, Kd, nactive, cpa, ep, tctr,
+                                                                   colscale);
       break;
     default:
-      k1_umma_persistent<BN, ST, 0, BK><<<grid, 192, SM, st>>>(ta, tb, U32, npad, Nc, Kd, nactive, cpa, ep, tctr);
+      k1_umma_persistent<BN, ST, 0, BK, EB><<<grid, 192, SM, st>>>(ta, tb, U32, npad, Nc, Kd, nactive, cpa, ep, tctr,
+                                                                   colscale);
   }
   LAUNCHED();
 }
-template <int BN, int ST, int BK>
+template <int BN, int ST, int BK, int EB = 4>
 void set_umma_attrs(lyap_ctx* ctx) {
-  constexpr int SM = UmCfg<BN, ST, BK>::SMEM;
-  CK(cudaFuncSetAttribute(k1_umma_persistent<BN, ST, 0, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM));
-  CK(cudaFuncSetAttribute(k1_umma_persistent<BN, ST, 1, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM));
-  CK(cudaFuncSetAttribute(k1_umma_persistent<BN, ST, 2, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM));
-  CK(cudaFuncSetAttribute(k1_umma_persistent<BN, ST, 4, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM));
+  constexpr int SM = UmCfg<BN, ST, BK, EB>::SMEM;
+  CK(cudaFuncSetAttribute(k1_umma_persistent<BN, ST, 0, BK, EB>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM));
+  CK(cudaFuncSetAttribute(k1_umma_persistent<BN, ST, 1, BK, EB>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM));
+  CK(cudaFuncSetAttribute(k1_umma_persistent<BN, ST, 2, BK, EB>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM));
+  CK(cudaFuncSetAttribute(k1_umma_persistent<BN, ST, 4, BK, EB>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM));
 }
 
 void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, cudaEvent_t evb = nullptr, cudaEvent_t eve = nullptr,
@@ -466,7 +492,8 @@ void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, cudaEvent_t evb 
   // mixed precision with the tcgen05 kernel and k = 1, 2, 4: both GEMMs carry the K1 epilogue (the
   // DMMA one for the VERIFY positions, the tcgen05 one for the ITER positions), k1_epi is not launched
   const bool fuse_mp =
-      mp == 1 && a.mode == 1 && mp_umma() && s.npad % UM_BM == 0 && (s.k == 1 || s.k == 2 || s.k == 4);
+      (mp == 1 || mp == 3) && a.mode == 1 && mp_umma() && s.npad % UM_BM == 0 &&
+      (s.k == 1 || s.k == 2 || s.k == 4);
   static const int fmask = [] {  // LYAP_MP_FUSE (diagnostics): bit 0 tcgen05 epilogue, bit 1 DMMA epilogue
     const char* ev = std::getenv("LYAP_MP_FUSE");
     return ev ? std::atoi(ev) : 3;
@@ -476,7 +503,18 @@ void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, cudaEvent_t evb 
   float* U32 = mp ? g.U32 + (size_t)group * s.npad * g.ncol : nullptr;
   K_DISPATCH(s.k, {
     dim3 grid((unsigned)(s.npad / K1_TILE_C), (unsigned)((a.nslot + K1Tile<KK>::TS - 1) / K1Tile<KK>::TS));
-    if (mp == 1)
+    if (mp == 3) {
+      // per-position max |X_t| first: the FP16 column scales (k1_gen) need it
+      // (slot indices are local to the slot group: each group has its own xmax rows)
+      float* xm = g.xmax + (size_t)group * ((g.b + g.groups - 1) / g.groups) * s.k;
+      k_xmax<KK><<<(unsigned)a.nslot, 256, 0, st>>>(a, (int)s.npad, xm);
+      K1Args a3 = a;
+      a3.xmax = xm;
+      a3.bmax = g.bmax;
+      a3.eA = ctx->basis->lf_eA;
+      a3.colscale = g.colscale + (size_t)group * g.ncol;
+      k1_gen<KK, 3><<<grid, K1_THREADS, 0, st>>>(a3, s.bhr, (int)s.npad, two_np, g.Bop, g.ncol, B32);
+    } else if (mp == 1)
       k1_gen<KK, 1><<<grid, K1_THREADS, 0, st>>>(a, s.bhr, (int)s.npad, two_np, g.Bop, g.ncol, B32);
     else if (mp == 2)
       k1_gen<KK, 2><<<grid, K1_THREADS, 0, st>>>(a, s.bhr, (int)s.npad, two_np, g.Bop, g.ncol, B32);
@@ -518,22 +556,30 @@ void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, cudaEvent_t evb 
     CK(cudaEventRecord(ctx->mpjoin[group], ss));
     const int Nc = (int)g.ncol, M = (int)s.npad;
     const float* A32 = ctx->basis->Lf32;  // row-major npad x 2 npad: [hi | lo]
-    if (mp == 1 && mp_umma() && s.npad % UM_BM == 0) {
+    if ((mp == 1 || mp == 3) && mp_umma() && s.npad % UM_BM == 0) {
       // tcgen05 3xTF32 GEMM (umma.cuh): U32t = A_hi B_lo + A_lo B_hi + A_hi B_hi in one TMEM accumulator
-      const uint32_t bk = um_bn() == 128 ? 32u : (uint32_t)UM_BKE;
-      if (ctx->um_ta_ptr != A32) {
-        ctx->um_ta = make_tmap_f32(ctx, A32, 2 * (uint64_t)s.npad, (uint64_t)s.npad, bk, UM_BM);
+      // 3xFP16: 32 half per 64-byte row; 3xTF32: 16 (or 32 for the 128-wide alternative) floats
+      const int eb = mp == 3 ? 2 : 4;
+      const uint32_t bk = mp == 3 ? 32u : (um_bn() == 128 ? 32u : (uint32_t)UM_BKE);
+      const uint32_t bn = mp == 3 ? (uint32_t)UM_BN : (uint32_t)um_bn();
+      if (ctx->um_ta_ptr != A32 || ctx->um_ta_mode != mp) {
+        ctx->um_ta = make_tmap_f32(ctx, A32, 2 * (uint64_t)s.npad, (uint64_t)s.npad, bk, UM_BM, eb);
         ctx->um_ta_ptr = A32;
+        ctx->um_ta_mode = mp;
       }
-      if (ctx->um_tb_ptr[group] != B32 || ctx->um_tb_ncol[group] != g.ncol) {
-        ctx->um_tb[group] = make_tmap_f32(ctx, B32, (uint64_t)s.npad, 2 * (uint64_t)g.ncol, bk, (uint32_t)um_bn());
+      if (ctx->um_tb_ptr[group] != B32 || ctx->um_tb_ncol[group] != g.ncol || ctx->um_tb_mode[group] != mp) {
+        ctx->um_tb[group] = make_tmap_f32(ctx, B32, (uint64_t)s.npad, 2 * (uint64_t)g.ncol, bk, bn, eb);
+        ctx->um_tb_mode[group] = mp;
         ctx->um_tb_ptr[group] = B32;
         ctx->um_tb_ncol[group] = g.ncol;
       }
       const int Kd = (int)std::min<int64_t>(roundup(s.n, 32), s.npad);  // zero rows skipped (multiple of both BKs)
       K1EpiArgs ep{a, s.btl, s.F, s.g0, (int)s.npad, two_np, (int)s.npairs, (int)s.n};
       const int cpa = (int)(s.k * s.k), epi = fuse_um ? (int)s.k : 0;
-      if (um_bn() == 128)
+      if (mp == 3)
+        launch_umma<UM_BN, UM_STAGES, 32, 2>(ctx, epi, ctx->um_ta, ctx->um_tb[group], U32, (int)s.npad, Nc, Kd, a.nactive,
+                                             cpa, ep, st, g.umctr + 2 * group, g.colscale + (size_t)group * g.ncol);
+      else if (um_bn() == 128)
         launch_umma<128, 3, 32>(ctx, epi, ctx->um_ta, ctx->um_tb[group], U32, (int)s.npad, Nc, Kd, a.nactive, cpa, ep, st,
                             g.umctr + 2 * group);
       else
@@ -633,7 +679,7 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   a.tol_inner = 0.5 * ctx->opts.tol;
   const int mp = record ? 0 : mp_mode(ctx);
   a.eta_rel = mp ? ctx->opts.mixed_eta : 0.0;
-  if (mp) ensure_lf32(ctx, mp);
+  if (mp) ensure_lf32(ctx, mp);  // (3xFP16: the half planes, in the same buffer)
   a.t0 = s.t0;
   a.nterms = s.qlin ? s.nterms : 0;
   a.t0t = s.t0t;
@@ -1398,6 +1444,7 @@ static int setup_core(int64_t n, int64_t k, const double* A0, const double* Bl, 
     set_smem_attrs<V_BM, V_BN, V_WM, V_WN, V_ST, V_BK>(ctx);
     set_umma_attrs<UM_BN, UM_STAGES, UM_BKE>(ctx);
     set_umma_attrs<128, 3, 32>(ctx);
+    set_umma_attrs<UM_BN, UM_STAGES, 32, 2>(ctx);
     cudaStream_t st = ctx->stream;
     CK(cudaEventRecord(ctx->ev0, st));
     Seed& s = ctx->seed;
@@ -2340,7 +2387,7 @@ static int apply_C_impl(lyap_ctx* ctx, int64_t nvec, const double* X, const doub
     set_err(ctx, "lyap_apply_C: invalid arguments");
     return LYAP_EINVAL;
   }
-  if (mixed && mp_mode(ctx) != 1) {
+  if (mixed && mp_mode(ctx) != 1 && mp_mode(ctx) != 3) {
     set_err(ctx, "lyap_apply_C_mixed: mixed precision is off for this context (opts.mixed)");
     return LYAP_EINVAL;
   }
@@ -2349,7 +2396,8 @@ static int apply_C_impl(lyap_ctx* ctx, int64_t nvec, const double* X, const doub
     cudaStream_t st = (cudaStream_t)cuda_stream;
     const int b = auto_batch(ctx, std::max<int64_t>(nvec, 1));
     ensure_engine(ctx, std::max(b, ctx->eng.b), ctx->eng.mmax > 0 ? ctx->eng.mmax : auto_mmax(ctx));
-    if (mixed) ensure_lf32(ctx, 1);
+    const int mpm = mixed ? mp_mode(ctx) : 0;
+    if (mixed) ensure_lf32(ctx, mpm);
     const Engine& g = ctx->eng;
     const int64_t cap = g.ncol / (ctx->seed.k * ctx->seed.k);  // vectors per K1 launch (group 0 buffers)
     int* zero = nullptr;
@@ -2369,7 +2417,7 @@ static int apply_C_impl(lyap_ctx* ctx, int64_t nvec, const double* X, const doub
       a.nactive = nullptr;
       a.alist = nullptr;
       a.nver = zero;
-      launch_k1(ctx, a, st, nullptr, nullptr, 0, 0, mixed ? 1 : 0);
+      launch_k1(ctx, a, st, nullptr, nullptr, 0, 0, mpm);
       ctx->stats.k1_launches++;
       ctx->stats.k1_vectors += nb;
       if (!mixed) ctx->stats.k1_exact_vectors += nb;
@@ -2397,6 +2445,7 @@ int lyap_apply_C_mixed(lyap_ctx* ctx, int64_t nvec, const double* X, const doubl
 int lyap_get_info(const lyap_ctx* ctx, lyap_info* info) {
   if (!ctx || !info) return LYAP_EINVAL;
   *info = ctx->info;
+  info->mixed_mode = mp_mode(ctx);
   return LYAP_OK;
 }
 

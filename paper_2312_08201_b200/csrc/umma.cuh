@@ -27,17 +27,22 @@ namespace lyap {
 constexpr int UM_BM = 128, UM_BK = 32;
 constexpr int UM_A_BYTES = UM_BM * UM_BK * 4;  // one A plane per stage: 16 KB
 // BN: GEMM columns per CTA (one tcgen05.mma N), STAGES: TMA pipeline depth
-template <int BN, int STAGES, int BK = UM_BK>
+// EB: operand element bytes, 4 = TF32 (kind::tf32, 8 k per instruction), 2 = FP16 (kind::f16, 16 k per
+// instruction; 3xFP16 with power-of-two operand scaling).  BK counts elements.
+template <int BN, int STAGES, int BK = UM_BK, int EB = 4>
 struct UmCfg {
-  static constexpr int A_BYTES = UM_BM * BK * 4;                       // one A plane per stage
-  static constexpr int B_BYTES = BN * BK * 4;                          // one B plane per stage
+  static constexpr int A_BYTES = UM_BM * BK * EB;                      // one A plane per stage
+  static constexpr int B_BYTES = BN * BK * EB;                         // one B plane per stage
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-  // K-major rows of BK fp32 = 128 B (SWIZZLE_128B) or 64 B (SWIZZLE_64B); 8-row atoms
-  static constexpr uint32_t LAYOUT = BK == 32 ? 2u : 4u, SBO = 8 * BK * 4;
+  static constexpr int ROW = BK * EB;                                  // bytes per K-major smem row
+  // K-major rows of 128 B (SWIZZLE_128B) or 64 B (SWIZZLE_64B); 8-row atoms
+  static constexpr uint32_t LAYOUT = ROW == 128 ? 2u : 4u, SBO = 8 * ROW;
+  static constexpr int KI = EB == 4 ? 8 : 16;                          // k per tcgen05.mma
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;       // + alignment slack + barriers
   static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
-  // instruction descriptor: D fp32, A/B tf32, both K-major, M = 128, N = BN
-  static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+  // instruction descriptor: D fp32, A/B tf32 (2) or f16 (0), both K-major, M = 128, N = BN
+  static constexpr uint32_t FMT = EB == 4 ? 2u : 0u;
+  static constexpr uint32_t IDESC = (1u << 4) | (FMT << 7) | (FMT << 10) | ((uint32_t)(BN >> 3) << 17) |
                                     ((uint32_t)(UM_BM >> 4) << 24);
 };
 // production configuration of the persistent kernel: 128 x 256 tiles, 16-wide k-blocks (64-byte swizzle),
@@ -84,13 +89,20 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
   return d;
 }
 __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) { return umma_desc<2, 1024>(saddr); }
-template <uint32_t IDESC>
+template <uint32_t IDESC, int EB = 4>
 __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(acc));
+  if constexpr (EB == 4)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(acc));
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(acc));
 }
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
@@ -257,12 +269,12 @@ struct EpiCoord {
 // (k1_out_element, the same code as the DMMA path's fused epilogue) and writes C(v)x straight into the
 // slot's Krylov basis; the Im row of a conjugate pair comes from the neighbouring lane (shfl).  VERIFY
 // positions [0, nver) are skipped (their exact FP64 apply comes from the DMMA GEMM).  EPI = 0: U32t.
-template <int BN, int STAGES, int EPI, int BK = UM_BK>
+template <int BN, int STAGES, int EPI, int BK = UM_BK, int EB = 4>
 __global__ void __launch_bounds__(192, 1)
     k1_umma_persistent(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                        float* __restrict__ U32t, int npad, int ncol, int Kd, const int* __restrict__ nactive, int cpa,
-                       const K1EpiArgs ep, int* __restrict__ tctr) {
-  using Cfg = UmCfg<BN, STAGES, BK>;
+                       const K1EpiArgs ep, int* __restrict__ tctr, const float* __restrict__ colscale = nullptr) {
+  using Cfg = UmCfg<BN, STAGES, BK, EB>;
   constexpr int SB = Cfg::STAGE_BYTES, BB = Cfg::B_BYTES, AB = Cfg::A_BYTES, TCOLS = 2 * BN <= 256 ? 256 : 512;
   extern __shared__ __align__(1024) uint8_t um_smem[];
   const uint32_t base = (smem_u32(um_smem) + 1023) & ~1023u;
@@ -360,11 +372,11 @@ __global__ void __launch_bounds__(192, 1)
           const uint32_t ah = base + s * SB, al = ah + AB, bl = ah + 2 * AB, bh = bl + BB;
           constexpr uint32_t LY = Cfg::LAYOUT, SO = Cfg::SBO;
 #pragma unroll
-          for (int j = 0; j < BK / 8; ++j) {
-            const uint32_t o = 32 * j;  // 8 tf32 = 32 bytes along the swizzled row
-            umma_tf32<Cfg::IDESC>(td, umma_desc<LY, SO>(ah + o), umma_desc<LY, SO>(bl + o), (kb > 0 || j > 0) ? 1u : 0u);
-            umma_tf32<Cfg::IDESC>(td, umma_desc<LY, SO>(al + o), umma_desc<LY, SO>(bh + o), 1u);
-            umma_tf32<Cfg::IDESC>(td, umma_desc<LY, SO>(ah + o), umma_desc<LY, SO>(bh + o), 1u);
+          for (int j = 0; j < BK / Cfg::KI; ++j) {
+            const uint32_t o = 32 * j;  // one instruction's k (8 tf32 / 16 fp16) = 32 bytes along the swizzled row
+            umma_tf32<Cfg::IDESC, EB>(td, umma_desc<LY, SO>(ah + o), umma_desc<LY, SO>(bl + o), (kb > 0 || j > 0) ? 1u : 0u);
+            umma_tf32<Cfg::IDESC, EB>(td, umma_desc<LY, SO>(al + o), umma_desc<LY, SO>(bh + o), 1u);
+            umma_tf32<Cfg::IDESC, EB>(td, umma_desc<LY, SO>(ah + o), umma_desc<LY, SO>(bh + o), 1u);
           }
           umma_commit(empty0 + 8 * s);
         }
@@ -403,6 +415,10 @@ __global__ void __launch_bounds__(192, 1)
               "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (colscale) {  // FP16 operands: undo the power-of-two operand scales of every column (exact)
+#pragma unroll
+          for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * colscale[n0 + c0 + j]);
+        }
         if constexpr (EPI == 0) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) U32t[(int64_t)(n0 + c0 + j) * npad + m] = __uint_as_float(r[j]);

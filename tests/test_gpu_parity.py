@@ -605,7 +605,9 @@ def test_two_level_preconditioner_configs(name, p):
 @pytest.mark.parametrize("n,k,seed", [(30, 3, 0), (64, 2, 1), (13, 1, 2), (40, 4, 3),
                                       # npad a multiple of 128: the tcgen05 path (fused epilogue for
                                       # k = 1, 2, 4; k1_epi for k = 3), real eigenvalues included
-                                      (150, 2, 4), (200, 4, 5), (130, 1, 6), (140, 3, 7)])
+                                      (150, 2, 4), (200, 4, 5), (130, 1, 6), (140, 3, 7),
+                                      # npad = 256 / 384: the 3xFP16 tcgen05 path (k = 3 unfused)
+                                      (250, 3, 8), (380, 2, 9)])
 def test_mixed_precision_random(n, k, seed):
     """opts.mixed = 1: Krylov steps with the 3xTF32 T-apply, every cycle restarted from
     the exact FP64 true residual.  The stopping test is the FP64 one, so every v meets tol = 1e-12 and
@@ -646,7 +648,7 @@ def test_mixed_precision_configs(name):
     P1.close()
 
 
-@pytest.mark.parametrize("n,k,seed", [(200, 4, 0), (256, 2, 1), (150, 3, 2), (1700, 4, 3)])
+@pytest.mark.parametrize("n,k,seed", [(200, 4, 0), (256, 2, 1), (150, 3, 2), (1700, 4, 3), (250, 3, 4)])
 def test_k1_mixed_apply_against_paper_blocks(n, k, seed):
     """The mixed-precision operator (lyap_apply_C_mixed: the Cauchy part on the tcgen05 3xTF32 GEMM,
     T_d and sigma o X in FP64) against the same entrywise operator of eqs. (N1M1)/(N2M1)/(N1M2):
