@@ -53,6 +53,9 @@ struct EngArgs {
   // applied identically by k_prec and the solution update; FP64 arithmetic throughout): half the bytes
   // of the largest per-iteration stream of k_prec
   float* Minv;
+  // 3xFP16 T-apply (mixed_mode 3): per slot and parameter max |Xin_t| as float bits (the FP16 column
+  // scales of k1_gen16), zeroed by k_pfactor and accumulated by k_prec (atomicMax); null otherwise
+  unsigned int* xmaxu;
   double *part2, *Gq, *cf;  // Gram-row partials, Gram matrix Q^T Q of the basis, projection coefficients
   int *phase, *m, *vidx, *applies, *restarts, *ctrl, *newv, *alist;
   int* qctr;      // shared by all slot groups: [0] next queue position, [1] finished v's
@@ -279,6 +282,8 @@ template <int K>
 __global__ void __launch_bounds__(128) k_pfactor(EngArgs a) {
   const int slot = blockIdx.y;
   const int64_t rep = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // (k_prec of this iteration accumulates the new maxima; it runs after this kernel on the same stream)
+  if (a.xmaxu && blockIdx.x == 0 && threadIdx.x < K) a.xmaxu[slot * K + threadIdx.x] = 0u;
   if (rep >= a.nrep || !a.newv[slot]) return;
   const bool pair = rep < a.npairs;
   float* out = a.Minv + (int64_t)slot * a.nrep * pb_stride<K>() + rep;
@@ -365,6 +370,21 @@ __device__ __forceinline__ void rep_store(double* __restrict__ x, int64_t npad, 
   }
 }
 
+// 3xFP16: fold this thread's rep values of Xin into the slot's max |Xin_t| (warp max, one atomic per
+// warp and t; non-negative floats order like their bit patterns)
+template <int K>
+__device__ __forceinline__ void note_xmax(const EngArgs& a, int slot, bool pair, const double (&z)[2 * K]) {
+  if (!a.xmaxu) return;
+  const unsigned mask = __activemask();
+  const int leader = __ffs(mask) - 1;
+#pragma unroll
+  for (int t = 0; t < K; ++t) {
+    const double v = pair ? fmax(fabs(z[2 * t]), fabs(z[2 * t + 1])) : fabs(z[t]);
+    const unsigned u = __reduce_max_sync(mask, __float_as_uint(__double2float_ru(v)));
+    if ((int)(threadIdx.x & 31) == leader) atomicMax(a.xmaxu + slot * K + t, u);
+  }
+}
+
 // ---------------------------------------------------------------- apply input (K2 apply)
 // ITER: Xin = P(v)^{-1} (q^_m / eta_m);  VERIFY: Xin = X.
 template <int K, typename QT = double>
@@ -380,11 +400,10 @@ __global__ void __launch_bounds__(128) k_prec(EngArgs a) {
   double* xin = a.Xin + (int64_t)slot * a.L;
   if (ph == PH_VERIFY) {
     const double* x = a.X + (int64_t)slot * a.L;
-#pragma unroll
-    for (int t = 0; t < K; ++t) {
-      xin[t * a.npad + c] = x[t * a.npad + c];
-      if (pair) xin[t * a.npad + c + 1] = x[t * a.npad + c + 1];
-    }
+    double z[2 * K];
+    rep_load<K>(x, a.npad, c, pair, 1.0, z);
+    rep_store<K>(xin, a.npad, c, pair, z, false);
+    note_xmax<K>(a, slot, pair, z);
     return;
   }
   const int m = a.m[slot];
@@ -413,10 +432,12 @@ __global__ void __launch_bounds__(128) k_prec(EngArgs a) {
     for (int i = 0; i < 2 * K; ++i) z[i] += y[i];
     rep_store<K>(xin, a.npad, c, pair, z, false);
     rep_store<K>(a.Zb + ((int64_t)slot * (a.mmax + 1) + m) * a.L, a.npad, c, pair, z, false);
+    note_xmax<K>(a, slot, pair, z);
     return;
   }
   apply_pinv<K>(minv_of(a.Minv, slot, rep, a.nrep, pb_stride<K>()), a.nrep, pair, r, z);
   rep_store<K>(xin, a.npad, c, pair, z, false);
+  note_xmax<K>(a, slot, pair, z);
 }
 
 // ---------------------------------------------------------------- two-level preconditioner

@@ -47,9 +47,9 @@ struct K1Args {
   // FP64 apply through the DMMA GEMM), positions [*nver, *nactive) ITER slots (apply through the
   // FP32-accurate tensor-core GEMM on the float planes B32 / U32).  nver == null: all FP64.
   const int* nver;
-  // MP = 3 (3xFP16): power-of-two operand scales -- per slot and parameter t the max |X_t| (xmax, from
-  // k_xmax), per s max |B^r_s| (bmax), the exponent of Lf's scale (eA); k1_gen writes each column's
-  // unscale factor 2^-(eA + e_n) to colscale
+  // 3xFP16: power-of-two operand scales -- per slot and parameter t the max |X_t| (xmax: accumulated by
+  // k_prec in the engine, k_xmax in apply mode), per s max |B^r_s| (bmax), the exponent of Lf's scale
+  // (eA); k1_gen16 writes each column's unscale factor 2^-(eA + e_n) to colscale
   const float *xmax, *bmax;
   int eA;
   float* colscale;
@@ -95,7 +95,7 @@ template <int K, int MP = 0>
 __global__ void __launch_bounds__(256) k1_gen(K1Args a, const double* __restrict__ bhr, int npad,
                                                int two_np, double* __restrict__ Bop, int64_t ncol,
                                                float* __restrict__ B32 = nullptr) {
-  __half* B16 = reinterpret_cast<__half*>(B32);  // MP = 3: the planes in FP16
+  static_assert(MP <= 2, "3xFP16 operands: k1_gen16");
   constexpr int TS = K1Tile<K>::TS, NC = K1Tile<K>::NC, TC = K1_TILE_C;
   const int nact = k1_nact(a);
   const int nver = MP ? *a.nver : nact;
@@ -131,21 +131,77 @@ __global__ void __launch_bounds__(256) k1_gen(K1Args a, const double* __restrict
       const double val = k1_bval<K>(xs[sl][t], bs, r, s, i0 + r < two_np);
       const int64_t nn = (int64_t)(s0 + sl) * K * K + col % (K * K);
       if (s0 + sl < nver) Bop[(int64_t)(i0 + r) * ncol + nn] = val;  // FP64 operand of the exact apply
-      if constexpr (MP == 3) {
-        // column scale 2^e: the bound max|B^r_s| max|X_t| (x 1.5 for the folded complex product) -> 2^13
-        const float bound = a.bmax[s] * a.xmax[k1_slot(a, s0 + sl) * K + t] * 1.5f;
-        const int e = bound > 0.f ? 13 - (int)ceilf(log2f(bound)) : 0;
-        const double xs_ = ldexp(val, e);
-        const __half hi = __double2half(xs_);
-        B16[(ncol + nn) * npad + i0 + r] = hi;
-        B16[nn * npad + i0 + r] = __double2half(xs_ - (double)__half2float(hi));
-        if (blockIdx.x == 0 && r == 0) a.colscale[nn] = ldexpf(1.f, -(a.eA + e));
+      const float f = (float)val;
+      const float hi = MP == 1 ? tf32_rn(f) : f;
+      B32[(ncol + nn) * npad + i0 + r] = hi;
+      if (MP == 1) B32[nn * npad + i0 + r] = (float)(val - (double)hi);
+    }
+  }
+}
+
+// 3xFP16 B operand (MP = 3), one active position per blockIdx.y, two consecutive coordinates per thread
+// (a conjugate pair's (Re, Im) rows, or two real rows): every value of the pair is formed from one
+// 16-byte load of each X_t and the two B^r rows, and the hi / lo planes are written as half2, so a
+// warp stores 128 contiguous bytes per (s, t) column.  Column scale 2^e_n (e_n from max|B^r_s|
+// max|X_t|, the same bound as k1_gen<K, 3>) is formed once per block; unscale 2^-(eA + e_n) goes to
+// colscale.  The FP64 operand is written for the VERIFY positions [0, nver) only.
+constexpr int K1G16_THREADS = 256;
+template <int K>
+__global__ void __launch_bounds__(K1G16_THREADS) k1_gen16(K1Args a, const double* __restrict__ bhr, int npad,
+                                                          int two_np, double* __restrict__ Bop, int64_t ncol,
+                                                          __half* __restrict__ B16) {
+  const int pos = blockIdx.y;
+  const int nact = k1_nact(a);
+  if (pos >= nact) return;
+  const int nver = *a.nver;
+  const int slot = k1_slot(a, pos);
+  __shared__ double scl[K * K];
+  if (threadIdx.x < K * K) {
+    const int s = threadIdx.x / K, t = threadIdx.x % K;
+    const float bound = a.bmax[s] * a.xmax[slot * K + t] * 1.5f;
+    const int e = bound > 0.f ? 13 - (int)ceilf(log2f(bound)) : 0;
+    scl[threadIdx.x] = ldexp(1.0, e);
+    if (blockIdx.x == 0) a.colscale[(int64_t)pos * K * K + threadIdx.x] = ldexpf(1.f, -(a.eA + e));
+  }
+  __syncthreads();
+  const int c = 2 * (blockIdx.x * K1G16_THREADS + threadIdx.x);
+  if (c >= npad) return;
+  const double* x = a.Xin + (int64_t)slot * a.L;
+  double2 xv[K];
+#pragma unroll
+  for (int t = 0; t < K; ++t) xv[t] = *reinterpret_cast<const double2*>(x + (int64_t)t * npad + c);
+  double b0[K], b1[K];
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+    b0[s] = bhr[(int64_t)c * K + s];
+    b1[s] = bhr[(int64_t)(c + 1) * K + s];
+  }
+  const bool pair = c < two_np;
+  const int64_t nb = (int64_t)pos * K * K;
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+#pragma unroll
+    for (int t = 0; t < K; ++t) {
+      double v0, v1;
+      if (pair) {  // (br + i bi)(x + i y): Re row c, Im row c + 1
+        v0 = b0[s] * xv[t].x - b1[s] * xv[t].y;
+        v1 = b0[s] * xv[t].y + b1[s] * xv[t].x;
       } else {
-        const float f = (float)val;
-        const float hi = MP == 1 ? tf32_rn(f) : f;
-        B32[(ncol + nn) * npad + i0 + r] = hi;
-        if (MP == 1) B32[nn * npad + i0 + r] = (float)(val - (double)hi);
+        v0 = b0[s] * xv[t].x;
+        v1 = b1[s] * xv[t].y;
       }
+      const int64_t nn = nb + s * K + t;
+      if (pos < nver) {
+        Bop[(int64_t)c * ncol + nn] = v0;
+        Bop[(int64_t)(c + 1) * ncol + nn] = v1;
+      }
+      const double sc = scl[s * K + t];
+      const double y0 = v0 * sc, y1 = v1 * sc;
+      const __half h0 = __double2half(y0), h1 = __double2half(y1);
+      const __half l0 = __double2half(y0 - (double)__half2float(h0));
+      const __half l1 = __double2half(y1 - (double)__half2float(h1));
+      *reinterpret_cast<__half2*>(B16 + (ncol + nn) * npad + c) = __halves2half2(h0, h1);
+      *reinterpret_cast<__half2*>(B16 + nn * npad + c) = __halves2half2(l0, l1);
     }
   }
 }

@@ -507,13 +507,16 @@ void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, cudaEvent_t evb 
       // per-position max |X_t| first: the FP16 column scales (k1_gen) need it
       // (slot indices are local to the slot group: each group has its own xmax rows)
       float* xm = g.xmax + (size_t)group * ((g.b + g.groups - 1) / g.groups) * s.k;
-      k_xmax<KK><<<(unsigned)a.nslot, 256, 0, st>>>(a, (int)s.npad, xm);
+      // (engine mode: k_prec has already accumulated them while writing Xin)
+      if (a.mode != 1) k_xmax<KK><<<(unsigned)a.nslot, 256, 0, st>>>(a, (int)s.npad, xm);
       K1Args a3 = a;
       a3.xmax = xm;
       a3.bmax = g.bmax;
       a3.eA = ctx->basis->lf_eA;
       a3.colscale = g.colscale + (size_t)group * g.ncol;
-      k1_gen<KK, 3><<<grid, K1_THREADS, 0, st>>>(a3, s.bhr, (int)s.npad, two_np, g.Bop, g.ncol, B32);
+      dim3 g16((unsigned)((s.npad + 2 * K1G16_THREADS - 1) / (2 * K1G16_THREADS)), (unsigned)a.nslot);
+      k1_gen16<KK><<<g16, K1G16_THREADS, 0, st>>>(a3, s.bhr, (int)s.npad, two_np, g.Bop, g.ncol,
+                                                  reinterpret_cast<__half*>(B32));
     } else if (mp == 1)
       k1_gen<KK, 1><<<grid, K1_THREADS, 0, st>>>(a, s.bhr, (int)s.npad, two_np, g.Bop, g.ncol, B32);
     else if (mp == 2)
@@ -728,6 +731,8 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
     x.Qb = g.Qb ? g.Qb + s0 * ld * g.L : nullptr;
     x.Qf = g.Qf ? g.Qf + s0 * ld * g.L : nullptr;
     x.Minv = g.Minv + s0 * s.nrep * s.k * s.k * 4;
+    // (the same rows launch_k1 hands to k1_gen16: group * bg0 * k)
+    x.xmaxu = mp == 3 ? reinterpret_cast<unsigned int*>(g.xmax + s0 * s.k) : nullptr;
     x.sigma = g.sigma + s0 * s.k;
     x.mask = g.mask + s0 * s.k;
     x.eta = g.eta + s0 * ld;

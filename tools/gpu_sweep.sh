@@ -8,7 +8,7 @@ OUT=gpurun_out/${P}_sweep.log
 run() {  # run <label> <bench args...>
   local label=$1; shift
   local line
-  line=$(timeout 400 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e "$@" 2>>gpurun_out/${P}_err.log | tail -1)
+  line=$(env $ENVS timeout 400 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e "$@" 2>>gpurun_out/${P}_err.log | tail -1)
   python - "$label" "$line" >> $OUT <<'EOF'
 import json, sys
 label, line = sys.argv[1], sys.argv[2]
@@ -22,6 +22,8 @@ except Exception as e:
 EOF
 }
 for spec in "$@"; do
-  # spec: label|args
-  run "${spec%%|*}" ${spec#*|}
+  # spec: label|ENV=VAL ...|bench args
+  label=${spec%%|*}; rest=${spec#*|}
+  ENVS=${rest%%|*}; args=${rest#*|}
+  run "$label" $args
 done
