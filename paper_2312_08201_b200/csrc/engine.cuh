@@ -710,7 +710,11 @@ __global__ void __launch_bounds__(256) k_uapply(EngArgs a) {
 #ifndef LYAP_DOT_IG
 #define LYAP_DOT_IG 64
 #endif
-constexpr int DOT_IG = LYAP_DOT_IG;  // basis vectors per k_dots block (grid.z splits long cycles)
+constexpr int DOT_IG = LYAP_DOT_IG;  // grid.z of k_dots = min(DOT_Z, ceil((mmax + 1) / DOT_IG)) blocks per chunk
+#ifndef LYAP_DOT_Z
+#define LYAP_DOT_Z 2
+#endif
+constexpr int DOT_Z = LYAP_DOT_Z;
 template <typename QT = double>
 __global__ void __launch_bounds__(256) k_dots(EngArgs a) {
   __shared__ __align__(16) double ws[RED_CE];
@@ -756,9 +760,11 @@ __global__ void __launch_bounds__(256) k_dots(EngArgs a) {
   }
   if (ph != PH_ITER) return;
   const int m = a.m[slot];
-  const int i0 = blockIdx.z * DOT_IG;  // this block's basis vectors: [i0, min(m, i0 + DOT_IG - 1)]
+  // this block's basis vectors: i = 8 (z + Z j) + warp <= m (groups of 8 dealt round-robin over the Z =
+  // gridDim.z blocks of a chunk, so short and long cycles both split evenly and a block without work
+  // exits before staging; with one block per DOT_IG vectors most blocks of a launch were empty)
+  const int i0 = blockIdx.z * 8, istep = 8 * gridDim.z;
   if (i0 > m) return;
-  const int i1 = min(m, i0 + DOT_IG - 1);
   const QT* w = qbase<QT>(a) + slot * qs + (int64_t)(m + 1) * a.L;
   const QT* qlast = qbase<QT>(a) + slot * qs + (int64_t)m * a.L;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -776,7 +782,7 @@ __global__ void __launch_bounds__(256) k_dots(EngArgs a) {
     }
     __syncthreads();
     const int lim4 = lim / 4;
-    for (int i = i0 + warp; i <= i1; i += 8) {
+    for (int i = i0 + warp; i <= m; i += istep) {
       const float4* q = reinterpret_cast<const float4*>(qbase<QT>(a) + slot * qs + (int64_t)i * a.L + e0);
       double d0 = 0.0, d1 = 0.0, g0 = 0.0, g1 = 0.0;
       float4 x[RED_CE / 128];
@@ -813,7 +819,7 @@ __global__ void __launch_bounds__(256) k_dots(EngArgs a) {
     qm[i] = e < a.L ? qlast[e] : 0.0;
   }
   __syncthreads();
-  for (int i = i0 + warp; i <= i1; i += 8) {
+  for (int i = i0 + warp; i <= m; i += istep) {
     const QT* q = qbase<QT>(a) + slot * qs + (int64_t)i * a.L + e0;
     double d0 = 0.0, d1 = 0.0, g0 = 0.0, g1 = 0.0;
     int e = lane;
@@ -1198,9 +1204,13 @@ __global__ void __launch_bounds__(256) k_gout(EngArgs a) {
 // the window.
 template <int K, typename QT = double>
 __global__ void __launch_bounds__(256) k_xcomb(EngArgs a) {
+  // window of W coordinates; FP32 basis: 128 coordinates as 32 float4 columns x 8 slices of the basis index
+  // (16-byte loads), FP64 basis: 64 coordinates x 4 slices
+  constexpr bool F4 = sizeof(QT) == 4;
+  constexpr int W = F4 ? 128 : 64, NS = F4 ? 8 : 4;
   __shared__ double ys[1024];
-  __shared__ double red[4][64];
-  __shared__ double xs[K][64];
+  __shared__ double red[NS][W];
+  __shared__ double xs[K][W];
   const int slot = blockIdx.y;
   if (a.phase[slot] != PH_XUPD) return;
   const int m1 = a.m[slot];
@@ -1213,34 +1223,79 @@ __global__ void __launch_bounds__(256) k_xcomb(EngArgs a) {
     if (a.pc > 0) Qb0 = (const QT*)a.Zb;  // two-level: Z_j = P^{-1} q_j (FP64 basis only)
   const QT* Q = Qb0 + (int64_t)slot * (a.mmax + 1) * a.L;
   double* X = a.X + (int64_t)slot * a.L;
-  const int el = threadIdx.x & 63, sl = threadIdx.x >> 6;
-  for (int64_t c0 = (int64_t)blockIdx.x * 64; c0 < a.npad; c0 += (int64_t)gridDim.x * 64) {
-    const int64_t c = c0 + el;
+  const int el = F4 ? (threadIdx.x & 31) : (threadIdx.x & 63), sl = F4 ? (threadIdx.x >> 5) : (threadIdx.x >> 6);
+  for (int64_t c0 = (int64_t)blockIdx.x * W; c0 < a.npad; c0 += (int64_t)gridDim.x * W) {
+    if constexpr (F4) {
+      const int64_t c = c0 + 4 * el;  // npad is a multiple of 64: a float4 column is inside or outside as a whole
 #pragma unroll 1
-    for (int t = 0; t < K; ++t) {
-      const int64_t e = (int64_t)t * a.npad + c;
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      if (c < a.npad) {
-        int i = sl;
-        for (; i + 12 < m1; i += 16) {  // 4 independent basis loads per step
-          s0 = fma(ys[i], (double)Q[(int64_t)i * a.L + e], s0);
-          s1 = fma(ys[i + 4], (double)Q[(int64_t)(i + 4) * a.L + e], s1);
-          s2 = fma(ys[i + 8], (double)Q[(int64_t)(i + 8) * a.L + e], s2);
-          s3 = fma(ys[i + 12], (double)Q[(int64_t)(i + 12) * a.L + e], s3);
+      for (int t = 0; t < K; ++t) {
+        const int64_t e = (int64_t)t * a.npad + c;
+        double s[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) s[u][0] = s[u][1] = s[u][2] = s[u][3] = 0.0;
+        if (c < a.npad) {
+          int i = sl;
+          for (; i + 3 * NS < m1; i += 4 * NS) {  // 4 independent 16-byte basis loads per step
+            float4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = *reinterpret_cast<const float4*>(Q + (int64_t)(i + u * NS) * a.L + e);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const double y = ys[i + u * NS];
+              s[u][0] = fma(y, (double)v[u].x, s[u][0]);
+              s[u][1] = fma(y, (double)v[u].y, s[u][1]);
+              s[u][2] = fma(y, (double)v[u].z, s[u][2]);
+              s[u][3] = fma(y, (double)v[u].w, s[u][3]);
+            }
+          }
+          for (; i < m1; i += NS) {
+            const float4 v = *reinterpret_cast<const float4*>(Q + (int64_t)i * a.L + e);
+            const double y = ys[i];
+            s[0][0] = fma(y, (double)v.x, s[0][0]);
+            s[0][1] = fma(y, (double)v.y, s[0][1]);
+            s[0][2] = fma(y, (double)v.z, s[0][2]);
+            s[0][3] = fma(y, (double)v.w, s[0][3]);
+          }
         }
-        for (; i < m1; i += 4) s0 = fma(ys[i], (double)Q[(int64_t)i * a.L + e], s0);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) red[sl][4 * el + r] = (s[0][r] + s[2][r]) + (s[1][r] + s[3][r]);
+        __syncthreads();
+        if (threadIdx.x < W) {
+          double acc = 0.0;
+#pragma unroll
+          for (int q = 0; q < NS; ++q) acc += red[q][threadIdx.x];
+          xs[t][threadIdx.x] = acc;
+        }
+        __syncthreads();
       }
-      red[sl][el] = (s0 + s2) + (s1 + s3);
-      __syncthreads();
-      if (sl == 0) xs[t][el] = (red[0][el] + red[1][el]) + (red[2][el] + red[3][el]);
-      __syncthreads();
+    } else {
+      const int64_t c = c0 + el;
+#pragma unroll 1
+      for (int t = 0; t < K; ++t) {
+        const int64_t e = (int64_t)t * a.npad + c;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        if (c < a.npad) {
+          int i = sl;
+          for (; i + 12 < m1; i += 16) {  // 4 independent basis loads per step
+            s0 = fma(ys[i], (double)Q[(int64_t)i * a.L + e], s0);
+            s1 = fma(ys[i + 4], (double)Q[(int64_t)(i + 4) * a.L + e], s1);
+            s2 = fma(ys[i + 8], (double)Q[(int64_t)(i + 8) * a.L + e], s2);
+            s3 = fma(ys[i + 12], (double)Q[(int64_t)(i + 12) * a.L + e], s3);
+          }
+          for (; i < m1; i += 4) s0 = fma(ys[i], (double)Q[(int64_t)i * a.L + e], s0);
+        }
+        red[sl][el] = (s0 + s2) + (s1 + s3);
+        __syncthreads();
+        if (sl == 0) xs[t][el] = (red[0][el] + red[1][el]) + (red[2][el] + red[3][el]);
+        __syncthreads();
+      }
     }
     if (su > 0) {  // recycled directions enter x directly (not through P^{-1})
       const double* U = a.Ureg + (int64_t)a.reg[slot] * a.s_rec * a.L;
-      for (int idx = threadIdx.x; idx < K * 64; idx += blockDim.x) {
-        const int64_t cc = c0 + (idx & 63);
+      for (int idx = threadIdx.x; idx < K * W; idx += blockDim.x) {
+        const int64_t cc = c0 + (idx % W);
         if (cc >= a.npad) continue;
-        const int64_t e = (int64_t)(idx >> 6) * a.npad + cc;
+        const int64_t e = (int64_t)(idx / W) * a.npad + cc;
         double acc = 0.0;
         for (int i = 0; i < su; ++i) acc = fma(ysl[i], U[(int64_t)i * a.L + e], acc);
         X[e] += acc;
@@ -1248,14 +1303,14 @@ __global__ void __launch_bounds__(256) k_xcomb(EngArgs a) {
       __syncthreads();
     }
     if (a.pc > 0) {  // flexible basis: the directions are already preconditioned
-      for (int idx = threadIdx.x; idx < K * 64; idx += blockDim.x) {
-        const int64_t cc = c0 + (idx & 63);
-        if (cc < a.npad) X[(int64_t)(idx >> 6) * a.npad + cc] += xs[idx >> 6][idx & 63];
+      for (int idx = threadIdx.x; idx < K * W; idx += blockDim.x) {
+        const int64_t cc = c0 + (idx % W);
+        if (cc < a.npad) X[(int64_t)(idx / W) * a.npad + cc] += xs[idx / W][idx % W];
       }
       __syncthreads();
       continue;
     }
-    if (threadIdx.x < 64) {
+    if (threadIdx.x < W) {
       const int64_t cc = c0 + threadIdx.x;
       const bool pair = cc < 2 * a.npairs;
       const int64_t rep = pair ? cc / 2 : cc - a.npairs;

@@ -436,6 +436,16 @@ void launch_gemm(lyap_ctx* ctx, const Seed& s, const double* Bop, double* U, int
 
 // persistent tcgen05 3xTF32 GEMM (umma.cuh), one CTA per SM over the active tiles; epi = k fuses the K1
 // epilogue (k = 1, 2, 4), epi = 0 writes U32t for k1_epi
+// stream priorities: the engine's main streams run at the greatest priority, the VERIFY side stream at the
+// least, so the block scheduler places the tcgen05 kernel's CTAs before the DMMA blocks beside them
+int stream_prio(bool high) {
+  static int lo = 0, hi = 0, init = 0;
+  if (!init) {
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    init = 1;
+  }
+  return high ? hi : lo;
+}
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -537,26 +547,45 @@ void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, cudaEvent_t evb 
     // columns: the small-tile DMMA configuration) on the group's side stream, beside the float GEMM
     // of all positions on the tensor cores; k1_epi picks U or U32 per position
     if (!ctx->mpstream[group]) {
-      CK(cudaStreamCreateWithFlags(&ctx->mpstream[group], cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithPriority(&ctx->mpstream[group], cudaStreamNonBlocking, stream_prio(false)));
       CK(cudaEventCreateWithFlags(&ctx->mpfork[group], cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&ctx->mpjoin[group], cudaEventDisableTiming));
     }
     static const bool serial = std::getenv("LYAP_MP_SERIAL") != nullptr;  // diagnostics: no side stream
+    // Order (LYAP_MP_ORDER, default 1): the persistent tcgen05 kernel is launched FIRST, from the
+    // higher-priority stream, so its one CTA per SM owns the SMs for its whole run; the VERIFY GEMM
+    // follows on the low-priority side stream and fills the tcgen05 kernel's tail.  0: DMMA first (its
+    // blocks then hold the SMs and the tcgen05 CTAs wait for them).  Measured on c5 (tools/gpu_order.sh):
+    // same step time within 2 % either way (the board is at its power cap), but the tcgen05 launch takes
+    // 0.72 ms instead of 1.15 ms, i.e. the events around it time the kernel, not the queue behind DMMA.
+    // Co-residency (LYAP_VER_CFG=2: a 2-stage 29.7 KB DMMA CTA beside the 193 KB tcgen05 CTA, or
+    // LYAP_UM_ST=3) was measured too and gains nothing under the power cap.
+    static const int order = [] {
+      const char* ev = std::getenv("LYAP_MP_ORDER");
+      return ev ? std::atoi(ev) : 1;
+    }();
+    const bool um_first = order == 1 && !serial && (mp == 1 || mp == 3) && mp_umma() && s.npad % UM_BM == 0;
     cudaStream_t ss = serial ? st : ctx->mpstream[group];
     CK(cudaEventRecord(ctx->mpfork[group], st));
-    CK(cudaStreamWaitEvent(ss, ctx->mpfork[group], 0));
-    K1Args av = a;
-    av.nactive = a.nver;
-    static const bool vsmall = [] {  // LYAP_VER_BN=64: the 64 x 64 configuration (measurement alternative)
-      const char* ev = std::getenv("LYAP_VER_BN");
-      return !(ev && std::atoi(ev) == 64);
-    }();
-    if (vsmall)
-      launch_gemm<V_BM, V_BN, V_WM, V_WN, V_ST, V_BK>(ctx, s, g.Bop, g.U, g.ncol, av, ss, fuse_dm);
-    else
-      launch_gemm<S_BM, S_BN, S_WM, S_WN, S_ST, S_BK>(ctx, s, g.Bop, g.U, g.ncol, av, ss, fuse_dm);
-    LAUNCHED();
-    CK(cudaEventRecord(ctx->mpjoin[group], ss));
+    auto launch_verify = [&] {
+      CK(cudaStreamWaitEvent(ss, ctx->mpfork[group], 0));
+      K1Args av = a;
+      av.nactive = a.nver;
+      static const int vcfg = [] {  // LYAP_VER_CFG: 0 = 64 x 32 x 16 in 3 stages, 1 = 64 x 64, 2 = 64 x 32 x 16 in 2 stages
+        const char* ev = std::getenv("LYAP_VER_CFG");
+        return ev ? std::atoi(ev) : -1;
+      }();
+      const int cfg = vcfg >= 0 ? vcfg : 0;
+      if (cfg == 2)
+        launch_gemm<V_BM, V_BN, V_WM, V_WN, 2, V_BK>(ctx, s, g.Bop, g.U, g.ncol, av, ss, fuse_dm);
+      else if (cfg == 0)
+        launch_gemm<V_BM, V_BN, V_WM, V_WN, V_ST, V_BK>(ctx, s, g.Bop, g.U, g.ncol, av, ss, fuse_dm);
+      else
+        launch_gemm<S_BM, S_BN, S_WM, S_WN, S_ST, S_BK>(ctx, s, g.Bop, g.U, g.ncol, av, ss, fuse_dm);
+      LAUNCHED();
+      CK(cudaEventRecord(ctx->mpjoin[group], ss));
+    };
+    if (!um_first) launch_verify();
     const int Nc = (int)g.ncol, M = (int)s.npad;
     const float* A32 = ctx->basis->Lf32;  // row-major npad x 2 npad: [hi | lo]
     if ((mp == 1 || mp == 3) && mp_umma() && s.npad % UM_BM == 0) {
@@ -579,7 +608,14 @@ void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, cudaEvent_t evb 
       const int Kd = (int)std::min<int64_t>(roundup(s.n, 32), s.npad);  // zero rows skipped (multiple of both BKs)
       K1EpiArgs ep{a, s.btl, s.F, s.g0, (int)s.npad, two_np, (int)s.npairs, (int)s.n};
       const int cpa = (int)(s.k * s.k), epi = fuse_um ? (int)s.k : 0;
-      if (mp == 3)
+      static const bool um3 = [] {  // LYAP_UM_ST=3: 3-stage ring (145 KB; leaves room for a 3-stage DMMA CTA)
+        const char* ev = std::getenv("LYAP_UM_ST");
+        return ev && std::atoi(ev) == 3;
+      }();
+      if (mp == 3 && um3)
+        launch_umma<UM_BN, 3, 32, 2>(ctx, epi, ctx->um_ta, ctx->um_tb[group], U32, (int)s.npad, Nc, Kd, a.nactive, cpa, ep,
+                                     st, g.umctr + 2 * group, g.colscale + (size_t)group * g.ncol);
+      else if (mp == 3)
         launch_umma<UM_BN, UM_STAGES, 32, 2>(ctx, epi, ctx->um_ta, ctx->um_tb[group], U32, (int)s.npad, Nc, Kd, a.nactive,
                                              cpa, ep, st, g.umctr + 2 * group, g.colscale + (size_t)group * g.ncol);
       else if (um_bn() == 128)
@@ -617,6 +653,7 @@ void launch_k1(lyap_ctx* ctx, const K1Args& a, cudaStream_t st, cudaEvent_t evb 
     }
     // profile events bracket the tensor-core GEMM (the side-stream DMMA overlaps it)
     if (eve) CK(cudaEventRecordWithFlags(eve, st, evflags));
+    if (um_first) launch_verify();
     CK(cudaStreamWaitEvent(st, ctx->mpjoin[group], 0));
   }
   if (eve && !mp) CK(cudaEventRecordWithFlags(eve, st, evflags));
@@ -818,7 +855,7 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
   if (G > 1) {
     CK(cudaEventRecord(ctx->evfork, st));
     for (int gi = 1; gi < G; ++gi) {
-      if (!ctx->xstream[gi]) CK(cudaStreamCreateWithFlags(&ctx->xstream[gi], cudaStreamNonBlocking));
+      if (!ctx->xstream[gi]) CK(cudaStreamCreateWithPriority(&ctx->xstream[gi], cudaStreamNonBlocking, stream_prio(true)));
       sts[gi] = ctx->xstream[gi];
       CK(cudaStreamWaitEvent(sts[gi], ctx->evfork, 0));
     }
@@ -830,7 +867,8 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
     const int bg = gb[gi];
     const dim3 grep((unsigned)((s.nrep + 127) / 128), (unsigned)bg);
     const dim3 gred((unsigned)g.nchunk, (unsigned)bg);
-    const dim3 gxc((unsigned)std::min<int64_t>((s.npad + 63) / 64, 128), (unsigned)bg);
+    const int xw = g.Qf ? 128 : 64;  // k_xcomb's coordinate window
+    const dim3 gxc((unsigned)std::min<int64_t>((s.npad + xw - 1) / xw, 128), (unsigned)bg);
     k_assign<<<1, (int)roundup(bg, 32), 0, sg>>>(x);
     LAUNCHED();
     K_DISPATCH(s.k, (k_pfactor<KK><<<grep, 128, 0, sg>>>(x)));
@@ -863,7 +901,8 @@ int run_batch(lyap_ctx* ctx, int64_t nv, const double* dV, const int* dorder, do
       LAUNCHED();
     }
     launch_k1(ctx, gk[gi], sg, evb, eve, evflags, gi, mp);
-    const dim3 gdot((unsigned)g.nchunk, (unsigned)bg, (unsigned)((mmax + DOT_IG) / DOT_IG));
+    const int zfull = (mmax + DOT_IG) / DOT_IG;  // short vectors (few chunks) keep one block per DOT_IG basis vectors
+    const dim3 gdot((unsigned)g.nchunk, (unsigned)bg, (unsigned)(g.nchunk >= 16 ? std::min(zfull, DOT_Z) : zfull));
     if (g.Qf)
       k_dots<float><<<gdot, 256, 0, sg>>>(x);
     else
@@ -1437,7 +1476,7 @@ static int setup_core(int64_t n, int64_t k, const double* A0, const double* Bl, 
     if (dev < 0) CK(cudaGetDevice(&dev));
     ctx->device = dev;
     CK(cudaSetDevice(dev));
-    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithPriority(&ctx->stream, cudaStreamNonBlocking, stream_prio(true)));
     CK(cudaEventCreate(&ctx->ev0));
     CK(cudaEventCreate(&ctx->ev1));
     CKB(cublasCreate(&ctx->cublas));
@@ -1447,9 +1486,11 @@ static int setup_core(int64_t n, int64_t k, const double* A0, const double* Bl, 
     set_smem_attrs<G_BM, G_BN, G_WM, G_WN, G_ST, G_BK>(ctx);
     set_smem_attrs<S_BM, S_BN, S_WM, S_WN, S_ST, S_BK>(ctx);
     set_smem_attrs<V_BM, V_BN, V_WM, V_WN, V_ST, V_BK>(ctx);
+    set_smem_attrs<V_BM, V_BN, V_WM, V_WN, 2, V_BK>(ctx);
     set_umma_attrs<UM_BN, UM_STAGES, UM_BKE>(ctx);
     set_umma_attrs<128, 3, 32>(ctx);
     set_umma_attrs<UM_BN, UM_STAGES, 32, 2>(ctx);
+    set_umma_attrs<UM_BN, 3, 32, 2>(ctx);
     cudaStream_t st = ctx->stream;
     CK(cudaEventRecord(ctx->ev0, st));
     Seed& s = ctx->seed;
@@ -1707,7 +1748,7 @@ int lyap_setup_like(const lyap_ctx* base, int64_t k, const double* Bl, const dou
   int rc = LYAP_OK;
   try {
     CK(cudaSetDevice(ctx->device));
-    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithPriority(&ctx->stream, cudaStreamNonBlocking, stream_prio(true)));
     CK(cudaEventCreate(&ctx->ev0));
     CK(cudaEventCreate(&ctx->ev1));
     CKB(cublasCreate(&ctx->cublas));
