@@ -147,8 +147,8 @@ def test_sharded_sweep_real_engine(name, mixed):
     """two ranks (gloo, both on cuda:0) running the real engine on their cost-balanced
     shards against a single-rank run of the whole grid.  FP64 engine, recycling off: BITWISE (every v
     starts from x = 0 and every reduction has a fixed order, so a trace does not depend on the batch it
-    was solved in).  Mixed precision: the 3xFP16 operand scales are taken per slot group, so a trace may
-    depend on its batch-mates at rounding level: <= 1e-10 relative, same argmin."""
+    was solved in).  Mixed precision: bitwise equality across batches is not claimed
+    (refinement cycles end on thresholds): <= 1e-10 relative, same argmin."""
     import socket
 
     import torch.multiprocessing as mp
