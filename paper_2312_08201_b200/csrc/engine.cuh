@@ -212,8 +212,9 @@ __device__ __forceinline__ constexpr int pb_stride() { return 4 * K * K; }
 
 // Minv[slot][rep] = P(v)_rep^{-1} by in-place Gauss-Jordan with partial pivoting (rows swapped
 // during elimination, the matching columns of the inverse swapped back at the end).
-// out: element (r, c) of the inverse at out[(r * 2K + c) * ostride] (Minv is element-major across the
-// reps of a slot, so the threads of a warp -- consecutive reps -- read and write coalesced)
+// out: element e = r * 2K + c of the inverse at out[(e / 4) * ostride * 4 + e % 4]: Minv is stored in groups
+// of four elements, group-major across the reps of a slot, so the threads of a warp -- consecutive reps --
+// read and write consecutive float4 (16-byte accesses instead of 64 scalar ones per block at k = 4)
 template <int D, int K>
 __device__ __forceinline__ void invert_block(const double* __restrict__ pb, const double* mask, const double* sigma,
                                              float* __restrict__ out, int64_t ostride) {
@@ -266,15 +267,22 @@ __device__ __forceinline__ void invert_block(const double* __restrict__ pb, cons
         M[r][p] = t;
       }
   }
+  // elements e = r * 2K + c in groups of four: group g of rep at out[g * ostride * 4 .. + 3] (one 16-byte store)
 #pragma unroll
-  for (int r = 0; r < D; ++r)
+  for (int g = 0; g < ((D - 1) * RS + D - 1) / 4 + 1; ++g) {
+    float v[4];
 #pragma unroll
-    for (int c = 0; c < D; ++c) out[(int64_t)(r * RS + c) * ostride] = (float)M[r][c];
+    for (int q = 0; q < 4; ++q) {
+      const int e = 4 * g + q, r = e / RS, c = e % RS;
+      v[q] = (r < D && c < D) ? (float)M[r < D ? r : 0][c < D ? c : 0] : 0.f;
+    }
+    *reinterpret_cast<float4*>(out + (int64_t)g * ostride * 4) = make_float4(v[0], v[1], v[2], v[3]);
+  }
 }
 
-// the Minv block of (slot, rep): element e at minv_of(...)[e * nrep]
+// the Minv block of (slot, rep): element e at minv_of(...)[(e / 4) * nrep * 4 + e % 4]
 __device__ __forceinline__ const float* minv_of(const float* Minv, int64_t slot, int64_t rep, int64_t nrep, int S) {
-  return Minv + slot * nrep * S + rep;
+  return Minv + slot * nrep * S + rep * 4;
 }
 
 // One thread per (slot with a new v, rep): factor the rep's block; a cold start zeroes X there.
@@ -286,7 +294,7 @@ __global__ void __launch_bounds__(128) k_pfactor(EngArgs a) {
   if (a.xmaxu && blockIdx.x == 0 && threadIdx.x < K) a.xmaxu[slot * K + threadIdx.x] = 0u;
   if (rep >= a.nrep || !a.newv[slot]) return;
   const bool pair = rep < a.npairs;
-  float* out = a.Minv + (int64_t)slot * a.nrep * pb_stride<K>() + rep;
+  float* out = a.Minv + (int64_t)slot * a.nrep * pb_stride<K>() + rep * 4;
   const double* pb = a.Pb + rep * pb_stride<K>();
   if (pair)
     invert_block<2 * K, K>(pb, a.mask + slot * K, a.sigma + slot * K, out, a.nrep);
@@ -324,19 +332,33 @@ __device__ __forceinline__ void apply_pinv(const float* __restrict__ mi, int64_t
                                            const double (&r)[2 * K], double (&z)[2 * K]) {
   constexpr int RS = 2 * K;
   if (pair) {
+    float m[4 * K * K];
+#pragma unroll
+    for (int g = 0; g < K * K; ++g) {
+      const float4 v = *reinterpret_cast<const float4*>(mi + (int64_t)g * st * 4);
+      m[4 * g] = v.x, m[4 * g + 1] = v.y, m[4 * g + 2] = v.z, m[4 * g + 3] = v.w;
+    }
 #pragma unroll
     for (int i = 0; i < 2 * K; ++i) {
       double acc = 0.0;
 #pragma unroll
-      for (int j = 0; j < 2 * K; ++j) acc = fma((double)mi[(i * RS + j) * st], r[j], acc);
+      for (int j = 0; j < 2 * K; ++j) acc = fma((double)m[i * RS + j], r[j], acc);
       z[i] = acc;
     }
   } else {
+    // real rep: the top-left K x K block (row stride 2K), i.e. the groups up to element (K - 1) * 2K + K - 1
+    constexpr int NG = ((K - 1) * RS + K - 1) / 4 + 1;
+    float m[4 * NG];
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+      const float4 v = *reinterpret_cast<const float4*>(mi + (int64_t)g * st * 4);
+      m[4 * g] = v.x, m[4 * g + 1] = v.y, m[4 * g + 2] = v.z, m[4 * g + 3] = v.w;
+    }
 #pragma unroll
     for (int i = 0; i < K; ++i) {
       double acc = 0.0;
 #pragma unroll
-      for (int j = 0; j < K; ++j) acc = fma((double)mi[(i * RS + j) * st], r[j], acc);
+      for (int j = 0; j < K; ++j) acc = fma((double)m[i * RS + j], r[j], acc);
       z[i] = acc;
     }
   }
