@@ -171,17 +171,36 @@ void free_engine(Engine& g, bool keep_order = true) {
   }
 }
 
+int mp_mode(const lyap_ctx* ctx);
+int auto_mmax(const lyap_ctx* ctx);
 int auto_batch(const lyap_ctx* ctx, int64_t nv) {
   const Seed& s = ctx->seed;
   int b = ctx->opts.batch;
   if (b <= 0) {
     // two slot groups, each aiming for ~8 waves of K1 tiles (16 for the small-tile config) on 148
     // SMs, but at least ~4 v per slot so the cost-ordered queue can balance the slots
+    // Mixed precision (one slot group, every kernel of an iteration fills the GPU): wider batches amortise
+    // the per-iteration latency and the tile tails of both GEMMs; measured on c5 (tools/gpu_smallshard.sh):
+    // 4096 v: b = 448 / 592 / 768 / 1024 -> 1108 / 1082 / 1049 / 1037 ms; a 512-v shard: b = 128 / 256 / 384 ->
+    // 208 / 196 / 204 ms.  Hence up to 1024 slots and at least 256 (or all v).
+    const bool mp = mp_mode(ctx) != 0;
     const int64_t mt = s.npad / tile_m(s);
-    const int64_t waves = s.n <= SMALL_N ? 16 * 148 : 8 * 148;
+    const int64_t waves = (s.n <= SMALL_N || mp) ? 16 * 148 : 8 * 148;
     const int64_t target_cols = (waves + mt - 1) / mt * tile_n(s);
     const int64_t per_group = std::max<int64_t>(32, std::min<int64_t>(1024, target_cols / (s.k * s.k)));
-    b = (int)std::min<int64_t>(2 * per_group, std::max<int64_t>(64, nv / 4));
+    b = (int)std::min<int64_t>(2 * per_group, std::max<int64_t>(mp ? 256 : 64, nv / 4));
+    // HBM budget: the Krylov basis ((mmax + 1) vectors of L elements per slot, FP32 under mixed precision)
+    // dominates; with the per-slot operands, iterates and preconditioner blocks (~80 L bytes) the engine
+    // takes at most 70 % of the memory that is free now or already held by this context's engine
+    // (queried only when the estimate exceeds 16 GB: small problems never pay for the query)
+    size_t fr = 0, tot = 0;
+    const double L = (double)s.npad * s.k;
+    const double per_slot = (auto_mmax(ctx) + 1) * L * (mp ? 4.0 : 8.0) + 80.0 * L;
+    if (b * per_slot > 16e9 && b > ctx->eng.bcap && cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
+      const double held = (double)ctx->eng.bcap * per_slot;
+      const int64_t cap = (int64_t)(0.7 * ((double)fr + held) / per_slot);
+      if (cap >= 1 && b > cap) b = (int)cap;
+    }
   }
   b = (int)std::min<int64_t>(b, std::max<int64_t>(nv, 1));
   b = std::max(1, std::min(b, 2048));  // <= 1024 per slot group (k_assign is one block)
