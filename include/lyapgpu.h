@@ -232,8 +232,9 @@ int lyap_apply_C(lyap_ctx* ctx, int64_t nvec, const double* X, const double* sig
                  void* cuda_stream);
 
 /* As lyap_apply_C, with the dense Cauchy part of T (eqs. (N2M1)/(N1M2)) applied in
- * 3xTF32 on the tcgen05 tensor cores -- the operator of the mixed-precision Krylov steps (DESIGN.md
- * §2.8); T_d and sigma o X stay FP64.  Relative error ~1e-5 of the Cauchy sums (not an exact apply).
+ * three reduced-precision passes on the tcgen05 tensor cores (3xFP16 with power-of-two operand scales when
+ * npad is a multiple of 128, else 3xTF32; lyap_info.mixed_mode) -- the operator of the mixed-precision
+ * Krylov steps; T_d and sigma o X stay FP64.  Relative error ~1e-5 of the Cauchy sums (not an exact apply).
  * Requires mixed precision on for ctx (opts.mixed = 1, or auto with n > 1536): else LYAP_EINVAL. */
 int lyap_apply_C_mixed(lyap_ctx* ctx, int64_t nvec, const double* X, const double* sigma, double* Y,
                        void* cuda_stream);
